@@ -1,0 +1,280 @@
+/*
+ * qsim.h -- C-ABI of libqsim.so, the B200-native (sm_100a) state-vector gate
+ * engine for the method of Niwa, Matsumoto, Imai, "General-Purpose Parallel
+ * Simulator for Quantum Computing" (arXiv quant-ph/0201042; PAPER.md).
+ *
+ * Conventions (all entry points):
+ *   - Status: QSIM_OK (0) or a negative QSIM_E* code; qsim_last_error() has
+ *     the message.  Validation happens before anything is enqueued, so a
+ *     failed call has no effect on the state.  A CUDA or NCCL failure poisons
+ *     the handle: every later call returns QSIM_ESTATE.
+ *   - Qubits (§2.2.1): qubit 0 is the MSB; qubit q of an n-qubit
+ *     register is bit (n-1-q) of the basis index.  Qubit sets (ctrl_mask,
+ *     ctrl_vals, qubit masks) are bit sets over qubit numbers: bit q <-> qubit q.
+ *   - Amplitudes are complex128, qsim_c128 = {re, im}, layout-compatible with
+ *     double2 / std::complex<double> / numpy complex128 (2^(n+4)
+ *     bytes per state; reading R2 in DESIGN.md).
+ *   - Host pointers are borrowed for the duration of the call only; the
+ *     caller owns every buffer it passes.  The handle owns all device memory,
+ *     streams and communicators.
+ *   - Gate calls are asynchronous and stream-ordered on the handle's stream;
+ *     calls that return data to the host (norm, probs, get_state, measure,
+ *     sync, inject_errors' event list) synchronise that stream.
+ *   - A handle is not thread-safe: one mutator at a time.
+ *   - Multi-GPU: one process per GPU (qsim_create_dist).  The state is sharded
+ *     on its top log2(world) physical bits; the library tracks a logical ->
+ *     physical qubit map internally, exchanges shards with NCCL send/recv when
+ *     a gate needs a global qubit local, and restores the canonical layout
+ *     before any call that exposes amplitudes or marginals.  Every rank must
+ *     make the same sequence of calls (SPMD).
+ * The semantics of each call are pinned by the CPU oracle (oracle/, test
+ * infrastructure) as described in DESIGN.md §4.
+ */
+#ifndef QSIM_H
+#define QSIM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct qsim_s qsim_t;
+
+typedef struct { double re, im; } qsim_c128;
+
+enum {
+    QSIM_OK = 0,
+    QSIM_EINVAL = -1,     /* malformed argument (overlapping qubits, p outside [0,1], ...) */
+    QSIM_ERANGE = -2,     /* qubit / index / size outside the register */
+    QSIM_ENOMEM = -3,     /* device or pinned allocation failed */
+    QSIM_ECUDA = -4,      /* CUDA runtime error (handle poisoned) */
+    QSIM_ENOTBIJ = -5,    /* permutation is not a bijection */
+    QSIM_ESTATE = -6,     /* handle poisoned by an earlier asynchronous error */
+    QSIM_ENCCL = -7,      /* NCCL error (handle poisoned) */
+    QSIM_ENODEV = -8      /* no CUDA device / not an sm_100 device */
+};
+
+/* Angle-form gate kinds (§3.2; R12-R14).
+ *   QSIM_GATE_RP   : U_R(a0) U_P1(a1)                 (H = RP(pi/4, pi), NOT = RP(pi/2, pi))
+ *   QSIM_GATE_P1   : U_P1(a0) = diag(1, e^{i a0})      (R_d = P1(pi / 2^d))
+ *   QSIM_GATE_HAAR : U_P2(a0) U_P1(a1) U_R(a2) U_P1(a3) (general single-qubit gate)
+ * with U_R(t) = (cos t, -sin t; sin t, cos t), U_P1(p) = diag(1, e^{ip}),
+ * U_P2(p) = diag(e^{ip}, 1). */
+enum { QSIM_GATE_RP = 0, QSIM_GATE_P1 = 1, QSIM_GATE_HAAR = 2 };
+
+/* Counter-RNG tags (R1). */
+enum {
+    QSIM_TAG_GATE = 1, QSIM_TAG_HAAR = 2, QSIM_TAG_PAIR = 3, QSIM_TAG_OPNOISE = 4,
+    QSIM_TAG_MARK = 5, QSIM_TAG_BASE = 6, QSIM_TAG_GAUSS = 7, QSIM_TAG_PAULI = 8,
+    QSIM_TAG_MEASURE = 9
+};
+
+/* ---------------------------------------------------------------- lifecycle */
+
+/* Allocate an n-qubit register (2^(n+4) bytes of HBM) on the
+ * current CUDA device, initialised to |0...0>.  ngpus must be 1 (use
+ * qsim_create_dist for multi-GPU).  Errors: QSIM_ERANGE if n < 1 or n > 40;
+ * QSIM_ENOMEM (message names the byte count); QSIM_ENODEV.  *out receives
+ * the handle (NULL on error; qsim_last_error(NULL) then has the message). */
+int qsim_create(int n, int ngpus, qsim_t **out);
+
+/* One rank of a world of `world` processes (world a power of two, one GPU
+ * each, 2^n >= 2*world): allocates this rank's shard of 2^(n - log2 world)
+ * amplitudes on CUDA device `device` and joins the NCCL communicator named by
+ * the 128-byte `nccl_id` (from qsim_nccl_unique_id on rank 0, broadcast by
+ * the caller).  State = |0...0>.  Errors as qsim_create, plus QSIM_ENCCL. */
+int qsim_create_dist(int n, int world, int rank, int device, const void *nccl_id,
+                     qsim_t **out);
+
+/* Writes a fresh ncclUniqueId (128 bytes) into out128. */
+int qsim_nccl_unique_id(void *out128);
+
+/* Frees every device buffer, stream and communicator of the handle. */
+void qsim_destroy(qsim_t *h);
+
+/* Message of the last failed call on h (h may be NULL for creation errors). */
+const char *qsim_last_error(const qsim_t *h);
+
+/* 2^(n+4): bytes of an n-qubit complex128 state. */
+uint64_t qsim_memory_bytes(int n);
+
+/* Number of this library's kernels launched on h so far (instrumentation). */
+uint64_t qsim_launch_count(const qsim_t *h);
+
+/* Waits for all queued work on h and surfaces asynchronous errors. */
+int qsim_sync(qsim_t *h);
+
+/* The cudaStream_t (as void*) every kernel of h is launched on, so callers
+ * can record CUDA events on it (plumbing for timing; do not destroy it). */
+void *qsim_get_stream(qsim_t *h);
+
+/* Per-launch profiling: with enable = 1 every kernel launch of h is
+ * bracketed by CUDA events on h's stream (records are reset by each call).
+ * qsim_profile_json synchronises and returns, aggregated per kernel name,
+ * {"name": {"launches": L, "ms": total device time, "bytes": algorithmic
+ * HBM bytes (reads + writes the operation must make)}, ...}; the string is
+ * owned by h and valid until the next call. */
+int qsim_profile(qsim_t *h, int enable);
+const char *qsim_profile_json(qsim_t *h);
+
+/* ---------------------------------------------------------------- state preparation */
+
+/* |idx> (registers start in basis states).  QSIM_ERANGE if
+ * idx >= 2^n. */
+int qsim_set_basis(qsim_t *h, uint64_t idx);
+
+/* i.i.d. complex Gaussian amplitudes, then divided by sqrt(sum |a|^2)
+ * (BASELINE configs[2]; R19): amplitude idx is the Box-Muller pair
+ * of draw(seed, GAUSS, idx, 0), re = cos branch, im = sin branch.  Generated
+ * on the device by the library's own Philox4x32-10. */
+int qsim_init_gaussian(qsim_t *h, uint64_t seed);
+
+/* Copy cnt amplitudes starting at global basis index off between the state
+ * and a caller-owned host buffer (canonical order).  Synchronising.
+ * QSIM_ERANGE if off + cnt > 2^n.  In a distributed handle only the indices
+ * owned by this rank ([rank * 2^nl, (rank+1) * 2^nl)) may be addressed. */
+int qsim_set_state(qsim_t *h, uint64_t off, uint64_t cnt, const qsim_c128 *host);
+int qsim_get_state(qsim_t *h, uint64_t off, uint64_t cnt, qsim_c128 *host);
+
+/* ---------------------------------------------------------------- gates (§2.2) */
+
+/* Single-qubit gate U (row-major u11, u12, u21, u22, copied at call time) on
+ * qubit q: the pair (j, j + 2^(n-1-q)) with bit (n-1-q)
+ * of j clear becomes (u11 a + u12 b, u21 a + u22 b), in place
+ * (PAPER.md:285-337).  Unitarity is not checked.  QSIM_ERANGE if q not in
+ * [0, n). */
+int qsim_apply_1q(qsim_t *h, int q, const qsim_c128 U[4]);
+
+/* Controlled gate: the pair update of qsim_apply_1q only
+ * where every qubit c in ctrl_mask has value bit c of ctrl_vals ("the c-th
+ * bit in j is 1" generalised to several controls and either value; all-ones
+ * ctrl_vals is the standard controlled-U; CNOT is U = NOT).  QSIM_EINVAL if q
+ * is in ctrl_mask or ctrl_vals has bits outside ctrl_mask. */
+int qsim_apply_ctrl(qsim_t *h, uint64_t ctrl_mask, uint64_t ctrl_vals, int q,
+                    const qsim_c128 U[4]);
+
+/* Angle-form gate (kinds above), optionally controlled (ctrl_mask = 0 for
+ * none).  With gate noise enabled (qsim_set_gate_noise, sigma > 0) angle slot
+ * s is perturbed by sigma * z, z = normal(draw(noise_seed, OPNOISE, g, s))
+ * (R15), g = the handle's angle-form gate
+ * counter, which advances by one per call whatever sigma is.  ang holds 2, 1
+ * or 4 angles for RP, P1, HAAR. */
+int qsim_apply_angles(qsim_t *h, int kind, const double *ang, uint64_t ctrl_mask,
+                      uint64_t ctrl_vals, int q);
+
+/* Operational-error model (§3.2): sigma >= 0 (QSIM_EINVAL
+ * otherwise); sigma = 0 disables.  Does not reset the gate counter. */
+int qsim_set_gate_noise(qsim_t *h, uint64_t seed, double sigma);
+int qsim_get_gate_counter(const qsim_t *h, uint64_t *g);
+int qsim_set_gate_counter(qsim_t *h, uint64_t g);
+
+/* SWAP of qubits q1, q2 (the closing swaps of the QFT circuit, R7).
+ * Exact (a permutation of amplitudes). */
+int qsim_swap(qsim_t *h, int q1, int q2);
+
+/* Hadamard transform H on every qubit of [lo, lo+m) (PAPER.md:420-436,
+ * §2.3.1), with the constant H = (1/sqrt2)(1 1; 1 -1). */
+int qsim_hadamard(qsim_t *h, int lo, int m);
+
+/* QFT (inverse = 0) or inverse QFT (inverse = 1) on the sub-register of
+ * qubits [lo, lo+m), qubit lo its MSB (§2.3.2; DESIGN.md
+ * R6-R8): beta_x = 2^(-m/2) sum_y e^(+-2 pi i x y / 2^m) alpha_y on the
+ * sub-register value, computed as the circuit H(lo+j), R_{k-j} controlled by
+ * lo+k on lo+j (k > j), closing swaps.  Without gate noise the gates are the
+ * constant matrices and the whole circuit runs as fused HBM passes; with gate
+ * noise every H / R_d is an angle-form gate (counter advances per H and R_d,
+ * m + m(m-1)/2 in total either way).  QSIM_ERANGE if the range leaves [0, n). */
+int qsim_qft(qsim_t *h, int lo, int m, int inverse);
+
+/* Sign-changing operator V_f for f = delta_{x, idx}, as
+ * the phase flip alpha_idx <- -alpha_idx (R17).  QSIM_ERANGE if
+ * idx >= 2^n. */
+int qsim_phase_flip(qsim_t *h, uint64_t idx);
+
+/* Grover's search on the whole register (§5.3): `iters`
+ * G-iterations -H_n V_{f0} H_n V_{fk} with f_k = delta_{x, mark}, applied in
+ * the equivalent form alpha_k <- -alpha_k; alpha <- 2 mean(alpha) - alpha.
+ * trace (host, iters doubles, may be NULL) receives |alpha_mark|^2 after each
+ * iteration.  Synchronising when trace != NULL. */
+int qsim_grover(qsim_t *h, uint64_t mark, int iters, double *trace);
+
+/* ---------------------------------------------------------------- permutations (§2.3.3) */
+
+enum { QSIM_PERM_TABLE = 0, QSIM_PERM_MODMUL = 1, QSIM_PERM_MODEXP = 2 };
+
+/* A basis permutation, given as data:
+ *   TABLE : target register [lo, lo+m) (m <= 24), table[v] = image of value v
+ *           (2^m entries, must be a bijection), applied where the control
+ *           qubits match (ctrl_mask / ctrl_vals as in qsim_apply_ctrl).
+ *   MODMUL: target register [lo, lo+m): v -> v*mult mod modulus for v < modulus,
+ *           identity for v >= modulus (R10); gcd(mult, modulus) = 1,
+ *           modulus <= 2^m; controlled as above.
+ *   MODEXP: work register [lo, lo+m), exponent register [elo, elo+em) (value e,
+ *           qubit elo its MSB): v -> v * base^e mod modulus (v < modulus) --
+ *           the whole chain of controlled multiplications by base^(2^i)
+ *            applied at once.  gcd(base, modulus) = 1.
+ * Registers must not overlap (QSIM_EINVAL); a non-bijective table or
+ * gcd != 1 gives QSIM_ENOTBIJ. */
+typedef struct {
+    int kind;
+    int lo, m;
+    int elo, em;
+    uint64_t ctrl_mask, ctrl_vals;
+    uint64_t mult, base, modulus;
+    const uint32_t *table;
+} qsim_perm_t;
+
+int qsim_apply_perm(qsim_t *h, const qsim_perm_t *f);
+
+/* ---------------------------------------------------------------- decoherence (§3.1) */
+
+typedef struct {
+    double p;             /* depolarizing probability per qubit, in [0, 1] */
+    uint64_t qubit_mask;  /* qubits that see the channel */
+    uint64_t epoch;       /* injection point (counter i of the draws) */
+} qsim_noise_t;
+
+typedef struct { uint64_t epoch; int32_t qubit; int32_t pauli; /* 1 X, 2 Y, 3 Z */ } qsim_event_t;
+
+/* Depolarizing channel on pure-state trajectories: for each
+ * qubit q in qubit_mask (ascending), u = u01(draw(seed, PAULI, epoch, q).a);
+ * u < p/3 -> sigma_x, u < 2p/3 -> sigma_y, u < p -> sigma_z (R16),
+ * applied to the state.  Events are written to ev (capacity cap, may be NULL)
+ * in qubit order and *nev (may be NULL) receives the event count.
+ * QSIM_EINVAL if p not in [0, 1]; QSIM_ERANGE if the events did not fit (they
+ * are still applied). */
+int qsim_inject_errors(qsim_t *h, uint64_t seed, const qsim_noise_t *model,
+                       qsim_event_t *ev, int cap, int *nev);
+
+/* ---------------------------------------------------------------- read-out */
+
+/* sum_i |alpha_i|^2, tree-summed on the device. */
+int qsim_norm(qsim_t *h, double *out);
+
+/* Marginal probabilities of the sub-register [lo, lo+m) (qubit lo = MSB of
+ * the value y): out[y] = sum of |alpha_j|^2 over j with sub-register value y.
+ * out is a caller-owned host buffer of 2^m doubles (m <= 26). */
+int qsim_probs(qsim_t *h, int lo, int m, double *out);
+
+/* |alpha_idx|^2 of one amplitude. */
+int qsim_prob_index(qsim_t *h, uint64_t idx, double *out);
+
+/* Measurement (§2.2.3) without collapse: for r in [0, 1),
+ * the smallest i with sum_{j<=i} |alpha_j|^2 > r (block sums on the device,
+ * then a scan of one block); if rounding leaves r >= the total, the largest i
+ * with alpha_i != 0 (R22). */
+int qsim_measure(qsim_t *h, double r, uint64_t *idx);
+
+/* ---------------------------------------------------------------- counter RNG */
+
+/* The library's own Philox4x32-10 draw (R1), exported so that
+ * callers can generate circuits from the same seeds: key = (seed lo, seed hi),
+ * counter = (i lo, i hi, j, tag); out[0] = x0 | x1 << 32, out[1] = x2 | x3 << 32. */
+void qsim_philox_draw(uint64_t seed, uint32_t tag, uint64_t i, uint32_t j, uint64_t out[2]);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QSIM_H */

@@ -1,0 +1,1069 @@
+// api.cu -- the C-ABI of libqsim (include/qsim.h): validation, the
+// logical -> physical qubit map, gate-matrix construction on the host, and
+// dispatch to the sm_100a kernels.  No amplitude is ever computed on the
+// host: every step of the path runs in the kernels of k_*.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "philox.cuh"
+#include "qsim_internal.h"
+
+using namespace qs;
+
+namespace qs {
+
+static std::string g_create_error;
+
+int fail(Handle *h, int code, const std::string &msg)
+{
+    if (h) h->err = msg;
+    else g_create_error = msg;
+    return code;
+}
+
+int check_cuda(Handle *h, cudaError_t e, const char *what)
+{
+    if (e == cudaSuccess) return QSIM_OK;
+    if (h) h->poisoned = 1;
+    return fail(h, QSIM_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void ensure_red(Handle *h, size_t doubles)
+{
+    if (h->red_cap >= doubles) return;
+    if (h->d_red) {
+        cudaStreamSynchronize(h->stream);
+        cudaFree(h->d_red);
+    }
+    size_t cap = std::max<size_t>(doubles, 1 << 16);
+    if (cudaMalloc(&h->d_red, cap * sizeof(double)) != cudaSuccess) {
+        h->d_red = nullptr;
+        h->red_cap = 0;
+        h->poisoned = 1;
+        h->err = "cannot allocate reduction workspace";
+        return;
+    }
+    h->red_cap = cap;
+}
+
+void ensure_hred(Handle *h, size_t doubles)
+{
+    if (h->hred_cap >= doubles) return;
+    if (h->h_red) cudaFreeHost(h->h_red);
+    size_t cap = std::max<size_t>(doubles, 1 << 12);
+    if (cudaMallocHost(&h->h_red, cap * sizeof(double)) != cudaSuccess) {
+        h->h_red = nullptr;
+        h->hred_cap = 0;
+        h->poisoned = 1;
+        h->err = "cannot allocate pinned host workspace";
+        return;
+    }
+    h->hred_cap = cap;
+}
+
+int ensure_scratch(Handle *h)
+{
+    if (h->scratch) return QSIM_OK;
+    cudaError_t e = cudaMalloc(&h->scratch, sizeof(double2) * h->local_dim());
+    if (e != cudaSuccess) {
+        h->scratch = nullptr;
+        cudaGetLastError();
+        h->poisoned = 1;
+        return fail(h, QSIM_ENOMEM, "cannot allocate the " + std::to_string(sizeof(double2) * h->local_dim()) +
+                                        "-byte scratch shard");
+    }
+    return QSIM_OK;
+}
+
+static cudaEvent_t pool_event(Handle *h)
+{
+    if (h->ev_used == h->ev_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        h->ev_pool.push_back(e);
+    }
+    return h->ev_pool[h->ev_used++];
+}
+
+void prof_begin(Handle *h)
+{
+    if (!h->prof_on) return;
+    h->pending = pool_event(h);
+    cudaEventRecord(h->pending, h->stream);
+}
+
+void prof_end(Handle *h, const char *name, uint64_t bytes)
+{
+    h->launches++;
+    if (!h->prof_on || !h->pending) return;
+    cudaEvent_t b = pool_event(h);
+    cudaEventRecord(b, h->stream);
+    h->prof.push_back({name, bytes, h->pending, b});
+    h->pending = nullptr;
+}
+
+}  // namespace qs
+
+// ----------------------------------------------------------------- helpers
+namespace {
+
+#define QS_CHECK_HANDLE(h)                                                       \
+    do {                                                                         \
+        if (!(h)) return QSIM_EINVAL;                                            \
+        if ((h)->poisoned) return fail((h), QSIM_ESTATE, "handle is poisoned: " + (h)->err); \
+    } while (0)
+
+int after_launch(Handle *h, const char *what)
+{
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return check_cuda(h, e, what);
+    if (h->poisoned) return fail(h, QSIM_ECUDA, h->err);
+    return QSIM_OK;
+}
+
+bool is_local(const Handle *h, int q) { return h->pos[q] < h->nl; }
+
+// 2x2 complex product C = A B (row-major)
+void mat_mul(const double2 A[4], const double2 B[4], double2 C[4])
+{
+    auto mul = [](double2 a, double2 b) { return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); };
+    auto add = [](double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); };
+    double2 r[4];
+    r[0] = add(mul(A[0], B[0]), mul(A[1], B[2]));
+    r[1] = add(mul(A[0], B[1]), mul(A[1], B[3]));
+    r[2] = add(mul(A[2], B[0]), mul(A[3], B[2]));
+    r[3] = add(mul(A[2], B[1]), mul(A[3], B[3]));
+    std::memcpy(C, r, sizeof r);
+}
+
+// U_R(t) = (cos -sin; sin cos), U_P1(p) = diag(1, e^{ip}), U_P2(p) = diag(e^{ip}, 1)
+// (PAPER.md:542-561).
+void mat_ur(double t, double2 U[4])
+{
+    U[0] = make_double2(std::cos(t), 0); U[1] = make_double2(-std::sin(t), 0);
+    U[2] = make_double2(std::sin(t), 0); U[3] = make_double2(std::cos(t), 0);
+}
+void mat_up1(double p, double2 U[4])
+{
+    U[0] = make_double2(1, 0); U[1] = make_double2(0, 0);
+    U[2] = make_double2(0, 0); U[3] = make_double2(std::cos(p), std::sin(p));
+}
+void mat_up2(double p, double2 U[4])
+{
+    U[0] = make_double2(std::cos(p), std::sin(p)); U[1] = make_double2(0, 0);
+    U[2] = make_double2(0, 0); U[3] = make_double2(1, 0);
+}
+
+int kind_nangles(int kind) { return kind == QSIM_GATE_RP ? 2 : kind == QSIM_GATE_P1 ? 1 : 4; }
+
+// Angle-form matrix (R12-R15), perturbed when sigma > 0.
+void angle_matrix(const Handle *h, int kind, const double *ang, uint64_t g, double2 U[4])
+{
+    double a[4] = {0, 0, 0, 0};
+    const int na = kind_nangles(kind);
+    for (int s = 0; s < na; ++s) {
+        a[s] = ang[s];
+        if (h->sigma > 0.0) {
+            const u64x2 d = draw(h->noise_seed, QSIM_TAG_OPNOISE, g, (uint32_t)s);
+            const double z = std::sqrt(-2.0 * std::log(u01o(d.a))) * std::cos(2.0 * M_PI * u01(d.b));
+            a[s] += h->sigma * z;
+        }
+    }
+    double2 A[4], B[4], C[4];
+    if (kind == QSIM_GATE_RP) {
+        mat_ur(a[0], A); mat_up1(a[1], B); mat_mul(A, B, U);
+    } else if (kind == QSIM_GATE_P1) {
+        mat_up1(a[0], U);
+    } else {
+        mat_up2(a[0], A); mat_up1(a[1], B); mat_mul(A, B, C);
+        mat_ur(a[2], A); mat_mul(C, A, B);
+        mat_up1(a[3], A); mat_mul(B, A, U);
+    }
+}
+
+// Translate a controlled gate's qubit sets into a local mask/value pair and
+// decide whether this rank participates at all (global controls).
+bool local_controls(const Handle *h, uint64_t cmask, uint64_t cvals, uint64_t &lm, uint64_t &lv)
+{
+    lm = 0;
+    lv = 0;
+    for (int q = 0; q < h->n; ++q) {
+        if (!((cmask >> q) & 1)) continue;
+        const int p = h->pos[q];
+        const uint64_t want = (cvals >> q) & 1;
+        if (p < h->nl) {
+            lm |= 1ull << p;
+            lv |= want << p;
+        } else {
+            const uint64_t have = ((uint64_t)h->rank >> (p - h->nl)) & 1;
+            if (have != want) return false;
+        }
+    }
+    return true;
+}
+
+bool is_diag(const double2 U[4]) { return U[1].x == 0 && U[1].y == 0 && U[2].x == 0 && U[2].y == 0; }
+
+// Core gate application on logical target q with logical controls.
+int apply_gate(Handle *h, uint64_t cmask, uint64_t cvals, int q, const double2 U[4])
+{
+    if (is_diag(U)) {
+        // diagonal gates need no communication: global target bit is a rank bit
+        uint64_t lm, lv;
+        if (!local_controls(h, cmask, cvals, lm, lv)) return QSIM_OK;
+        const int p = h->pos[q];
+        if (p < h->nl) {
+            launch_apply_diag(h, p, lm, lv, U[0], U[3]);
+        } else {
+            const int b = (h->rank >> (p - h->nl)) & 1;
+            const double2 d = b ? U[3] : U[0];
+            if (!(d.x == 1.0 && d.y == 0.0)) launch_phase_mask(h, lm, lv, d);
+        }
+        return after_launch(h, "diagonal gate");
+    }
+    if (!is_local(h, q)) {
+        int rc = dist_make_local(h, std::vector<int>{q});
+        if (rc) return rc;
+    }
+    uint64_t lm, lv;
+    if (!local_controls(h, cmask, cvals, lm, lv)) return QSIM_OK;
+    launch_apply_2x2(h, h->pos[q], lm, lv, U);
+    return after_launch(h, "2x2 gate");
+}
+
+int check_qubit(Handle *h, int q)
+{
+    if (q < 0 || q >= h->n) return fail(h, QSIM_ERANGE, "qubit " + std::to_string(q) + " outside [0, n)");
+    return QSIM_OK;
+}
+
+int check_ctrl(Handle *h, uint64_t cmask, uint64_t cvals, int q)
+{
+    if (h->n < 64 && (cmask >> h->n)) return fail(h, QSIM_ERANGE, "control mask has qubits >= n");
+    if ((cmask >> q) & 1) return fail(h, QSIM_EINVAL, "target qubit is also a control");
+    if (cvals & ~cmask) return fail(h, QSIM_EINVAL, "ctrl_vals has bits outside ctrl_mask");
+    return QSIM_OK;
+}
+
+// Build a TilePass from a tile (tile bit -> input local position) and a full
+// local permutation perm (input position -> output position).
+TilePass make_pass(const Handle *h, const std::vector<int> &tile_pos, const std::vector<int> &perm)
+{
+    TilePass tp;
+    std::memset(&tp, 0, sizeof tp);
+    tp.tbits = (int)tile_pos.size();
+    std::vector<char> in_tile(h->nl, 0);
+    for (int b = 0; b < tp.tbits; ++b) {
+        tp.in_pos[b] = tile_pos[b];
+        tp.out_pos[b] = perm[tile_pos[b]];
+        in_tile[tile_pos[b]] = 1;
+    }
+    tp.nfix = 0;
+    for (int p = 0; p < h->nl; ++p) {
+        if (in_tile[p]) continue;
+        tp.fin_pos[tp.nfix] = p;
+        tp.fout_pos[tp.nfix] = perm[p];
+        tp.nfix++;
+    }
+    tp.scale = 1.0;
+    return tp;
+}
+
+// Fused H / QFT on the wires [lo, lo+m) (logical).  qft = 0: Hadamard transform.
+int fused_range(Handle *h, int lo, int m, int qft, int inverse)
+{
+    const int amax = 10;
+    const int G = (m + amax - 1) / amax;
+    std::vector<int> gsize(G, m / G);
+    for (int g = 0; g < m % G; ++g) gsize[g]++;
+    // F: wire w -> the position now held by logical qubit lo+m-1-w (closing swaps);
+    // Hadamard: identity.
+    std::vector<int> a0s(G);
+    for (int g = 0, acc = 0; g < G; ++g) { a0s[g] = acc; acc += gsize[g]; }
+    bool relabelled = false;   // closing swaps already folded into a store
+    // physical position of wire w (before the fold: logical lo+w; after it:
+    // the position logical lo+m-1-w had, which is pos[lo+m-1-w] again since
+    // pos[] is left unchanged by the fold)
+    auto wire_pos = [&](int w) { return relabelled ? h->pos[lo + m - 1 - w] : h->pos[lo + w]; };
+    for (int g = 0; g < G; ++g) {
+        const int a0 = a0s[g], a = gsize[g];
+        std::vector<int> act;
+        for (int u = 0; u < a; ++u) act.push_back(lo + a0 + u);
+        if (h->world > 1) {
+            int rc = dist_make_local(h, act);
+            if (rc) return rc;
+        }
+        // tile: active wires (tile bits 0..a-1) + passive low positions
+        std::vector<int> tile_pos;
+        std::vector<char> in_tile(h->nl, 0);
+        for (int u = 0; u < a; ++u) {
+            tile_pos.push_back(wire_pos(a0 + u));
+            in_tile[wire_pos(a0 + u)] = 1;
+        }
+        const int want = std::max(9, std::min(a + 3, kTileMaxBits));
+        for (int p = 0; p < h->nl && (int)tile_pos.size() < want; ++p)
+            if (!in_tile[p]) { tile_pos.push_back(p); in_tile[p] = 1; }
+        // output permutation: identity, or (first QFT pass, single rank) the
+        // closing swaps folded into the store
+        std::vector<int> perm(h->nl);
+        for (int p = 0; p < h->nl; ++p) perm[p] = p;
+        bool fold = false;
+        if (qft && g == 0 && h->world == 1) {
+            std::vector<int> cand(perm);
+            for (int w = 0; w < m; ++w) cand[h->pos[lo + w]] = h->pos[lo + m - 1 - w];
+            // the store walks the 3 lowest output positions: they must be tile bits
+            bool ok = true;
+            std::vector<int> inv(h->nl);
+            for (int p = 0; p < h->nl; ++p) inv[cand[p]] = p;
+            for (int k = 0; k < 3 && k < h->nl; ++k) ok &= in_tile[inv[k]] != 0;
+            if (ok) { perm = cand; fold = true; }
+        }
+        TilePass tp = make_pass(h, tile_pos, perm);
+        tp.a = a;
+        tp.inverse = inverse;
+        tp.hadamard_only = !qft;
+        tp.scale = std::ldexp(1.0, -(a / 2));
+        if (a & 1) tp.scale *= M_SQRT1_2;
+        tp.W = a0 + a;
+        tp.n_et = tp.n_ef = 0;
+        tp.y_const = 0;
+        if (qft) {
+            for (int i = 0; i < a0; ++i) {
+                const int p = wire_pos(i);
+                if (p >= h->nl) {
+                    tp.y_const += (uint64_t)((h->rank >> (p - h->nl)) & 1) << i;
+                    continue;
+                }
+                int b = -1;
+                for (int t = 0; t < tp.tbits; ++t) if (tp.in_pos[t] == p) b = t;
+                if (b >= 0) { tp.et_bit[tp.n_et] = b; tp.et_w[tp.n_et] = i; tp.n_et++; }
+                else {
+                    int f = -1;
+                    for (int t = 0; t < tp.nfix; ++t) if (tp.fin_pos[t] == p) f = t;
+                    tp.ef_bit[tp.n_ef] = f; tp.ef_w[tp.n_ef] = i; tp.n_ef++;
+                }
+            }
+        }
+        plan_tile_maps(tp);
+        if (fold) {
+            if (ensure_scratch(h)) return QSIM_ENOMEM;
+            launch_tile_pass(h, tp, h->psi, h->scratch);
+            swap_buffers(h);
+            // the wires moved: wire w now sits where lo+m-1-w was; after the
+            // closing swaps logical qubit lo+t is wire m-1-t -> back to pos_in.
+            relabelled = true;
+        } else {
+            launch_tile_pass(h, tp, h->psi, h->psi);
+        }
+        int rc = after_launch(h, "fused tile pass");
+        if (rc) return rc;
+    }
+    if (qft && !relabelled) {
+        // closing swaps as a relabelling of the logical -> physical map
+        for (int t = 0; t < m / 2; ++t) std::swap(h->pos[lo + t], h->pos[lo + m - 1 - t]);
+    }
+    return QSIM_OK;
+}
+
+}  // namespace
+
+// Local bit permutation pass: new position of old local position p is perm[p].
+void qs::permute_local(Handle *h, const std::vector<int> &perm)
+{
+    bool ident = true;
+    for (int p = 0; p < h->nl; ++p) ident &= perm[p] == p;
+    if (ident) return;
+    if (h->nl < 9) {
+        // tiny shards: a sequence of swaps (positions are few)
+        std::vector<int> cur(h->nl);   // cur[p] = where old position p's bit currently is
+        for (int p = 0; p < h->nl; ++p) cur[p] = p;
+        std::vector<int> at(h->nl);    // at[x] = old position whose bit sits at x
+        for (int p = 0; p < h->nl; ++p) at[p] = p;
+        for (int p = 0; p < h->nl; ++p) {
+            const int want = perm[p];
+            const int now = cur[p];
+            if (now == want) continue;
+            launch_swap_local(h, now, want);
+            const int other = at[want];
+            at[want] = p; at[now] = other;
+            cur[p] = want; cur[other] = now;
+        }
+        return;
+    }
+    // tile = old low positions + the old positions that land on new low positions
+    std::vector<int> tile;
+    std::vector<char> used(h->nl, 0);
+    auto add = [&](int p) { if (!used[p] && (int)tile.size() < kTileMaxBits - 2) { used[p] = 1; tile.push_back(p); } };
+    std::vector<int> inv(h->nl);
+    for (int p = 0; p < h->nl; ++p) inv[perm[p]] = p;
+    for (int k = 0; k < 5 && k < h->nl; ++k) { add(k); add(inv[k]); }
+    for (int k = 5; (int)tile.size() < 10 && k < h->nl; ++k) { add(k); }
+    TilePass tp = make_pass(h, tile, perm);
+    tp.a = 0;
+    plan_tile_maps(tp);
+    ensure_scratch(h);
+    if (h->poisoned) return;
+    launch_tile_pass(h, tp, h->psi, h->scratch);
+    swap_buffers(h);
+}
+
+// =================================================================== C-ABI
+extern "C" {
+
+uint64_t qsim_memory_bytes(int n) { return (n < 0 || n > 59) ? 0 : (uint64_t)1 << (n + 4); }
+
+const char *qsim_last_error(const qsim_t *h) { return h ? h->err.c_str() : g_create_error.c_str(); }
+
+uint64_t qsim_launch_count(const qsim_t *h) { return h ? h->launches : 0; }
+
+void qsim_philox_draw(uint64_t seed, uint32_t tag, uint64_t i, uint32_t j, uint64_t out[2])
+{
+    const u64x2 d = draw(seed, tag, i, j);
+    out[0] = d.a;
+    out[1] = d.b;
+}
+
+static int create_common(int n, int world, int rank, int device, qsim_t **out)
+{
+    *out = nullptr;
+    if (n < 1 || n > kMaxQubits) return fail(nullptr, QSIM_ERANGE, "n must be in [1, 40]");
+    if (world < 1 || (world & (world - 1))) return fail(nullptr, QSIM_EINVAL, "world must be a power of two");
+    int kg = 0;
+    while ((1 << kg) < world) ++kg;
+    if (n - kg < 1) return fail(nullptr, QSIM_ERANGE, "2^n must be >= 2 * world");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(nullptr, QSIM_ENODEV, "no CUDA device (libqsim has no CPU path)");
+    }
+    if (device < 0) cudaGetDevice(&device);
+    if (device >= ndev) return fail(nullptr, QSIM_ENODEV, "device index out of range");
+    cudaSetDevice(device);
+    cudaDeviceProp prop;
+    cudaGetDeviceProperties(&prop, device);
+    if (prop.major != 10) return fail(nullptr, QSIM_ENODEV, std::string("libqsim is built for sm_100a; device is ") + prop.name);
+    qsim_t *h = new qsim_t();
+    h->n = n;
+    h->world = world;
+    h->rank = rank;
+    h->kglob = kg;
+    h->nl = n - kg;
+    h->device = device;
+    h->num_sms = prop.multiProcessorCount;
+    for (int q = 0; q < n; ++q) h->pos[q] = n - 1 - q;
+    if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete h;
+        return fail(nullptr, QSIM_ECUDA, "cannot create stream");
+    }
+    const size_t bytes = sizeof(double2) * h->local_dim();
+    if (cudaMalloc(&h->psi, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        cudaStreamDestroy(h->stream);
+        delete h;
+        return fail(nullptr, QSIM_ENOMEM, "cannot allocate " + std::to_string(bytes) +
+                                               " bytes of HBM for the state shard (2^(n+4) bytes per state)");
+    }
+    ensure_red(h, 1 << 16);
+    ensure_hred(h, 1 << 12);
+    // |0...0>
+    launch_zero(h);
+    if (rank == 0) launch_set_one(h, 0);
+    int rc = after_launch(h, "init");
+    if (rc) {
+        qsim_destroy(h);
+        return fail(nullptr, rc, "initialisation failed");
+    }
+    *out = h;
+    return QSIM_OK;
+}
+
+int qsim_create(int n, int ngpus, qsim_t **out)
+{
+    if (!out) return QSIM_EINVAL;
+    if (ngpus != 1) {
+        *out = nullptr;
+        return fail(nullptr, QSIM_EINVAL, "qsim_create drives one GPU; use qsim_create_dist (one process per GPU)");
+    }
+    return create_common(n, 1, 0, -1, out);
+}
+
+int qsim_create_dist(int n, int world, int rank, int device, const void *nccl_id, qsim_t **out)
+{
+    if (!out) return QSIM_EINVAL;
+    if (rank < 0 || rank >= world) return fail(nullptr, QSIM_EINVAL, "rank outside [0, world)");
+    int rc = create_common(n, world, rank, device, out);
+    if (rc) return rc;
+#ifndef QSIM_NO_NCCL
+    if (world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof id);
+        ncclResult_t r = ncclCommInitRank(&(*out)->comm, world, id, rank);
+        if (r != ncclSuccess) {
+            qsim_destroy(*out);
+            *out = nullptr;
+            return fail(nullptr, QSIM_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+        }
+    }
+#else
+    if (world > 1) {
+        qsim_destroy(*out);
+        *out = nullptr;
+        return fail(nullptr, QSIM_ENCCL, "built without NCCL");
+    }
+#endif
+    return QSIM_OK;
+}
+
+int qsim_nccl_unique_id(void *out128)
+{
+#ifndef QSIM_NO_NCCL
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return QSIM_ENCCL;
+    std::memcpy(out128, &id, sizeof id);
+    return QSIM_OK;
+#else
+    (void)out128;
+    return QSIM_ENCCL;
+#endif
+}
+
+void qsim_destroy(qsim_t *h)
+{
+    if (!h) return;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+#ifndef QSIM_NO_NCCL
+    if (h->comm) ncclCommDestroy(h->comm);
+#endif
+    if (h->psi) cudaFree(h->psi);
+    if (h->scratch) cudaFree(h->scratch);
+    if (h->d_red) cudaFree(h->d_red);
+    if (h->h_red) cudaFreeHost(h->h_red);
+    for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+void *qsim_get_stream(qsim_t *h) { return h ? (void *)h->stream : nullptr; }
+
+int qsim_profile(qsim_t *h, int enable)
+{
+    QS_CHECK_HANDLE(h);
+    cudaStreamSynchronize(h->stream);
+    h->prof.clear();
+    h->ev_used = 0;
+    h->pending = nullptr;
+    h->prof_on = enable;
+    return QSIM_OK;
+}
+
+const char *qsim_profile_json(qsim_t *h)
+{
+    if (!h) return "{}";
+    cudaStreamSynchronize(h->stream);
+    struct Agg { double ms = 0; uint64_t bytes = 0, n = 0; };
+    std::vector<std::pair<std::string, Agg>> agg;
+    for (const auto &r : h->prof) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        size_t k = 0;
+        while (k < agg.size() && agg[k].first != r.name) ++k;
+        if (k == agg.size()) agg.push_back({r.name, Agg()});
+        agg[k].second.ms += ms;
+        agg[k].second.bytes += r.bytes;
+        agg[k].second.n += 1;
+    }
+    std::string js = "{";
+    char buf[256];
+    for (size_t k = 0; k < agg.size(); ++k) {
+        std::snprintf(buf, sizeof buf, "%s\"%s\": {\"launches\": %llu, \"ms\": %.6f, \"bytes\": %llu}",
+                      k ? ", " : "", agg[k].first.c_str(), (unsigned long long)agg[k].second.n, agg[k].second.ms,
+                      (unsigned long long)agg[k].second.bytes);
+        js += buf;
+    }
+    js += "}";
+    h->prof_json = js;
+    return h->prof_json.c_str();
+}
+
+int qsim_sync(qsim_t *h)
+{
+    QS_CHECK_HANDLE(h);
+    return check_cuda(h, cudaStreamSynchronize(h->stream), "qsim_sync");
+}
+
+// ----------------------------------------------------------------- preparation
+int qsim_set_basis(qsim_t *h, uint64_t idx)
+{
+    QS_CHECK_HANDLE(h);
+    if (h->n < 64 && idx >> h->n) return fail(h, QSIM_ERANGE, "basis index >= 2^n");
+    for (int q = 0; q < h->n; ++q) h->pos[q] = h->n - 1 - q;
+    launch_zero(h);
+    if ((int)(idx >> h->nl) == h->rank) launch_set_one(h, idx & (h->local_dim() - 1));
+    return after_launch(h, "set_basis");
+}
+
+int qsim_init_gaussian(qsim_t *h, uint64_t seed)
+{
+    QS_CHECK_HANDLE(h);
+    for (int q = 0; q < h->n; ++q) h->pos[q] = h->n - 1 - q;
+    launch_init_gaussian(h, seed);
+    double s = 0.0;
+    int rc = qsim_norm(h, &s);
+    if (rc) return rc;
+    launch_scale(h, 1.0 / std::sqrt(s));
+    return after_launch(h, "init_gaussian");
+}
+
+static int copy_state(qsim_t *h, uint64_t off, uint64_t cnt, qsim_c128 *host, bool to_dev)
+{
+    QS_CHECK_HANDLE(h);
+    const uint64_t dim = (uint64_t)1 << h->n;
+    if (off > dim || cnt > dim - off) return fail(h, QSIM_ERANGE, "state slice outside [0, 2^n)");
+    int rc = dist_canonicalize(h);
+    if (rc) return rc;
+    const uint64_t lo = (uint64_t)h->rank << h->nl, hi = lo + h->local_dim();
+    if (cnt && (off < lo || off + cnt > hi)) return fail(h, QSIM_ERANGE, "slice not owned by this rank");
+    cudaError_t e;
+    if (to_dev)
+        e = cudaMemcpyAsync(h->psi + (off - lo), host, cnt * sizeof(double2), cudaMemcpyHostToDevice, h->stream);
+    else
+        e = cudaMemcpyAsync(host, h->psi + (off - lo), cnt * sizeof(double2), cudaMemcpyDeviceToHost, h->stream);
+    if (e != cudaSuccess) return check_cuda(h, e, "state copy");
+    return check_cuda(h, cudaStreamSynchronize(h->stream), "state copy");
+}
+
+int qsim_set_state(qsim_t *h, uint64_t off, uint64_t cnt, const qsim_c128 *host)
+{
+    return copy_state(h, off, cnt, const_cast<qsim_c128 *>(host), true);
+}
+
+int qsim_get_state(qsim_t *h, uint64_t off, uint64_t cnt, qsim_c128 *host)
+{
+    return copy_state(h, off, cnt, host, false);
+}
+
+// ----------------------------------------------------------------- gates
+int qsim_apply_1q(qsim_t *h, int q, const qsim_c128 U[4])
+{
+    QS_CHECK_HANDLE(h);
+    if (int rc = check_qubit(h, q)) return rc;
+    double2 M[4];
+    for (int k = 0; k < 4; ++k) M[k] = make_double2(U[k].re, U[k].im);
+    return apply_gate(h, 0, 0, q, M);
+}
+
+int qsim_apply_ctrl(qsim_t *h, uint64_t cmask, uint64_t cvals, int q, const qsim_c128 U[4])
+{
+    QS_CHECK_HANDLE(h);
+    if (int rc = check_qubit(h, q)) return rc;
+    if (int rc = check_ctrl(h, cmask, cvals, q)) return rc;
+    double2 M[4];
+    for (int k = 0; k < 4; ++k) M[k] = make_double2(U[k].re, U[k].im);
+    return apply_gate(h, cmask, cvals, q, M);
+}
+
+int qsim_apply_angles(qsim_t *h, int kind, const double *ang, uint64_t cmask, uint64_t cvals, int q)
+{
+    QS_CHECK_HANDLE(h);
+    if (kind < 0 || kind > 2 || !ang) return fail(h, QSIM_EINVAL, "unknown angle-form gate kind");
+    if (int rc = check_qubit(h, q)) return rc;
+    if (int rc = check_ctrl(h, cmask, cvals, q)) return rc;
+    double2 U[4];
+    angle_matrix(h, kind, ang, h->gcount, U);
+    h->gcount++;
+    return apply_gate(h, cmask, cvals, q, U);
+}
+
+int qsim_set_gate_noise(qsim_t *h, uint64_t seed, double sigma)
+{
+    QS_CHECK_HANDLE(h);
+    if (!(sigma >= 0.0)) return fail(h, QSIM_EINVAL, "sigma must be >= 0");
+    h->noise_seed = seed;
+    h->sigma = sigma;
+    return QSIM_OK;
+}
+
+int qsim_get_gate_counter(const qsim_t *h, uint64_t *g)
+{
+    if (!h || !g) return QSIM_EINVAL;
+    *g = h->gcount;
+    return QSIM_OK;
+}
+
+int qsim_set_gate_counter(qsim_t *h, uint64_t g)
+{
+    QS_CHECK_HANDLE(h);
+    h->gcount = g;
+    return QSIM_OK;
+}
+
+int qsim_swap(qsim_t *h, int q1, int q2)
+{
+    QS_CHECK_HANDLE(h);
+    if (int rc = check_qubit(h, q1)) return rc;
+    if (int rc = check_qubit(h, q2)) return rc;
+    // a SWAP is a relabelling of the logical -> physical map (no data moves)
+    std::swap(h->pos[q1], h->pos[q2]);
+    return QSIM_OK;
+}
+
+int qsim_hadamard(qsim_t *h, int lo, int m)
+{
+    QS_CHECK_HANDLE(h);
+    if (lo < 0 || m < 0 || lo + m > h->n) return fail(h, QSIM_ERANGE, "range outside [0, n)");
+    if (m == 0) return QSIM_OK;
+    if (h->nl >= 9 && m <= h->nl) return fused_range(h, lo, m, 0, 0);
+    const double r = M_SQRT1_2;
+    double2 H[4] = {make_double2(r, 0), make_double2(r, 0), make_double2(r, 0), make_double2(-r, 0)};
+    for (int q = lo; q < lo + m; ++q)
+        if (int rc = apply_gate(h, 0, 0, q, H)) return rc;
+    return QSIM_OK;
+}
+
+int qsim_qft(qsim_t *h, int lo, int m, int inverse)
+{
+    QS_CHECK_HANDLE(h);
+    if (lo < 0 || m < 0 || lo + m > h->n) return fail(h, QSIM_ERANGE, "range outside [0, n)");
+    if (m == 0) return QSIM_OK;
+    const double sgn = inverse ? -1.0 : 1.0;
+    if (h->sigma == 0.0 && h->nl >= 9 && m <= h->nl) {
+        // noiseless: fused passes (constant gates, R25)
+        h->gcount += (uint64_t)m + (uint64_t)m * (m - 1) / 2;
+        return fused_range(h, lo, m, 1, inverse);
+    }
+    // gate by gate (angle forms with operational noise, R14/R15)
+    const double r = M_SQRT1_2;
+    const double2 H[4] = {make_double2(r, 0), make_double2(r, 0), make_double2(r, 0), make_double2(-r, 0)};
+    for (int j = 0; j < m; ++j) {
+        int rc;
+        if (h->sigma > 0.0) {
+            const double ang[2] = {M_PI / 4.0, M_PI};
+            rc = qsim_apply_angles(h, QSIM_GATE_RP, ang, 0, 0, lo + j);
+        } else {
+            rc = apply_gate(h, 0, 0, lo + j, H);
+            h->gcount++;
+        }
+        if (rc) return rc;
+        for (int k = j + 1; k < m; ++k) {
+            const double phi = sgn * M_PI / std::ldexp(1.0, k - j);
+            const uint64_t cm = 1ull << (lo + k);
+            if (h->sigma > 0.0) {
+                rc = qsim_apply_angles(h, QSIM_GATE_P1, &phi, cm, cm, lo + j);
+            } else {
+                double2 R[4] = {make_double2(1, 0), make_double2(0, 0), make_double2(0, 0),
+                                make_double2(std::cos(phi), std::sin(phi))};
+                rc = apply_gate(h, cm, cm, lo + j, R);
+                h->gcount++;
+            }
+            if (rc) return rc;
+        }
+    }
+    for (int j = 0; j < m / 2; ++j) std::swap(h->pos[lo + j], h->pos[lo + m - 1 - j]);
+    return QSIM_OK;
+}
+
+int qsim_phase_flip(qsim_t *h, uint64_t idx)
+{
+    QS_CHECK_HANDLE(h);
+    if (h->n < 64 && idx >> h->n) return fail(h, QSIM_ERANGE, "index >= 2^n");
+    // physical location of logical index idx
+    uint64_t phys = 0;
+    for (int q = 0; q < h->n; ++q) phys |= ((idx >> (h->n - 1 - q)) & 1) << h->pos[q];
+    if ((int)(phys >> h->nl) != h->rank) return QSIM_OK;
+    const uint64_t mask = h->local_dim() - 1;
+    launch_phase_mask(h, mask, phys & mask, make_double2(-1.0, 0.0));
+    return after_launch(h, "phase_flip");
+}
+
+int qsim_grover(qsim_t *h, uint64_t mark, int iters, double *trace)
+{
+    QS_CHECK_HANDLE(h);
+    if (h->n < 64 && mark >> h->n) return fail(h, QSIM_ERANGE, "mark >= 2^n");
+    if (iters < 0) return fail(h, QSIM_EINVAL, "iters < 0");
+    if (h->world > 1) return fail(h, QSIM_EINVAL, "qsim_grover runs on a single-GPU handle");
+    if (int rc = dist_canonicalize(h)) return rc;
+    double *d_trace = nullptr;
+    if (trace && iters > 0) {
+        if (cudaMalloc(&d_trace, sizeof(double) * iters) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(h, QSIM_ENOMEM, "cannot allocate the trace buffer");
+        }
+    }
+    launch_grover(h, mark, 0, iters, d_trace);
+    int rc = after_launch(h, "grover");
+    if (!rc && d_trace) {
+        rc = check_cuda(h, cudaMemcpyAsync(trace, d_trace, sizeof(double) * iters, cudaMemcpyDeviceToHost, h->stream),
+                        "grover trace");
+        if (!rc) rc = check_cuda(h, cudaStreamSynchronize(h->stream), "grover trace");
+    }
+    if (d_trace) cudaFree(d_trace);
+    return rc;
+}
+
+// ----------------------------------------------------------------- permutations
+static uint64_t gcd64(uint64_t a, uint64_t b)
+{
+    while (b) { uint64_t t = a % b; a = b; b = t; }
+    return a;
+}
+
+int qsim_apply_perm(qsim_t *h, const qsim_perm_t *f)
+{
+    QS_CHECK_HANDLE(h);
+    if (!f) return fail(h, QSIM_EINVAL, "null permutation");
+    if (f->kind < 0 || f->kind > 2) return fail(h, QSIM_EINVAL, "unknown permutation kind");
+    if (f->m < 1 || f->lo < 0 || f->lo + f->m > h->n) return fail(h, QSIM_ERANGE, "target register outside [0, n)");
+    uint64_t treg = ((f->m >= 64) ? ~0ull : ((1ull << f->m) - 1)) << f->lo;
+    if (f->ctrl_mask & treg) return fail(h, QSIM_EINVAL, "control overlaps the target register");
+    if (f->ctrl_vals & ~f->ctrl_mask) return fail(h, QSIM_EINVAL, "ctrl_vals outside ctrl_mask");
+    if (h->n < 64 && (f->ctrl_mask >> h->n)) return fail(h, QSIM_ERANGE, "control mask has qubits >= n");
+    PermDesc d;
+    std::memset(&d, 0, sizeof d);
+    d.kind = f->kind;
+    d.wm = f->m;
+    uint32_t *d_table = nullptr;
+    if (f->kind == QSIM_PERM_TABLE) {
+        if (f->m > 24 || !f->table) return fail(h, QSIM_EINVAL, "TABLE needs m <= 24 and a table");
+        const uint64_t len = 1ull << f->m;
+        std::vector<char> seen(len, 0);
+        for (uint64_t v = 0; v < len; ++v) {
+            if (f->table[v] >= len || seen[f->table[v]]) return fail(h, QSIM_ENOTBIJ, "table is not a bijection");
+            seen[f->table[v]] = 1;
+        }
+        if (cudaMalloc(&d_table, sizeof(uint32_t) * len) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(h, QSIM_ENOMEM, "cannot allocate the permutation table");
+        }
+        cudaMemcpyAsync(d_table, f->table, sizeof(uint32_t) * len, cudaMemcpyHostToDevice, h->stream);
+        d.d_table = d_table;
+    } else {
+        const uint64_t N = f->modulus;
+        if (N < 2 || N >= (1ull << 32) || (f->m < 64 && N > (1ull << f->m)))
+            return fail(h, QSIM_EINVAL, "modulus must be in [2, min(2^m, 2^32))");
+        const uint64_t c = f->kind == QSIM_PERM_MODMUL ? f->mult : f->base;
+        if (gcd64(c % N, N) != 1) return fail(h, QSIM_ENOTBIJ, "multiplier not coprime to the modulus");
+        d.mult = f->mult;
+        d.base = f->base;
+        d.modulus = N;
+        if (f->kind == QSIM_PERM_MODEXP) {
+            if (f->em < 1 || f->em > 40 || f->elo < 0 || f->elo + f->em > h->n)
+                return fail(h, QSIM_ERANGE, "exponent register outside [0, n)");
+            uint64_t ereg = ((1ull << f->em) - 1) << f->elo;
+            if (ereg & (treg | f->ctrl_mask)) return fail(h, QSIM_EINVAL, "exponent register overlaps");
+        }
+    }
+    // the work register must be local
+    std::vector<int> need;
+    for (int q = f->lo; q < f->lo + f->m; ++q) need.push_back(q);
+    if (int rc = dist_make_local(h, need)) { if (d_table) cudaFree(d_table); return rc; }
+    // work value bit b (LSB) <-> logical qubit lo+m-1-b
+    for (int b = 0; b < f->m; ++b) d.wpos[b] = h->pos[f->lo + f->m - 1 - b];
+    if (f->kind == QSIM_PERM_MODEXP) {
+        d.em = f->em;
+        for (int b = 0; b < f->em; ++b) {
+            const int p = h->pos[f->elo + f->em - 1 - b];
+            d.epos[b] = p < h->nl ? p : -1 - (p - h->nl);
+        }
+    }
+    uint64_t lm, lv;
+    if (!local_controls(h, f->ctrl_mask, f->ctrl_vals, lm, lv)) {
+        if (d_table) { cudaStreamSynchronize(h->stream); cudaFree(d_table); }
+        return QSIM_OK;
+    }
+    d.cmask = lm;
+    d.cval = lv;
+    d.rank_bits = (uint64_t)h->rank;
+    launch_perm(h, d);
+    int rc = after_launch(h, "permutation");
+    if (d_table) { cudaStreamSynchronize(h->stream); cudaFree(d_table); }
+    return rc;
+}
+
+// ----------------------------------------------------------------- decoherence
+int qsim_inject_errors(qsim_t *h, uint64_t seed, const qsim_noise_t *model, qsim_event_t *ev, int cap,
+                       int *nev)
+{
+    QS_CHECK_HANDLE(h);
+    if (!model) return fail(h, QSIM_EINVAL, "null noise model");
+    if (!(model->p >= 0.0 && model->p <= 1.0)) return fail(h, QSIM_EINVAL, "p must be in [0, 1]");
+    int count = 0;
+    for (int q = 0; q < h->n; ++q) {
+        if (!((model->qubit_mask >> q) & 1)) continue;
+        const u64x2 d = draw(seed, QSIM_TAG_PAULI, model->epoch, (uint32_t)q);
+        const double u = u01(d.a);
+        const double p = model->p;
+        const int which = u < p / 3.0 ? 1 : u < 2.0 * p / 3.0 ? 2 : u < p ? 3 : 0;
+        if (!which) continue;
+        double2 P[4];
+        if (which == 1) { P[0] = make_double2(0, 0); P[1] = make_double2(1, 0); P[2] = make_double2(1, 0); P[3] = make_double2(0, 0); }
+        else if (which == 2) { P[0] = make_double2(0, 0); P[1] = make_double2(0, -1); P[2] = make_double2(0, 1); P[3] = make_double2(0, 0); }
+        else { P[0] = make_double2(1, 0); P[1] = make_double2(0, 0); P[2] = make_double2(0, 0); P[3] = make_double2(-1, 0); }
+        if (int rc = apply_gate(h, 0, 0, q, P)) return rc;
+        if (ev && count < cap) {
+            ev[count].epoch = model->epoch;
+            ev[count].qubit = q;
+            ev[count].pauli = which;
+        }
+        ++count;
+    }
+    if (nev) *nev = count;
+    if (ev && count > cap) return fail(h, QSIM_ERANGE, "event buffer too small");
+    return QSIM_OK;
+}
+
+// ----------------------------------------------------------------- read-out
+int qsim_norm(qsim_t *h, double *out)
+{
+    QS_CHECK_HANDLE(h);
+    if (!out) return QSIM_EINVAL;
+    launch_norm(h, h->d_red);
+    if (int rc = after_launch(h, "norm")) return rc;
+    double s = 0.0;
+    if (int rc = check_cuda(h, cudaMemcpyAsync(h->h_red, h->d_red, sizeof(double), cudaMemcpyDeviceToHost, h->stream), "norm"))
+        return rc;
+    if (int rc = check_cuda(h, cudaStreamSynchronize(h->stream), "norm")) return rc;
+    s = h->h_red[0];
+    if (h->world > 1) {
+        if (int rc = dist_allreduce_sum_host(h, &s, 1)) return rc;
+    }
+    *out = s;
+    return QSIM_OK;
+}
+
+int qsim_probs(qsim_t *h, int lo, int m, double *out)
+{
+    QS_CHECK_HANDLE(h);
+    if (!out) return QSIM_EINVAL;
+    if (lo < 0 || m < 1 || m > 26 || lo + m > h->n) return fail(h, QSIM_ERANGE, "range outside [0, n) or m > 26");
+    if (int rc = dist_canonicalize(h)) return rc;
+    // canonical: value bit b <-> position n-lo-m+b; local part [pl, min(nl, pl+m))
+    const int pl = h->n - lo - m;
+    const int ph = pl + m;   // exclusive
+    const uint64_t ny = 1ull << m;
+    if (ph <= h->nl) {
+        ensure_red(h, ny + (1 << 16));
+        double *d_out = h->d_red + h->red_cap - ny;   // tail of the workspace
+        (void)d_out;
+        double *d_res = nullptr;
+        if (cudaMalloc(&d_res, ny * sizeof(double)) != cudaSuccess) { cudaGetLastError(); return fail(h, QSIM_ENOMEM, "probs buffer"); }
+        launch_probs_contig(h, pl, m, d_res);
+        int rc = after_launch(h, "probs");
+        if (!rc) rc = check_cuda(h, cudaMemcpyAsync(out, d_res, ny * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "probs");
+        if (!rc) rc = check_cuda(h, cudaStreamSynchronize(h->stream), "probs");
+        cudaFree(d_res);
+        if (rc) return rc;
+        if (h->world > 1) return dist_allreduce_sum_host(h, out, ny);
+        return QSIM_OK;
+    }
+    // part of the sub-register is on rank bits
+    const int mloc = pl < h->nl ? h->nl - pl : 0;
+    const uint64_t nyl = 1ull << mloc;
+    std::vector<double> part(nyl);
+    double *d_res = nullptr;
+    if (cudaMalloc(&d_res, nyl * sizeof(double)) != cudaSuccess) { cudaGetLastError(); return fail(h, QSIM_ENOMEM, "probs buffer"); }
+    if (mloc > 0) launch_probs_contig(h, pl, mloc, d_res);
+    else launch_norm(h, d_res);
+    int rc = after_launch(h, "probs");
+    if (!rc) rc = check_cuda(h, cudaMemcpyAsync(part.data(), d_res, nyl * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "probs");
+    if (!rc) rc = check_cuda(h, cudaStreamSynchronize(h->stream), "probs");
+    cudaFree(d_res);
+    if (rc) return rc;
+    // place this rank's partial at y = (rank bits of the range) << mloc | y_loc
+    std::vector<double> full(ny, 0.0);
+    const int gl = pl > h->nl ? pl - h->nl : 0;       // first rank bit in the range
+    const int gh = ph - h->nl;                          // exclusive
+    const uint64_t yhi = ((uint64_t)h->rank >> gl) & ((1ull << (gh - gl)) - 1);
+    for (uint64_t y = 0; y < nyl; ++y) full[(yhi << mloc) | y] = part[y];
+    std::memcpy(out, full.data(), ny * sizeof(double));
+    return dist_allreduce_sum_host(h, out, ny);
+}
+
+int qsim_prob_index(qsim_t *h, uint64_t idx, double *out)
+{
+    QS_CHECK_HANDLE(h);
+    if (!out) return QSIM_EINVAL;
+    if (h->n < 64 && idx >> h->n) return fail(h, QSIM_ERANGE, "index >= 2^n");
+    if (int rc = dist_canonicalize(h)) return rc;
+    double v = 0.0;
+    if ((int)(idx >> h->nl) == h->rank) {
+        double2 a;
+        if (int rc = check_cuda(h, cudaMemcpyAsync(&a, h->psi + (idx & (h->local_dim() - 1)), sizeof a,
+                                                   cudaMemcpyDeviceToHost, h->stream), "prob_index"))
+            return rc;
+        if (int rc = check_cuda(h, cudaStreamSynchronize(h->stream), "prob_index")) return rc;
+        v = a.x * a.x + a.y * a.y;
+    }
+    if (h->world > 1) {
+        if (int rc = dist_allreduce_sum_host(h, &v, 1)) return rc;
+    }
+    *out = v;
+    return QSIM_OK;
+}
+
+int qsim_measure(qsim_t *h, double r, uint64_t *idx)
+{
+    QS_CHECK_HANDLE(h);
+    if (!idx) return QSIM_EINVAL;
+    if (!(r >= 0.0 && r < 1.0)) return fail(h, QSIM_EINVAL, "r must be in [0, 1)");
+    if (int rc = dist_canonicalize(h)) return rc;
+    const int bb = h->nl < 16 ? h->nl : 16;
+    const uint64_t nb = h->local_dim() >> bb;
+    double *d_blk = nullptr;
+    if (cudaMalloc(&d_blk, nb * sizeof(double)) != cudaSuccess) { cudaGetLastError(); return fail(h, QSIM_ENOMEM, "measure buffer"); }
+    launch_block_abs2(h, bb, d_blk);
+    int rc = after_launch(h, "measure");
+    std::vector<double> blk(nb * h->world, 0.0);
+    if (!rc) rc = check_cuda(h, cudaMemcpyAsync(blk.data() + nb * h->rank, d_blk, nb * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "measure");
+    if (!rc) rc = check_cuda(h, cudaStreamSynchronize(h->stream), "measure");
+    cudaFree(d_blk);
+    if (rc) return rc;
+    if (h->world > 1) {
+        if (int rc2 = dist_allreduce_sum_host(h, blk.data(), blk.size())) return rc2;
+    }
+    // sequential scan over block sums (fixed order), then inside one block
+    double acc = 0.0;
+    int64_t sel = -1, last_nz_blk = -1;
+    for (uint64_t b = 0; b < blk.size(); ++b) {
+        if (blk[b] != 0.0) last_nz_blk = (int64_t)b;
+        if (sel < 0 && r < acc + blk[b]) { sel = (int64_t)b; break; }
+        acc += blk[b];
+    }
+    const uint64_t blen = 1ull << bb;
+    bool fallback = false;
+    if (sel < 0) { sel = last_nz_blk < 0 ? 0 : last_nz_blk; fallback = true; }
+    const int owner = (int)(((uint64_t)sel * blen) >> h->nl);
+    uint64_t result = 0;
+    std::vector<double2> amp(blen);
+    if (owner == h->rank) {
+        const uint64_t loc = ((uint64_t)sel * blen) & (h->local_dim() - 1);
+        rc = check_cuda(h, cudaMemcpyAsync(amp.data(), h->psi + loc, blen * sizeof(double2), cudaMemcpyDeviceToHost, h->stream), "measure");
+        if (!rc) rc = check_cuda(h, cudaStreamSynchronize(h->stream), "measure");
+        if (rc) return rc;
+        uint64_t last_nz = 0;
+        bool found = false;
+        for (uint64_t i = 0; i < blen; ++i) {
+            const double p = amp[i].x * amp[i].x + amp[i].y * amp[i].y;
+            if (p != 0.0) last_nz = i;
+            acc += p;
+            if (!fallback && r < acc) { result = i; found = true; break; }
+        }
+        if (!found) result = last_nz;
+        result += (uint64_t)sel * blen;
+    }
+    if (h->world > 1) {
+        double v = owner == h->rank ? (double)result : 0.0;
+        if (int rc2 = dist_allreduce_sum_host(h, &v, 1)) return rc2;
+        result = (uint64_t)v;
+    }
+    *idx = result;
+    return QSIM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,253 @@
+// dist.cu -- state-vector sharding over GPUs (one process per GPU, NCCL).
+//
+// The paper's "large subblock" rule (§2.2.1): the rows j
+// and j + 2^(n-i-1) of a gate on qubit i must meet on one processor.  On P
+// GPUs the state is sharded on its top log2(P) physical bits ("global"
+// positions nl..n-1 = the rank bits).  A non-diagonal gate on a qubit at a
+// global position g first swaps that qubit with the top local position:
+// rank r exchanges the half of its shard whose top local bit differs from
+// its own bit g with partner r ^ 2^(g-nl) (ncclSend/ncclRecv in one group;
+// the half is one contiguous block of S/2 bytes).  Only the logical ->
+// physical map changes; nothing is swapped back.  Diagonal gates and
+// gates whose controls sit on rank bits need no communication.
+//
+// Read-outs restore the canonical layout first: global positions by
+// pairwise exchanges, local positions by one bit-permutation pass.
+// Host-side partial results are combined in fixed rank order (allgather,
+// then summed on the host), so results are deterministic.
+#include <cstring>
+#include <vector>
+
+#include "qsim_internal.h"
+
+namespace qs {
+
+#ifndef QSIM_NO_NCCL
+static int nccl_check(Handle *h, ncclResult_t r, const char *what)
+{
+    if (r == ncclSuccess) return QSIM_OK;
+    h->poisoned = 1;
+    return fail(h, QSIM_ENCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+#endif
+
+// Host-side planner (pure; exported as qsim_plan_make_local /
+// qsim_plan_canonicalize for the multi-process CPU tests).  A plan is a list
+// of steps on the physical layout:
+//   {LSWAP, p1, p2}: swap local positions p1 and p2 (a half pass on the shard)
+//   {XCHG, g, -}   : swap global position g with the top local position nl-1
+//                    (rank r exchanges its half with top bit != bit g of r with
+//                    rank r ^ 2^(g-nl))
+// and pos[] (logical -> physical) is updated as the steps would move the data.
+enum { STEP_LSWAP = 0, STEP_XCHG = 1 };
+struct Step { int kind, a, b; };
+
+static int qubit_at(const std::vector<int> &pos, int p)
+{
+    for (int q = 0; q < (int)pos.size(); ++q)
+        if (pos[q] == p) return q;
+    return -1;
+}
+
+static void apply_step(std::vector<int> &pos, int nl, const Step &s)
+{
+    const int pa = s.a, pb = s.kind == STEP_LSWAP ? s.b : nl - 1;
+    const int qa = qubit_at(pos, pa), qb = qubit_at(pos, pb);
+    std::swap(pos[qa], pos[qb]);
+}
+
+static int plan_make_local(int n, int nl, std::vector<int> &pos, const std::vector<int> &need,
+                           std::vector<Step> &steps)
+{
+    std::vector<char> needed(n, 0);
+    for (int q : need) needed[q] = 1;
+    for (int q : need) {
+        const int g = pos[q];
+        if (g < nl) continue;
+        // victim: the highest local position holding a qubit we do not need
+        int victim = -1;
+        for (int p = nl - 1; p >= 0 && victim < 0; --p)
+            if (!needed[qubit_at(pos, p)]) victim = p;
+        if (victim < 0) return QSIM_EINVAL;
+        if (victim != nl - 1) {
+            steps.push_back({STEP_LSWAP, victim, nl - 1});
+            apply_step(pos, nl, steps.back());
+        }
+        steps.push_back({STEP_XCHG, g, -1});
+        apply_step(pos, nl, steps.back());
+    }
+    return QSIM_OK;
+}
+
+// Global positions to canonical (qubit n-1-g at global position g); the local
+// positions are left to one bit-permutation pass.
+static int plan_canonical_globals(int n, int nl, std::vector<int> &pos, std::vector<Step> &steps)
+{
+    for (int g = nl; g < n; ++g) {
+        const int want = n - 1 - g;
+        if (pos[want] == g) continue;
+        if (pos[want] >= nl) {
+            // bring it local first (it sits on a global position > g, so the
+            // positions already placed are not touched)
+            if (int rc = plan_make_local(n, nl, pos, std::vector<int>{want}, steps)) return rc;
+        }
+        const int p = pos[want];
+        if (p != nl - 1) {
+            steps.push_back({STEP_LSWAP, p, nl - 1});
+            apply_step(pos, nl, steps.back());
+        }
+        steps.push_back({STEP_XCHG, g, -1});
+        apply_step(pos, nl, steps.back());
+    }
+    return QSIM_OK;
+}
+
+// Swap global position g with the top local position nl-1 (collective).
+static int exchange_top(Handle *h, int g)
+{
+#ifndef QSIM_NO_NCCL
+    const int gb = g - h->nl;
+    const int partner = h->rank ^ (1 << gb);
+    const int b = (h->rank >> gb) & 1;
+    const uint64_t half = h->local_dim() >> 1;
+    if (int rc = ensure_scratch(h)) return rc;
+    double2 *mine = h->psi + (uint64_t)(1 - b) * half;
+    if (int rc = nccl_check(h, ncclGroupStart(), "ncclGroupStart")) return rc;
+    ncclSend(mine, half * 2, ncclDouble, partner, h->comm, h->stream);
+    ncclRecv(h->scratch, half * 2, ncclDouble, partner, h->comm, h->stream);
+    if (int rc = nccl_check(h, ncclGroupEnd(), "ncclGroupEnd")) return rc;
+    cudaError_t e = cudaMemcpyAsync(mine, h->scratch, half * sizeof(double2), cudaMemcpyDeviceToDevice, h->stream);
+    if (e != cudaSuccess) return check_cuda(h, e, "exchange copy");
+    // bookkeeping: the qubits at g and nl-1 trade places
+    int qg = -1, qt = -1;
+    for (int q = 0; q < h->n; ++q) {
+        if (h->pos[q] == g) qg = q;
+        if (h->pos[q] == h->nl - 1) qt = q;
+    }
+    std::swap(h->pos[qg], h->pos[qt]);
+    return QSIM_OK;
+#else
+    (void)g;
+    return fail(h, QSIM_ENCCL, "built without NCCL");
+#endif
+}
+
+static int run_steps(Handle *h, const std::vector<Step> &steps)
+{
+    for (const Step &st : steps) {
+        if (st.kind == STEP_LSWAP) {
+            launch_swap_local(h, st.a, st.b);
+            std::vector<int> pos(h->pos, h->pos + h->n);
+            apply_step(pos, h->nl, st);
+            for (int q = 0; q < h->n; ++q) h->pos[q] = pos[q];
+        } else {
+            if (int rc = exchange_top(h, st.a)) return rc;
+        }
+    }
+    return QSIM_OK;
+}
+
+int dist_make_local(Handle *h, const std::vector<int> &need)
+{
+    if (h->world == 1) return QSIM_OK;
+    std::vector<int> pos(h->pos, h->pos + h->n);
+    std::vector<Step> steps;
+    if (plan_make_local(h->n, h->nl, pos, need, steps)) return fail(h, QSIM_EINVAL, "too many qubits requested local");
+    return run_steps(h, steps);
+}
+
+int dist_canonicalize(Handle *h)
+{
+    if (h->world > 1) {
+        std::vector<int> pos(h->pos, h->pos + h->n);
+        std::vector<Step> steps;
+        if (plan_canonical_globals(h->n, h->nl, pos, steps)) return fail(h, QSIM_EINVAL, "canonicalize plan");
+        if (int rc = run_steps(h, steps)) return rc;
+    }
+    bool canon = true;
+    for (int q = 0; q < h->n; ++q) canon &= h->pos[q] == h->n - 1 - q;
+    if (canon) return QSIM_OK;
+    std::vector<int> perm(h->nl);
+    for (int q = 0; q < h->n; ++q) {
+        const int p = h->pos[q];
+        if (p < h->nl) perm[p] = h->n - 1 - q;
+    }
+    permute_local(h, perm);
+    for (int q = 0; q < h->n; ++q) h->pos[q] = h->n - 1 - q;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return check_cuda(h, e, "canonicalize");
+    return h->poisoned ? fail(h, QSIM_ECUDA, h->err) : QSIM_OK;
+}
+
+int dist_allgather_doubles(Handle *h, const double *d_in, double *d_out, size_t count)
+{
+#ifndef QSIM_NO_NCCL
+    return nccl_check(h, ncclAllGather(d_in, d_out, count, ncclDouble, h->comm, h->stream), "ncclAllGather");
+#else
+    (void)d_in; (void)d_out; (void)count;
+    return fail(h, QSIM_ENCCL, "built without NCCL");
+#endif
+}
+
+// Sum a host vector over ranks in fixed rank order (allgather + host sum).
+int dist_allreduce_sum_host(Handle *h, double *host, size_t count)
+{
+    if (h->world == 1) return QSIM_OK;
+    double *d_in = nullptr, *d_out = nullptr;
+    if (cudaMalloc(&d_in, count * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&d_out, count * h->world * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        if (d_in) cudaFree(d_in);
+        return fail(h, QSIM_ENOMEM, "allreduce buffers");
+    }
+    cudaMemcpyAsync(d_in, host, count * sizeof(double), cudaMemcpyHostToDevice, h->stream);
+    int rc = dist_allgather_doubles(h, d_in, d_out, count);
+    std::vector<double> all(count * h->world);
+    if (!rc) rc = check_cuda(h, cudaMemcpyAsync(all.data(), d_out, all.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "allgather copy");
+    if (!rc) rc = check_cuda(h, cudaStreamSynchronize(h->stream), "allgather");
+    cudaFree(d_in);
+    cudaFree(d_out);
+    if (rc) return rc;
+    for (size_t i = 0; i < count; ++i) {
+        double s = 0.0;
+        for (int r = 0; r < h->world; ++r) s += all[(size_t)r * count + i];
+        host[i] = s;
+    }
+    return QSIM_OK;
+}
+
+}  // namespace qs
+
+// Exported planners for the host-side tests (no GPU needed).  Steps are
+// written as triples (kind, a, b) into steps[0 .. 3*cap); returns the step
+// count (or a negative QSIM_E* code); pos_io is updated in place.
+extern "C" int qsim_plan_make_local(int n, int world, int *pos_io, const int *need, int nneed,
+                                    int *steps, int cap)
+{
+    using namespace qs;
+    int kg = 0;
+    while ((1 << kg) < world) ++kg;
+    std::vector<int> pos(pos_io, pos_io + n);
+    std::vector<Step> st;
+    if (int rc = plan_make_local(n, n - kg, pos, std::vector<int>(need, need + nneed), st)) return rc;
+    for (int q = 0; q < n; ++q) pos_io[q] = pos[q];
+    for (int i = 0; i < (int)st.size() && i < cap; ++i) {
+        steps[3 * i] = st[i].kind; steps[3 * i + 1] = st[i].a; steps[3 * i + 2] = st[i].b;
+    }
+    return (int)st.size();
+}
+
+extern "C" int qsim_plan_canonical_globals(int n, int world, int *pos_io, int *steps, int cap)
+{
+    using namespace qs;
+    int kg = 0;
+    while ((1 << kg) < world) ++kg;
+    std::vector<int> pos(pos_io, pos_io + n);
+    std::vector<Step> st;
+    if (int rc = plan_canonical_globals(n, n - kg, pos, st)) return rc;
+    for (int q = 0; q < n; ++q) pos_io[q] = pos[q];
+    for (int i = 0; i < (int)st.size() && i < cap; ++i) {
+        steps[3 * i] = st[i].kind; steps[3 * i + 1] = st[i].a; steps[3 * i + 2] = st[i].b;
+    }
+    return (int)st.size();
+}

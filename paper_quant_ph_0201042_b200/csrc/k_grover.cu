@@ -1,0 +1,130 @@
+// k_grover.cu -- Grover iterations (§5.3), fused.
+//
+// One G-iteration is -H_n V_{f0} H_n V_{fk}.  Since -H_n V_{f0} H_n =
+// 2|s><s| - I, the iteration is alpha_k <- -alpha_k followed by
+// alpha <- 2 mean(alpha) - alpha (R17; the oracle applies the
+// literal H_n / V_f0 / H_n sequence and the tests compare the two).
+// Each iteration is ONE kernel over the state: every block updates a
+// contiguous chunk and accumulates the sum of its new amplitudes; the last
+// block to finish (atomic ticket) adds the block partials in a fixed tree
+// order, forms the mean needed by the next iteration, (S - 2 alpha_k) / N,
+// and records |alpha_k|^2 for this iteration.  At n = 20 the 16 MiB state
+// stays resident in the 126 MB L2, so an iteration costs one L2 read+write
+// of the state plus one launch.
+#include "qsim_internal.h"
+
+namespace qs {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxBlocks = 1024;
+
+struct GroverCtl {
+    double2 mean;
+    unsigned int ticket;
+    unsigned int pad;
+    double2 part[kMaxBlocks];
+};
+
+__device__ __forceinline__ double2 warp_sum2(double2 v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+    }
+    return v;
+}
+
+__device__ double2 block_sum2(double2 v, double2 *sh)
+{
+    v = warp_sum2(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double2 t = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : make_double2(0.0, 0.0);
+    if (w == 0) t = warp_sum2(t);
+    if (threadIdx.x == 0) sh[0] = t;
+    __syncthreads();
+    return sh[0];
+}
+
+// init != 0: only sum the current state and form the first mean.
+__global__ void __launch_bounds__(kThreads) k_grover_iter(double2 *__restrict__ psi, uint64_t N,
+                                                          uint64_t chunk, uint64_t k,
+                                                          GroverCtl *__restrict__ ctl,
+                                                          double *__restrict__ trace, int t, int init)
+{
+    __shared__ double2 sh[32];
+    __shared__ int s_last;
+    const double2 mean = ctl->mean;
+    const double m2x = 2.0 * mean.x, m2y = 2.0 * mean.y;
+    const uint64_t b0 = (uint64_t)blockIdx.x * chunk;
+    const uint64_t b1 = b0 + chunk < N ? b0 + chunk : N;
+    double2 acc = make_double2(0.0, 0.0);
+    for (uint64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+        double2 a = psi[i];
+        if (!init) {
+            if (i == k) { a.x = -a.x; a.y = -a.y; }        // V_{f_k}
+            a = make_double2(m2x - a.x, m2y - a.y);        // 2|s><s| - I
+            psi[i] = a;
+        }
+        acc.x += a.x;
+        acc.y += a.y;
+    }
+    const double2 s = block_sum2(acc, sh);
+    if (threadIdx.x == 0) {
+        ctl->part[blockIdx.x] = s;
+        __threadfence();
+        const unsigned tk = atomicAdd(&ctl->ticket, 1u);
+        s_last = tk == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // fixed-order tree over the block partials
+    double2 v = make_double2(0.0, 0.0);
+    for (unsigned j = threadIdx.x; j < gridDim.x; j += blockDim.x) {
+        const double2 pj = __ldcg(&ctl->part[j]);
+        v.x += pj.x;
+        v.y += pj.y;
+    }
+    const double2 S = block_sum2(v, sh);
+    if (threadIdx.x == 0) {
+        const double2 ak = __ldcg(&psi[k]);
+        const double inv = 1.0 / (double)N;
+        ctl->mean = make_double2((S.x - 2.0 * ak.x) * inv, (S.y - 2.0 * ak.y) * inv);
+        if (!init && trace) trace[t] = fma(ak.x, ak.x, ak.y * ak.y);
+        ctl->ticket = 0;
+        __threadfence();
+    }
+}
+
+}  // namespace
+
+void launch_grover(Handle *h, uint64_t mark_local, int mark_rank, int iters, double *d_trace)
+{
+    (void)mark_rank;
+    const uint64_t N = h->local_dim();
+    unsigned blocks = (unsigned)h->num_sms * 4;
+    if (blocks > kMaxBlocks) blocks = kMaxBlocks;
+    uint64_t chunk = (N + blocks - 1) / blocks;
+    chunk = (chunk + kThreads - 1) / kThreads * kThreads;
+    blocks = (unsigned)((N + chunk - 1) / chunk);
+    const size_t need = (sizeof(GroverCtl) + sizeof(double) - 1) / sizeof(double);
+    ensure_red(h, need + 8);
+    GroverCtl *ctl = reinterpret_cast<GroverCtl *>(h->d_red + 8);
+    cudaMemsetAsync(ctl, 0, sizeof(GroverCtl), h->stream);
+    prof_begin(h);
+    k_grover_iter<<<blocks, kThreads, 0, h->stream>>>(h->psi, N, chunk, mark_local, ctl, d_trace, 0, 1);
+    prof_end(h, "k_grover_iter", N * 16);
+    for (int t = 0; t < iters; ++t) {
+        prof_begin(h);
+        k_grover_iter<<<blocks, kThreads, 0, h->stream>>>(h->psi, N, chunk, mark_local, ctl, d_trace, t, 0);
+        prof_end(h, "k_grover_iter", N * 32);
+    }
+}
+
+}  // namespace qs

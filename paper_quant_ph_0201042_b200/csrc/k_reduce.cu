@@ -1,0 +1,198 @@
+// k_reduce.cu -- state preparation and read-out reductions (sm_100a).
+//
+// Reductions (norm, marginals, block sums for measurement) are read-only
+// streaming passes: 16 bytes per amplitude.  Sums follow a fixed tree
+// (per-thread sums of a few contiguous elements, warp shuffle tree, block
+// tree, then a second-level tree over block partials), so results are
+// deterministic and the rounding error grows like log(N), not sqrt(N)
+// (R23).
+#include "philox.cuh"
+#include "qsim_internal.h"
+
+namespace qs {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ double abs2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
+
+__device__ __forceinline__ double warp_sum(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-wide sum (all threads must call); result valid in every thread.
+__device__ double block_sum(double v, double *sh)
+{
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    const int nw = blockDim.x >> 5;
+    double t = (threadIdx.x < nw) ? sh[threadIdx.x] : 0.0;
+    if (w == 0) t = warp_sum(t);
+    if (threadIdx.x == 0) sh[0] = t;
+    __syncthreads();
+    return sh[0];
+}
+
+// Sum of |a|^2 over chunks: block b sums [b*chunk, (b+1)*chunk) (chunk a
+// multiple of blockDim) and writes out[b].
+__global__ void __launch_bounds__(kThreads) k_chunk_abs2(const double2 *__restrict__ psi,
+                                                         uint64_t chunk, double *__restrict__ out)
+{
+    __shared__ double sh[32];
+    const uint64_t base = (uint64_t)blockIdx.x * chunk;
+    double acc = 0.0;
+    for (uint64_t i = threadIdx.x; i < chunk; i += blockDim.x) acc += abs2(psi[base + i]);
+    const double s = block_sum(acc, sh);
+    if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+// Tree sum of chunks of doubles: block b sums in[b*chunk .. b*chunk+count)
+// (count <= chunk) and writes out[b]; each thread first sums a contiguous
+// segment.
+__global__ void __launch_bounds__(1024) k_sum_doubles(const double *__restrict__ in, uint64_t chunk,
+                                                      uint64_t count, double *__restrict__ out)
+{
+    __shared__ double sh[32];
+    in += (uint64_t)blockIdx.x * chunk;
+    const uint64_t per = (count + blockDim.x - 1) / blockDim.x;
+    double acc = 0.0;
+    const uint64_t b = threadIdx.x * per;
+    for (uint64_t i = b; i < b + per && i < count; ++i) acc += in[i];
+    const double s = block_sum(acc, sh);
+    if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+// Marginals when the sub-register occupies contiguous local positions
+// [pl, pl+m): element i has value y = (i >> pl) & (2^m - 1).  Grid: one
+// block per (y, rest-chunk); out[y * nchunk + c].
+__global__ void __launch_bounds__(kThreads) k_probs_contig(const double2 *__restrict__ psi, int nl,
+                                                           int pl, int m, uint64_t chunk,
+                                                           uint64_t nchunk, double *__restrict__ out)
+{
+    __shared__ double sh[32];
+    const uint64_t y = blockIdx.x / nchunk, c = blockIdx.x % nchunk;
+    const uint64_t lowmask = (1ull << pl) - 1;
+    double acc = 0.0;
+    for (uint64_t r = c * chunk + threadIdx.x; r < (c + 1) * chunk; r += blockDim.x) {
+        // r enumerates the bits outside [pl, pl+m): low pl bits, then the high ones
+        const uint64_t i = ((r >> pl) << (pl + m)) | (y << pl) | (r & lowmask);
+        acc += abs2(psi[i]);
+    }
+    const double s = block_sum(acc, sh);
+    if (threadIdx.x == 0) out[blockIdx.x] = s;
+    (void)nl;
+}
+
+// per-y tree over its chunks
+__global__ void k_probs_finish(const double *__restrict__ part, uint64_t ny, uint64_t nchunk,
+                               double *__restrict__ out)
+{
+    const uint64_t y = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (y >= ny) return;
+    // pairwise over nchunk (a power of two)
+    double buf[64];
+    uint64_t w = nchunk;
+    if (w <= 64) {
+        for (uint64_t c = 0; c < w; ++c) buf[c] = part[y * nchunk + c];
+        while (w > 1) {
+            for (uint64_t c = 0; c < w / 2; ++c) buf[c] = buf[2 * c] + buf[2 * c + 1];
+            w /= 2;
+        }
+        out[y] = buf[0];
+    } else {
+        double s = 0.0;
+        for (uint64_t c = 0; c < nchunk; ++c) s += part[y * nchunk + c];
+        out[y] = s;
+    }
+}
+
+// Gaussian amplitudes (R19) generated on the device with the library's Philox.
+__global__ void __launch_bounds__(kThreads) k_init_gaussian(double2 *__restrict__ psi, uint64_t count,
+                                                            uint64_t gbase, uint64_t seed)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+        const u64x2 d = draw(seed, QSIM_TAG_GAUSS, gbase + i, 0);
+        const double rad = sqrt(-2.0 * log(u01o(d.a)));
+        double s, c;
+        sincospi(2.0 * u01(d.b), &s, &c);
+        psi[i] = make_double2(rad * c, rad * s);
+    }
+}
+
+}  // namespace
+
+static void sum_tree(Handle *h, const double *d_in, uint64_t count, double *d_out)
+{
+    prof_begin(h);
+    k_sum_doubles<<<1, 1024, 0, h->stream>>>(d_in, count, count, d_out);
+    prof_end(h, "k_sum_doubles", count * 8);
+}
+
+void launch_block_abs2(Handle *h, int blk_bits, double *d_out)
+{
+    const uint64_t chunk = 1ull << blk_bits;
+    const uint64_t nb = h->local_dim() >> blk_bits;
+    prof_begin(h);
+    k_chunk_abs2<<<(unsigned)nb, kThreads, 0, h->stream>>>(h->psi, chunk, d_out);
+    prof_end(h, "k_chunk_abs2", h->local_dim() * 16);
+}
+
+void launch_norm(Handle *h, double *d_out)
+{
+    // chunks of 2^12 (or the whole shard if smaller), then one tree over them
+    const int bb = h->nl < 12 ? h->nl : 12;
+    const uint64_t nb = h->local_dim() >> bb;
+    ensure_red(h, nb + 8);
+    launch_block_abs2(h, bb, h->d_red + 8);
+    if (nb <= (1u << 20)) {
+        sum_tree(h, h->d_red + 8, nb, d_out);
+    } else {
+        // two levels (n_local > 32)
+        const uint64_t nb2 = nb >> 10;
+        ensure_red(h, nb + nb2 + 8);
+        prof_begin(h);
+        k_sum_doubles<<<(unsigned)nb2, 1024, 0, h->stream>>>(h->d_red + 8, 1024, 1024, h->d_red + 8 + nb);
+        prof_end(h, "k_sum_doubles", nb * 8);
+        sum_tree(h, h->d_red + 8 + nb, nb2, d_out);
+    }
+}
+
+void launch_probs_contig(Handle *h, int pl, int m, double *d_out)
+{
+    const uint64_t ny = 1ull << m;
+    const uint64_t rest = h->local_dim() >> m;
+    // chunks so that the grid has >= ~2 waves of blocks
+    uint64_t nchunk = 1;
+    while (ny * nchunk < (uint64_t)h->num_sms * 16 && rest / (nchunk * 2) >= kThreads && nchunk < 64) nchunk *= 2;
+    const uint64_t chunk = rest / nchunk;
+    ensure_red(h, ny * nchunk + 8);
+    prof_begin(h);
+    k_probs_contig<<<(unsigned)(ny * nchunk), kThreads, 0, h->stream>>>(h->psi, h->nl, pl, m, chunk,
+                                                                         nchunk, h->d_red + 8);
+    prof_end(h, "k_probs_contig", h->local_dim() * 16);
+    prof_begin(h);
+    k_probs_finish<<<(unsigned)((ny + 255) / 256), 256, 0, h->stream>>>(h->d_red + 8, ny, nchunk, d_out);
+    prof_end(h, "k_probs_finish", ny * nchunk * 8);
+}
+
+void launch_init_gaussian(Handle *h, uint64_t seed)
+{
+    const uint64_t count = h->local_dim();
+    const uint64_t gbase = (uint64_t)h->rank << h->nl;
+    const uint64_t want = (count + kThreads - 1) / kThreads;
+    const uint64_t cap = (uint64_t)h->num_sms * 8;
+    prof_begin(h);
+    k_init_gaussian<<<(unsigned)(want < cap ? want : cap), kThreads, 0, h->stream>>>(h->psi, count,
+                                                                                      gbase, seed);
+    prof_end(h, "k_init_gaussian", count * 16);
+}
+
+}  // namespace qs

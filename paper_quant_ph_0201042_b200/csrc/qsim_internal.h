@@ -1,0 +1,180 @@
+// qsim_internal.h -- the handle, layout map and kernel launchers of libqsim.
+//
+// Layout of the state in HBM: each rank holds one contiguous
+// shard of 2^nl complex128 amplitudes (double2: re, im interleaved, 16 B).
+// Physical bit positions 0..nl-1 index inside the shard; positions
+// nl..n-1 are the rank bits ("global" positions).  The handle keeps a map
+// pos[q] = physical position of logical qubit q; the canonical map is
+// pos[q] = n-1-q (qubit 0 = MSB).  Kernels only ever see local
+// positions; the API layer translates logical qubits through pos[] and
+// brings global qubits local with NCCL exchanges (dist.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/qsim.h"
+
+#ifndef QSIM_NO_NCCL
+#include <nccl.h>
+#endif
+
+namespace qs {
+
+constexpr int kMaxQubits = 40;
+
+constexpr int kMaxFixedBits = 48;
+
+struct Handle;
+
+// --------------------------------------------------------------- kernels
+// Every launcher enqueues on h->stream and bumps h->launches.
+
+// Dense 2x2 on local position p; applied where (i & cmask) == cval (local mask).
+void launch_apply_2x2(Handle *h, int p, uint64_t cmask, uint64_t cval, const double2 U[4]);
+// Diagonal diag(d0, d1) on local position p (both entries applied), controlled.
+void launch_apply_diag(Handle *h, int p, uint64_t cmask, uint64_t cval, double2 d0, double2 d1);
+// Multiply every amplitude with (i & mask) == val by ph.
+void launch_phase_mask(Handle *h, uint64_t mask, uint64_t val, double2 ph);
+// Swap local positions p1 != p2.
+void launch_swap_local(Handle *h, int p1, int p2);
+// Scale every amplitude by s (real).
+void launch_scale(Handle *h, double s);
+// |0..0> style initialisation: zero the shard, then set element idx (local) to 1.
+void launch_zero(Handle *h);
+void launch_set_one(Handle *h, uint64_t local_idx);
+// Gaussian amplitudes for the shard; logical index of local element i is
+// (rank << nl) | i in canonical layout.
+void launch_init_gaussian(Handle *h, uint64_t seed);
+// sum |a|^2 over the shard -> one double on the device (d_out), tree order.
+void launch_norm(Handle *h, double *d_out);
+// Partial sums of |a|^2 over consecutive blocks of 2^blk_bits amplitudes.
+void launch_block_abs2(Handle *h, int blk_bits, double *d_out);
+// Marginals over the `m` physical positions [pl, pl+m) (value bit b <-> position pl+b).
+void launch_probs_contig(Handle *h, int pl, int m, double *d_out);
+// Modular exponentiation / multiplication permutation (out of place).
+struct PermDesc {
+    int kind;
+    int wpos[40], wm;      // work register: value bit b (LSB = 0) at local position wpos[b]
+    int epos[40], em;      // exponent register value bits (LSB = 0): local position, or -1 - g for global bit g
+    uint64_t cmask, cval;  // local control mask / values
+    uint64_t mult, base, modulus;
+    const uint32_t *d_table;
+    uint64_t rank_bits;    // this rank's global bits (for exponent bits that are global)
+};
+void launch_perm(Handle *h, const PermDesc &d);
+// Grover: iters fused iterations; d_trace receives |a_mark|^2 per iteration.
+void launch_grover(Handle *h, uint64_t mark_local, int mark_rank, int iters, double *d_trace);
+
+// Fused tile passes (k_tile.cu).  A pass reads every amplitude once and
+// writes it once: the shard is cut into tiles of 2^tbits amplitudes that
+// share the values of the "fixed" local bits; a CTA gathers a tile (tile bit
+// b at input position in_pos[b]), applies the pass's QFT block in registers
+// (16 amplitudes per thread, shared-memory transposes between register
+// windows), and scatters it to out_pos[] (a bit permutation of the layout
+// folded into the store).  With a = 0 the pass is a pure bit permutation.
+constexpr int kTileMaxBits = 13;   // <= 8192 amplitudes = 128 KiB of smem
+constexpr int kRegBits = 4;        // 16 amplitudes per thread
+constexpr int kMaxMaps = 5;
+
+struct TileMap {
+    int win[kRegBits];             // tile bits held in registers (slot bit b <-> tile bit win[b])
+    int order[kTileMaxBits];       // thread bit t <-> tile bit order[t]
+    int ustart, ucnt;              // active wires u in [ustart, ustart+ucnt) get phase + H here
+};
+
+struct TilePass {
+    int tbits;                     // tile bits (kRegBits+5 <= tbits <= kTileMaxBits)
+    int a;                         // active wires: tile bits 0..a-1 in H order (a <= 10)
+    int in_pos[kTileMaxBits];      // tile bit -> input local position
+    int out_pos[kTileMaxBits];     // tile bit -> output local position
+    int nfix;                      // fixed bits: tile index bit f of the tile id
+    int fin_pos[kMaxFixedBits];
+    int fout_pos[kMaxFixedBits];
+    int nmaps;
+    TileMap map[kMaxMaps];
+    // twiddle exp(+-2 pi i Y J / 2^W): J = sum_u b_u 2^(a-1-u), Y = early-wire value
+    int n_et, et_bit[kTileMaxBits], et_w[kTileMaxBits];   // early wires on tile bits
+    int n_ef, ef_bit[kMaxFixedBits], ef_w[kMaxFixedBits]; // early wires on fixed bits
+    uint64_t y_const;              // early wires on rank bits
+    int W;
+    int inverse;
+    int hadamard_only;             // 1: H on the active wires only (no R_d phases, no twiddle)
+    double scale;                  // 2^(-a/2)
+};
+// in -> out (may alias when the pass does not move fixed bits between tiles)
+void launch_tile_pass(Handle *h, const TilePass &tp, const double2 *in, double2 *out);
+// host planner helpers (k_tile.cu): fill tp.map[] from tbits/a/in_pos/out_pos
+void plan_tile_maps(TilePass &tp);
+
+// --------------------------------------------------------------- handle
+struct Handle {
+    int n = 0;              // qubits
+    int world = 1, rank = 0;
+    int kglob = 0;          // log2(world)
+    int nl = 0;             // local qubits
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    double2 *psi = nullptr;      // shard (2^nl)
+    double2 *scratch = nullptr;  // lazily allocated, 2^nl (bit permutations, exchanges)
+    int pos[kMaxQubits];         // logical qubit -> physical position
+    // reduction workspace
+    double *d_red = nullptr;
+    size_t red_cap = 0;          // doubles
+    double *h_red = nullptr;     // pinned
+    size_t hred_cap = 0;
+    // angle noise (R15)
+    uint64_t noise_seed = 0;
+    double sigma = 0.0;
+    uint64_t gcount = 0;
+    // bookkeeping
+    uint64_t launches = 0;
+    int poisoned = 0;
+    std::string err;
+#ifndef QSIM_NO_NCCL
+    ncclComm_t comm = nullptr;
+#endif
+    int num_sms = 148;
+    // profiling
+    int prof_on = 0;
+    struct ProfRec { const char *name; uint64_t bytes; cudaEvent_t a, b; };
+    std::vector<ProfRec> prof;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    cudaEvent_t pending = nullptr;
+    std::string prof_json;
+
+    uint64_t local_dim() const { return (uint64_t)1 << nl; }
+};
+
+// per-launch profiling (qsim_profile): events around every kernel launch when
+// enabled; prof_end also counts the launch.
+void prof_begin(Handle *h);
+void prof_end(Handle *h, const char *name, uint64_t bytes);
+
+// error helpers
+int fail(Handle *h, int code, const std::string &msg);
+int check_cuda(Handle *h, cudaError_t e, const char *what);
+void ensure_red(Handle *h, size_t doubles);
+void ensure_hred(Handle *h, size_t doubles);
+int ensure_scratch(Handle *h);
+inline void swap_buffers(Handle *h)
+{
+    double2 *t = h->psi;
+    h->psi = h->scratch;
+    h->scratch = t;
+}
+
+// distributed layer (dist.cu)
+int dist_make_local(Handle *h, const std::vector<int> &need);  // make logical qubits local
+int dist_canonicalize(Handle *h);                                // pos[q] = n-1-q everywhere
+int dist_allgather_doubles(Handle *h, const double *d_in, double *d_out, size_t count);
+int dist_allreduce_sum_host(Handle *h, double *host, size_t count);  // fixed rank order
+// local bit-permutation pass (api.cu): new position of old local position p is perm[p]
+void permute_local(Handle *h, const std::vector<int> &perm);
+
+}  // namespace qs
+
+struct qsim_s : public qs::Handle {};

@@ -1,0 +1,319 @@
+"""ctypes binding of libqsim.so (include/qsim.h) -- argument marshalling only.
+
+Every function here has the name of the C entry point it wraps and does
+nothing but convert arguments and raise ``QsimError`` on a negative status.
+All computation happens in the sm_100a kernels of ``libqsim.so``; there is no
+CPU fallback: importing this module raises if the library cannot be loaded,
+and ``qsim_create`` fails with QSIM_ENODEV when no B200 (sm_100) is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libqsim.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `make -C {_HERE}/csrc` "
+        "(or __graft_entry__.build()); the gate engine has no CPU fallback"
+    )
+
+lib = C.CDLL(LIB_PATH)
+
+QSIM_OK, QSIM_EINVAL, QSIM_ERANGE, QSIM_ENOMEM = 0, -1, -2, -3
+QSIM_ECUDA, QSIM_ENOTBIJ, QSIM_ESTATE, QSIM_ENCCL, QSIM_ENODEV = -4, -5, -6, -7, -8
+QSIM_GATE_RP, QSIM_GATE_P1, QSIM_GATE_HAAR = 0, 1, 2
+QSIM_PERM_TABLE, QSIM_PERM_MODMUL, QSIM_PERM_MODEXP = 0, 1, 2
+QSIM_TAG_GATE, QSIM_TAG_HAAR, QSIM_TAG_PAIR, QSIM_TAG_OPNOISE = 1, 2, 3, 4
+QSIM_TAG_MARK, QSIM_TAG_BASE, QSIM_TAG_GAUSS, QSIM_TAG_PAULI, QSIM_TAG_MEASURE = 5, 6, 7, 8, 9
+
+_ERRNAMES = {
+    -1: "QSIM_EINVAL", -2: "QSIM_ERANGE", -3: "QSIM_ENOMEM", -4: "QSIM_ECUDA",
+    -5: "QSIM_ENOTBIJ", -6: "QSIM_ESTATE", -7: "QSIM_ENCCL", -8: "QSIM_ENODEV",
+}
+
+
+class QsimError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_ERRNAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class qsim_c128(C.Structure):
+    _fields_ = [("re", C.c_double), ("im", C.c_double)]
+
+
+class qsim_perm_t(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int), ("lo", C.c_int), ("m", C.c_int), ("elo", C.c_int), ("em", C.c_int),
+        ("ctrl_mask", C.c_uint64), ("ctrl_vals", C.c_uint64),
+        ("mult", C.c_uint64), ("base", C.c_uint64), ("modulus", C.c_uint64),
+        ("table", C.POINTER(C.c_uint32)),
+    ]
+
+
+class qsim_noise_t(C.Structure):
+    _fields_ = [("p", C.c_double), ("qubit_mask", C.c_uint64), ("epoch", C.c_uint64)]
+
+
+class qsim_event_t(C.Structure):
+    _fields_ = [("epoch", C.c_uint64), ("qubit", C.c_int32), ("pauli", C.c_int32)]
+
+
+_H = C.c_void_p
+_u64, _u32, _i32, _f64, _p = C.c_uint64, C.c_uint32, C.c_int, C.c_double, C.c_void_p
+
+
+def _sig(name, res, *args):
+    f = getattr(lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+
+
+_sig("qsim_create", _i32, _i32, _i32, C.POINTER(_H))
+_sig("qsim_create_dist", _i32, _i32, _i32, _i32, _i32, _p, C.POINTER(_H))
+_sig("qsim_nccl_unique_id", _i32, _p)
+_sig("qsim_destroy", None, _H)
+_sig("qsim_last_error", C.c_char_p, _H)
+_sig("qsim_memory_bytes", _u64, _i32)
+_sig("qsim_launch_count", _u64, _H)
+_sig("qsim_sync", _i32, _H)
+_sig("qsim_set_basis", _i32, _H, _u64)
+_sig("qsim_init_gaussian", _i32, _H, _u64)
+_sig("qsim_set_state", _i32, _H, _u64, _u64, _p)
+_sig("qsim_get_state", _i32, _H, _u64, _u64, _p)
+_sig("qsim_apply_1q", _i32, _H, _i32, _p)
+_sig("qsim_apply_ctrl", _i32, _H, _u64, _u64, _i32, _p)
+_sig("qsim_apply_angles", _i32, _H, _i32, _p, _u64, _u64, _i32)
+_sig("qsim_set_gate_noise", _i32, _H, _u64, _f64)
+_sig("qsim_get_gate_counter", _i32, _H, C.POINTER(_u64))
+_sig("qsim_set_gate_counter", _i32, _H, _u64)
+_sig("qsim_swap", _i32, _H, _i32, _i32)
+_sig("qsim_hadamard", _i32, _H, _i32, _i32)
+_sig("qsim_qft", _i32, _H, _i32, _i32, _i32)
+_sig("qsim_phase_flip", _i32, _H, _u64)
+_sig("qsim_grover", _i32, _H, _u64, _i32, _p)
+_sig("qsim_apply_perm", _i32, _H, C.POINTER(qsim_perm_t))
+_sig("qsim_inject_errors", _i32, _H, _u64, C.POINTER(qsim_noise_t), _p, _i32, C.POINTER(_i32))
+_sig("qsim_norm", _i32, _H, C.POINTER(_f64))
+_sig("qsim_probs", _i32, _H, _i32, _i32, _p)
+_sig("qsim_prob_index", _i32, _H, _u64, C.POINTER(_f64))
+_sig("qsim_measure", _i32, _H, _f64, C.POINTER(_u64))
+_sig("qsim_philox_draw", None, _u64, _u32, _u64, _u32, _p)
+_sig("qsim_get_stream", _p, _H)
+_sig("qsim_profile", _i32, _H, _i32)
+_sig("qsim_profile_json", C.c_char_p, _H)
+_sig("qsim_plan_make_local", _i32, _i32, _i32, _p, _p, _i32, _p, _i32)
+_sig("qsim_plan_canonical_globals", _i32, _i32, _i32, _p, _p, _i32)
+
+
+def _chk(h, rc: int) -> None:
+    if rc != QSIM_OK:
+        msg = lib.qsim_last_error(h)
+        raise QsimError(rc, msg.decode() if msg else "")
+
+
+def _mat(U) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(U, dtype=np.complex128).reshape(4))
+
+
+# ------------------------------------------------------------------ lifecycle
+def qsim_create(n: int, ngpus: int = 1):
+    h = _H()
+    _chk(None, lib.qsim_create(n, ngpus, C.byref(h)))
+    return h
+
+
+def qsim_create_dist(n: int, world: int, rank: int, device: int, nccl_id: bytes):
+    h = _H()
+    buf = C.create_string_buffer(bytes(nccl_id), 128)
+    _chk(None, lib.qsim_create_dist(n, world, rank, device, buf, C.byref(h)))
+    return h
+
+
+def qsim_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _chk(None, lib.qsim_nccl_unique_id(buf))
+    return buf.raw
+
+
+def qsim_destroy(h) -> None:
+    lib.qsim_destroy(h)
+
+
+def qsim_last_error(h) -> str:
+    m = lib.qsim_last_error(h)
+    return m.decode() if m else ""
+
+
+def qsim_memory_bytes(n: int) -> int:
+    return lib.qsim_memory_bytes(n)
+
+
+def qsim_launch_count(h) -> int:
+    return lib.qsim_launch_count(h)
+
+
+def qsim_sync(h) -> None:
+    _chk(h, lib.qsim_sync(h))
+
+
+def qsim_get_stream(h) -> int:
+    return lib.qsim_get_stream(h) or 0
+
+
+def qsim_profile(h, enable: bool) -> None:
+    _chk(h, lib.qsim_profile(h, int(bool(enable))))
+
+
+def qsim_profile_json(h) -> dict:
+    import json
+    return json.loads(lib.qsim_profile_json(h).decode())
+
+
+# ------------------------------------------------------------------ preparation
+def qsim_set_basis(h, idx: int) -> None:
+    _chk(h, lib.qsim_set_basis(h, idx))
+
+
+def qsim_init_gaussian(h, seed: int) -> None:
+    _chk(h, lib.qsim_init_gaussian(h, seed))
+
+
+def qsim_set_state(h, off: int, amps: np.ndarray) -> None:
+    a = np.ascontiguousarray(amps, dtype=np.complex128)
+    _chk(h, lib.qsim_set_state(h, off, a.size, a.ctypes.data))
+
+
+def qsim_get_state(h, off: int, cnt: int, out: np.ndarray | None = None) -> np.ndarray:
+    if out is None:
+        out = np.empty(cnt, np.complex128)
+    assert out.dtype == np.complex128 and out.flags["C_CONTIGUOUS"] and out.size >= cnt
+    _chk(h, lib.qsim_get_state(h, off, cnt, out.ctypes.data))
+    return out
+
+
+# ------------------------------------------------------------------ gates
+def qsim_apply_1q(h, q: int, U) -> None:
+    m = _mat(U)
+    _chk(h, lib.qsim_apply_1q(h, q, m.ctypes.data))
+
+
+def qsim_apply_ctrl(h, ctrl_mask: int, ctrl_vals: int, q: int, U) -> None:
+    m = _mat(U)
+    _chk(h, lib.qsim_apply_ctrl(h, ctrl_mask, ctrl_vals, q, m.ctypes.data))
+
+
+def qsim_apply_angles(h, kind: int, ang, ctrl_mask: int, ctrl_vals: int, q: int) -> None:
+    a = np.zeros(4, np.float64)
+    a[: len(ang)] = ang
+    _chk(h, lib.qsim_apply_angles(h, kind, a.ctypes.data, ctrl_mask, ctrl_vals, q))
+
+
+def qsim_set_gate_noise(h, seed: int, sigma: float) -> None:
+    _chk(h, lib.qsim_set_gate_noise(h, seed, sigma))
+
+
+def qsim_get_gate_counter(h) -> int:
+    g = _u64()
+    _chk(h, lib.qsim_get_gate_counter(h, C.byref(g)))
+    return g.value
+
+
+def qsim_set_gate_counter(h, g: int) -> None:
+    _chk(h, lib.qsim_set_gate_counter(h, g))
+
+
+def qsim_swap(h, q1: int, q2: int) -> None:
+    _chk(h, lib.qsim_swap(h, q1, q2))
+
+
+def qsim_hadamard(h, lo: int, m: int) -> None:
+    _chk(h, lib.qsim_hadamard(h, lo, m))
+
+
+def qsim_qft(h, lo: int, m: int, inverse: bool = False) -> None:
+    _chk(h, lib.qsim_qft(h, lo, m, int(bool(inverse))))
+
+
+def qsim_phase_flip(h, idx: int) -> None:
+    _chk(h, lib.qsim_phase_flip(h, idx))
+
+
+def qsim_grover(h, mark: int, iters: int, trace: bool = True):
+    out = np.zeros(max(iters, 1), np.float64) if trace else None
+    _chk(h, lib.qsim_grover(h, mark, iters, out.ctypes.data if trace else None))
+    return out[:iters] if trace else None
+
+
+def qsim_apply_perm(h, kind: int, lo: int, m: int, *, elo: int = 0, em: int = 0, ctrl_mask: int = 0,
+                    ctrl_vals: int = 0, mult: int = 0, base: int = 0, modulus: int = 0,
+                    table=None) -> None:
+    f = qsim_perm_t(kind, lo, m, elo, em, ctrl_mask, ctrl_vals, mult, base, modulus, None)
+    keep = None
+    if table is not None:
+        keep = np.ascontiguousarray(np.asarray(table, dtype=np.uint32))
+        f.table = keep.ctypes.data_as(C.POINTER(C.c_uint32))
+    _chk(h, lib.qsim_apply_perm(h, C.byref(f)))
+    del keep
+
+
+def qsim_inject_errors(h, seed: int, p: float, qubit_mask: int, epoch: int, cap: int = 256):
+    model = qsim_noise_t(p, qubit_mask, epoch)
+    ev = (qsim_event_t * max(cap, 1))()
+    nev = _i32(0)
+    _chk(h, lib.qsim_inject_errors(h, seed, C.byref(model), ev, cap, C.byref(nev)))
+    return [(int(ev[i].epoch), int(ev[i].qubit), int(ev[i].pauli)) for i in range(nev.value)]
+
+
+# ------------------------------------------------------------------ read-out
+def qsim_norm(h) -> float:
+    v = _f64()
+    _chk(h, lib.qsim_norm(h, C.byref(v)))
+    return v.value
+
+
+def qsim_probs(h, lo: int, m: int) -> np.ndarray:
+    out = np.zeros(1 << m, np.float64)
+    _chk(h, lib.qsim_probs(h, lo, m, out.ctypes.data))
+    return out
+
+
+def qsim_prob_index(h, idx: int) -> float:
+    v = _f64()
+    _chk(h, lib.qsim_prob_index(h, idx, C.byref(v)))
+    return v.value
+
+
+def qsim_measure(h, r: float) -> int:
+    v = _u64()
+    _chk(h, lib.qsim_measure(h, r, C.byref(v)))
+    return v.value
+
+
+# ------------------------------------------------------------------ RNG + planners
+def qsim_philox_draw(seed: int, tag: int, i: int, j: int):
+    out = np.zeros(2, np.uint64)
+    lib.qsim_philox_draw(seed, tag, i, j, out.ctypes.data)
+    return int(out[0]), int(out[1])
+
+
+def qsim_plan_make_local(n: int, world: int, pos, need):
+    pos = np.ascontiguousarray(np.asarray(pos, dtype=np.int32)).copy()
+    nd = np.ascontiguousarray(np.asarray(need, dtype=np.int32))
+    steps = np.zeros(3 * 256, np.int32)
+    k = lib.qsim_plan_make_local(n, world, pos.ctypes.data, nd.ctypes.data, nd.size, steps.ctypes.data, 256)
+    _chk(None, min(k, 0))
+    return pos, [tuple(int(x) for x in steps[3 * i: 3 * i + 3]) for i in range(k)]
+
+
+def qsim_plan_canonical_globals(n: int, world: int, pos):
+    pos = np.ascontiguousarray(np.asarray(pos, dtype=np.int32)).copy()
+    steps = np.zeros(3 * 256, np.int32)
+    k = lib.qsim_plan_canonical_globals(n, world, pos.ctypes.data, steps.ctypes.data, 256)
+    _chk(None, min(k, 0))
+    return pos, [tuple(int(x) for x in steps[3 * i: 3 * i + 3]) for i in range(k)]

@@ -17,6 +17,7 @@ import numpy as np
 import pytest
 
 import oracle as O
+from _closed_forms import fejer_distribution, order
 
 
 def rand_state(n, rng):
@@ -167,27 +168,6 @@ def test_modmul_is_a_bijection():
     before = np.sort_complex(psi.copy())
     O.modmul(psi, 4, 6, 0b1010, 0b1000, 35, 61)
     assert np.array_equal(np.sort_complex(psi), before)
-
-
-def fejer_distribution(M, r):
-    """Exact P(y) of the noiseless order-finding register."""
-    y = np.arange(M, dtype=np.int64)
-    t = ((r * y) % M) / M
-    P = np.zeros(M)
-    for a0 in range(r):
-        c = (M - 1 - a0) // r + 1
-        with np.errstate(invalid="ignore", divide="ignore"):
-            F = np.sin(np.pi * c * t) ** 2 / np.sin(np.pi * t) ** 2
-        F[t == 0] = c * c
-        P += F
-    return P / M**2
-
-
-def order(a, N):
-    r, x = 1, a % N
-    while x != 1:
-        x = (x * a) % N; r += 1
-    return r
 
 
 @pytest.mark.parametrize("N,a,ne,nw", [(15, 7, 8, 4), (15, 11, 8, 4), (21, 2, 9, 5),
