@@ -58,16 +58,15 @@ __device__ __forceinline__ uint32_t thread_part(const TileMap &m, int nthr_bits,
 
 // exp(+-2 pi i t / 2^W) from the root table (tab[k] = exp(+-2 pi i k/1024))
 // and a Taylor series for the remainder angle (|theta| < 2 pi / 1024).
-__device__ __forceinline__ double2 root_of_unity(uint64_t t, int W, const double2 *tab, int inverse)
+// tw = +-2 pi / 2^W (sign = direction of the transform).
+__device__ __forceinline__ double2 root_of_unity(uint64_t t, int W, const double2 *tab, double tw)
 {
     if (W <= 10) return tab[(uint32_t)(t << (10 - W)) & 1023u];
     const uint64_t hi = t >> (W - 10);
     const uint64_t lo = t & ((1ull << (W - 10)) - 1);
     double2 p = tab[(uint32_t)hi & 1023u];
     if (lo) {
-        // theta = 2 pi lo / 2^W
-        double th = (double)lo * ldexp(6.283185307179586476925286766559, -W);
-        if (inverse) th = -th;
+        const double th = (double)lo * tw;
         const double t2 = th * th;
         const double c = fma(fma(fma(-t2, 1.0 / 720.0, 1.0 / 24.0), t2, -0.5), t2, 1.0);
         const double s = th * fma(fma(fma(-t2, 1.0 / 5040.0, 1.0 / 120.0), t2, -1.0 / 6.0), t2, 1.0);
@@ -76,7 +75,21 @@ __device__ __forceinline__ double2 root_of_unity(uint64_t t, int W, const double
     return p;
 }
 
-__global__ void __launch_bounds__(512) k_tile_pass(const __grid_constant__ TilePass tp,
+// c * exp(+-i pi / 2^d) for d = 1, 2, 3 (sg = +-1: direction of the transform)
+__device__ __forceinline__ double2 rot(double2 c, int d, double sg)
+{
+    if (d == 1) return make_double2(-sg * c.y, sg * c.x);
+    if (d == 2) {
+        const double r = 0.70710678118654752440;
+        return make_double2((c.x - sg * c.y) * r, (c.y + sg * c.x) * r);
+    }
+    return cmul(c, make_double2(0.92387953251128675613, sg * 0.38268343236508977173));
+}
+
+// The pass kernel.  NM = number of register maps (compile time, so that all
+// per-map values live in registers and every slot index is static).
+template <int NM>
+__global__ void __launch_bounds__(256, 1) k_tile_pass(const __grid_constant__ TilePass tp,
                                                    const double2 *in, double2 *out, uint64_t ntiles)
 {
     extern __shared__ double2 smem[];
@@ -84,32 +97,40 @@ __global__ void __launch_bounds__(512) k_tile_pass(const __grid_constant__ TileP
     double2 *tab = smem + (1u << tp.tbits);
     const uint32_t tid = threadIdx.x;
     const int tb = tp.tbits - kRegBits;   // thread bits
+    const double sg = tp.inverse ? -1.0 : 1.0;
 
     // roots of unity exp(+-2 pi i k / 1024)
     for (uint32_t k = tid; k < 1024; k += blockDim.x) {
         double s, c;
         sincospi((double)k / 512.0, &s, &c);
-        tab[k] = make_double2(c, tp.inverse ? -s : s);
+        tab[k] = make_double2(c, sg * s);
     }
     __syncthreads();
 
-    const TileMap &m0 = tp.map[0];
-    const TileMap &mL = tp.map[tp.nmaps - 1];
-    // per-thread parts of the load / store offsets (tile-local -> position offsets)
+    // per-thread constants (all maps)
+    uint32_t tpart[NM], stp[NM];
+#pragma unroll
+    for (int m = 0; m < NM; ++m) {
+        tpart[m] = thread_part(tp.map[m], tb, tid);
+        stp[m] = swz(tpart[m]);
+    }
     uint64_t tin = 0, tout = 0;
     for (int t = 0; t < tb; ++t) {
         const uint64_t bit = (tid >> t) & 1u;
-        tin |= bit << tp.in_pos[m0.order[t]];
-        tout |= bit << tp.out_pos[mL.order[t]];
+        tin |= bit << tp.in_pos[tp.map[0].order[t]];
+        tout |= bit << tp.out_pos[tp.map[NM - 1].order[t]];
     }
     uint64_t pin[kRegBits], pout[kRegBits];
 #pragma unroll
     for (int b = 0; b < kRegBits; ++b) {
-        pin[b] = 1ull << tp.in_pos[m0.win[b]];
-        pout[b] = 1ull << tp.out_pos[mL.win[b]];
+        pin[b] = 1ull << tp.in_pos[tp.map[0].win[b]];
+        pout[b] = 1ull << tp.out_pos[tp.map[NM - 1].win[b]];
     }
-
+    const bool twid = !tp.hadamard_only && tp.a > 0 && (tp.n_et > 0 || tp.n_ef > 0 || tp.y_const != 0);
     const uint32_t amask = (1u << tp.a) - 1u;
+    const uint32_t Jt = tp.a > 0 ? (__brev(tpart[0] & amask) >> (32 - tp.a)) : 0u;
+    uint64_t yt = 0;
+    for (int e = 0; e < tp.n_et; ++e) yt += (uint64_t)((tpart[0] >> tp.et_bit[e]) & 1u) << tp.et_w[e];
 
     for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x) {
         uint64_t ib = 0, ob = 0;
@@ -118,99 +139,96 @@ __global__ void __launch_bounds__(512) k_tile_pass(const __grid_constant__ TileP
             ib |= bit << tp.fin_pos[f];
             ob |= bit << tp.fout_pos[f];
         }
-        uint64_t yfix = tp.y_const;
-        for (int e = 0; e < tp.n_ef; ++e) yfix += ((T >> tp.ef_bit[e]) & 1u) << tp.ef_w[e];
-
         double2 v[NS];
-        // ---- gather (map 0)
+        // ---- gather (map 0): lowest thread bits walk the lowest input positions
         {
-            const uint64_t base = ib | tin;
+            uint64_t o[NS];
+            o[0] = ib | tin;
 #pragma unroll
-            for (int k = 0; k < NS; ++k) {
-                uint64_t o = 0;
+            for (int b = 0; b < kRegBits; ++b)
 #pragma unroll
-                for (int b = 0; b < kRegBits; ++b)
-                    if (k & (1 << b)) o |= pin[b];
-                v[k] = __ldcs(in + (base | o));
-            }
+                for (int j = 0; j < (1 << b); ++j) o[j | (1 << b)] = o[j] | pin[b];
+#pragma unroll
+            for (int k = 0; k < NS; ++k) v[k] = __ldcs(in + o[k]);
         }
-        // ---- twiddle + normalisation (before any H of this pass)
-        {
-            uint32_t wb[kRegBits];
+        // ---- twiddle of the earlier blocks' R_d gates + normalisation
+        if (twid) {
+            uint64_t Y = tp.y_const + yt;
+            for (int e = 0; e < tp.n_ef; ++e) Y += ((T >> tp.ef_bit[e]) & 1u) << tp.ef_w[e];
+            if (tp.twiddle_fast) {
+                // J = Jt + sum_b k_b jwin[b]  ->  phase(k) = A * prod_b beta_b^{k_b},
+                // applied progressively (no table of 16 phases in registers)
+                const double2 A = root_of_unity(Y * Jt, tp.W, tab, tp.tw);
+                const double2 As = make_double2(A.x * tp.scale, A.y * tp.scale);
 #pragma unroll
-            for (int b = 0; b < kRegBits; ++b) wb[b] = 1u << m0.win[b];
-            const uint32_t tpart = thread_part(m0, tb, tid);
-            const bool has_y = !tp.hadamard_only && (tp.n_et > 0 || tp.n_ef > 0 || tp.y_const != 0);
+                for (int k = 0; k < NS; ++k) v[k] = cmul(v[k], As);
 #pragma unroll
-            for (int k = 0; k < NS; ++k) {
-                uint32_t ti = tpart;
+                for (int b = 0; b < kRegBits; ++b) {
+                    if (!tp.jwin[b]) continue;
+                    const double2 beta = root_of_unity(Y * tp.jwin[b], tp.W, tab, tp.tw);
 #pragma unroll
-                for (int b = 0; b < kRegBits; ++b)
-                    if (k & (1 << b)) ti |= wb[b];
-                double2 ph = make_double2(tp.scale, 0.0);
-                if (has_y && tp.a > 0) {
-                    uint64_t Y = yfix;
-                    for (int e = 0; e < tp.n_et; ++e) Y += (uint64_t)((ti >> tp.et_bit[e]) & 1u) << tp.et_w[e];
-                    const uint32_t J = __brev(ti & amask) >> (32 - tp.a);
-                    const uint64_t t = Y * (uint64_t)J;
-                    if (t) {
-                        const double2 r = root_of_unity(t, tp.W, tab, tp.inverse);
-                        ph = make_double2(r.x * tp.scale, r.y * tp.scale);
-                    }
+                    for (int k = 0; k < NS; ++k)
+                        if (k & (1 << b)) v[k] = cmul(v[k], beta);
                 }
-                v[k] = cmul(v[k], ph);
+            } else {
+#pragma unroll
+                for (int k = 0; k < NS; ++k) {
+                    uint32_t ti = tpart[0];
+#pragma unroll
+                    for (int b = 0; b < kRegBits; ++b)
+                        if (k & (1 << b)) ti |= 1u << tp.map[0].win[b];
+                    uint64_t Yk = Y - yt;
+                    for (int e = 0; e < tp.n_et; ++e) Yk += (uint64_t)((ti >> tp.et_bit[e]) & 1u) << tp.et_w[e];
+                    const uint32_t J = __brev(ti & amask) >> (32 - tp.a);
+                    const double2 r = root_of_unity(Yk * J, tp.W, tab, tp.tw);
+                    v[k] = cmul(v[k], make_double2(r.x * tp.scale, r.y * tp.scale));
+                }
             }
+        } else if (tp.scale != 1.0) {
+#pragma unroll
+            for (int k = 0; k < NS; ++k) v[k] = make_double2(v[k].x * tp.scale, v[k].y * tp.scale);
         }
-        // ---- register windows
-        for (int mi = 0; mi < tp.nmaps; ++mi) {
-            const TileMap &m = tp.map[mi];
-            uint32_t wb[kRegBits];
+        // ---- register maps
 #pragma unroll
-            for (int b = 0; b < kRegBits; ++b) wb[b] = 1u << m.win[b];
-            const uint32_t tpart = thread_part(m, tb, tid);
-            if (mi > 0) {
-                const TileMap &pm = tp.map[mi - 1];
-                uint32_t pwb[kRegBits];
+        for (int m = 0; m < NM; ++m) {
+            if (m > 0) {
+                uint32_t s[NS];
+                s[0] = stp[m - 1];
 #pragma unroll
-                for (int b = 0; b < kRegBits; ++b) pwb[b] = 1u << pm.win[b];
-                const uint32_t ptpart = thread_part(pm, tb, tid);
+                for (int b = 0; b < kRegBits; ++b)
+#pragma unroll
+                    for (int j = 0; j < (1 << b); ++j) s[j | (1 << b)] = s[j] ^ tp.wswz[m - 1][b];
                 __syncthreads();   // previous readers of the tile buffer are done
 #pragma unroll
-                for (int k = 0; k < NS; ++k) {
-                    uint32_t ti = ptpart;
+                for (int k = 0; k < NS; ++k) tile[s[k]] = v[k];
+                s[0] = stp[m];
 #pragma unroll
-                    for (int b = 0; b < kRegBits; ++b)
-                        if (k & (1 << b)) ti |= pwb[b];
-                    tile[swz(ti)] = v[k];
-                }
+                for (int b = 0; b < kRegBits; ++b)
+#pragma unroll
+                    for (int j = 0; j < (1 << b); ++j) s[j | (1 << b)] = s[j] ^ tp.wswz[m][b];
                 __syncthreads();
 #pragma unroll
-                for (int k = 0; k < NS; ++k) {
-                    uint32_t ti = tpart;
-#pragma unroll
-                    for (int b = 0; b < kRegBits; ++b)
-                        if (k & (1 << b)) ti |= wb[b];
-                    v[k] = tile[swz(ti)];
-                }
+                for (int k = 0; k < NS; ++k) v[k] = tile[s[k]];
             }
-            if (m.ucnt > 0) {
-                const int w0 = m.win[0];   // compute windows are contiguous: win[b] = w0 + b
+            const TileMap &mp = tp.map[m];
+            if (mp.ucnt > 0) {
+                const int w0 = mp.win[0];   // compute windows are contiguous: win[b] = w0 + b
 #pragma unroll
                 for (int rb = 0; rb < kRegBits; ++rb) {
                     const int u = w0 + rb;
-                    if (u < m.ustart || u >= m.ustart + m.ucnt) continue;
-                    // phase exp(i pi sum_{u'<u} y_u' 2^(u'-u)) on b_u = 1
-                    if (u > 0 && !tp.hadamard_only) {
-                        const uint32_t zmask = (1u << u) - 1u;
+                    if (u < mp.ustart || u >= mp.ustart + mp.ucnt) continue;
+                    if (!tp.hadamard_only && u > 0) {
+                        // exp(i pi sum_{u'<u} y_u' 2^(u'-u)) on b_u = 1: thread part
+                        // from the root table, window part = products of R_1..R_3
+                        const double2 P = tab[((tpart[m] & ((1u << u) - 1u)) << (9 - u)) & 1023u];
 #pragma unroll
                         for (int k = 0; k < NS; ++k) {
                             if (!(k & (1 << rb))) continue;
-                            uint32_t ti = tpart;
+                            double2 x = cmul(v[k], P);
 #pragma unroll
-                            for (int b = 0; b < kRegBits; ++b)
-                                if (k & (1 << b)) ti |= wb[b];
-                            const uint32_t z = ti & zmask;
-                            if (z) v[k] = cmul(v[k], tab[(z << (9 - u)) & 1023u]);
+                            for (int r2 = 0; r2 < rb; ++r2)
+                                if (k & (1 << r2)) x = rot(x, rb - r2, sg);
+                            v[k] = x;
                         }
                     }
                     // H (unnormalised): (x, y) -> (x + y, x - y)
@@ -224,17 +242,16 @@ __global__ void __launch_bounds__(512) k_tile_pass(const __grid_constant__ TileP
                 }
             }
         }
-        // ---- scatter (last map)
+        // ---- scatter (last map): lowest thread bits walk the lowest output positions
         {
-            const uint64_t base = ob | tout;
+            uint64_t o[NS];
+            o[0] = ob | tout;
 #pragma unroll
-            for (int k = 0; k < NS; ++k) {
-                uint64_t o = 0;
+            for (int b = 0; b < kRegBits; ++b)
 #pragma unroll
-                for (int b = 0; b < kRegBits; ++b)
-                    if (k & (1 << b)) o |= pout[b];
-                __stcs(out + (base | o), v[k]);
-            }
+                for (int j = 0; j < (1 << b); ++j) o[j | (1 << b)] = o[j] | pout[b];
+#pragma unroll
+            for (int k = 0; k < NS; ++k) __stcs(out + o[k], v[k]);
         }
     }
 }
@@ -309,25 +326,56 @@ void plan_tile_maps(TilePass &tp)
     for (int i = 0; i < tp.nmaps; ++i) tp.map[i] = maps[i];
 }
 
-void launch_tile_pass(Handle *h, const TilePass &tp, const double2 *in, double2 *out)
+static uint32_t swz_host(uint32_t ti)
+{
+    uint32_t f = (ti >> 3) ^ (ti >> 6) ^ (ti >> 9) ^ (ti >> 12);
+    return ti ^ (f & 7u);
+}
+
+template <int NM>
+static void launch_nm(Handle *h, const TilePass &tp, const double2 *in, double2 *out)
 {
     const size_t smem = (sizeof(double2) << tp.tbits) + 1024 * sizeof(double2);
     static bool attr_done = false;
     if (!attr_done) {
-        cudaFuncSetAttribute(k_tile_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_tile_pass<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)((sizeof(double2) << kTileMaxBits) + 1024 * sizeof(double2)));
         attr_done = true;
     }
     const int threads = 1 << (tp.tbits - kRegBits);
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile_pass, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile_pass<NM>, threads, smem);
     if (per_sm < 1) per_sm = 1;
     const uint64_t ntiles = 1ull << tp.nfix;
     const uint64_t cap = (uint64_t)h->num_sms * per_sm;
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
     prof_begin(h);
-    k_tile_pass<<<grid, threads, smem, h->stream>>>(tp, in, out, ntiles);
+    k_tile_pass<NM><<<grid, threads, smem, h->stream>>>(tp, in, out, ntiles);
     prof_end(h, "k_tile_pass", (1ull << (tp.tbits + tp.nfix)) * 32);
+}
+
+void launch_tile_pass(Handle *h, const TilePass &tp_in, const double2 *in, double2 *out)
+{
+    TilePass tp = tp_in;
+    // derived constants (host side): swizzled window bits, J weights of the
+    // map-0 window, whether every early tile bit is a thread bit of map 0
+    for (int m = 0; m < tp.nmaps; ++m)
+        for (int b = 0; b < kRegBits; ++b) tp.wswz[m][b] = swz_host(1u << tp.map[m].win[b]);
+    for (int b = 0; b < kRegBits; ++b) {
+        const int w = tp.map[0].win[b];
+        tp.jwin[b] = w < tp.a ? (1u << (tp.a - 1 - w)) : 0u;
+    }
+    tp.twiddle_fast = 1;
+    for (int e = 0; e < tp.n_et; ++e)
+        for (int b = 0; b < kRegBits; ++b) tp.twiddle_fast &= tp.et_bit[e] != tp.map[0].win[b];
+    tp.tw = (tp.inverse ? -1.0 : 1.0) * 6.283185307179586476925286766559 / std::ldexp(1.0, tp.W);
+    switch (tp.nmaps) {
+    case 1: launch_nm<1>(h, tp, in, out); break;
+    case 2: launch_nm<2>(h, tp, in, out); break;
+    case 3: launch_nm<3>(h, tp, in, out); break;
+    case 4: launch_nm<4>(h, tp, in, out); break;
+    default: launch_nm<5>(h, tp, in, out); break;
+    }
 }
 
 }  // namespace qs

@@ -75,7 +75,7 @@ void launch_grover(Handle *h, uint64_t mark_local, int mark_rank, int iters, dou
 // (16 amplitudes per thread, shared-memory transposes between register
 // windows), and scatters it to out_pos[] (a bit permutation of the layout
 // folded into the store).  With a = 0 the pass is a pure bit permutation.
-constexpr int kTileMaxBits = 13;   // <= 8192 amplitudes = 128 KiB of smem
+constexpr int kTileMaxBits = 12;   // <= 4096 amplitudes = 64 KiB of smem
 constexpr int kRegBits = 4;        // 16 amplitudes per thread
 constexpr int kMaxMaps = 5;
 
@@ -103,6 +103,11 @@ struct TilePass {
     int inverse;
     int hadamard_only;             // 1: H on the active wires only (no R_d phases, no twiddle)
     double scale;                  // 2^(-a/2)
+    // derived by launch_tile_pass
+    uint32_t wswz[kMaxMaps][kRegBits];   // swizzled smem index of each window bit
+    uint32_t jwin[kRegBits];             // J weight of the map-0 window bits
+    int twiddle_fast;                    // early tile bits are all thread bits of map 0
+    double tw;                           // +-2 pi / 2^W
 };
 // in -> out (may alias when the pass does not move fixed bits between tiles)
 void launch_tile_pass(Handle *h, const TilePass &tp, const double2 *in, double2 *out);

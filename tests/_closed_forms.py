@@ -4,19 +4,27 @@
   (§5.1): with M = 2^m exponent values and r = ord_N(a),
   P(y) = M^-2 sum_{a0<r} F_{c(a0)}(t), t = ((r y) mod M)/M,
   c(a0) = floor((M-1-a0)/r) + 1, F_c(t) = sin^2(pi c t)/sin^2(pi t), F_c(0) = c^2.
+  Both sine arguments are reduced exactly in integers first
+  (sin^2(pi c T / M) = sin^2(pi ((c T) mod M) / M), T = r y mod M), so the
+  closed form keeps full double precision for M = 2^20; angles are folded into
+  [0, pi/2] (sin^2 is symmetric about pi/2) so that sines near pi keep their
+  relative accuracy.
 """
 import numpy as np
 
 
 def fejer_distribution(M, r):
     y = np.arange(M, dtype=np.int64)
-    t = ((r * y) % M) / M
+    T = (r * y) % M
+    den = np.sin(np.pi * np.minimum(T, M - T) / M) ** 2
     P = np.zeros(M)
     for a0 in range(r):
         c = (M - 1 - a0) // r + 1
+        X = (c * T) % M
+        X = np.minimum(X, M - X)          # sin^2(pi x) = sin^2(pi (1 - x)): keep the angle <= pi/2
         with np.errstate(invalid="ignore", divide="ignore"):
-            F = np.sin(np.pi * c * t) ** 2 / np.sin(np.pi * t) ** 2
-        F[t == 0] = c * c
+            F = np.sin(np.pi * X / M) ** 2 / den
+        F[T == 0] = c * c
         P += F
     return P / M**2
 

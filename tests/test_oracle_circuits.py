@@ -60,7 +60,7 @@ def test_qft_basis_state_closed_form(inverse):
     for y in range(N):
         psi = np.zeros(N, complex); psi[y] = 1
         O.qft(psi, 0, n, inverse)
-        ref = np.exp(s * 2j * np.pi * np.arange(N) * y / N) / math.sqrt(N)
+        ref = np.exp(s * 2j * np.pi * ((np.arange(N) * y) % N) / N) / math.sqrt(N)
         assert np.max(np.abs(psi - ref)) < 1e-14
 
 
