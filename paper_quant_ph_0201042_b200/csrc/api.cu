@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -276,54 +277,63 @@ TilePass make_pass(const Handle *h, const std::vector<int> &tile_pos, const std:
 }
 
 // Fused H / QFT on the wires [lo, lo+m) (logical).  qft = 0: Hadamard transform.
+//
+// Wires are cut into G blocks of <= amax consecutive wires; pass g applies
+// every gate of block g (see k_tile.cu).  A pass reads a tile of 2^12
+// amplitudes: the block's wires + the lowest other positions ("passive", so
+// the tile moves in runs of >= 2^(12-a) contiguous amplitudes).
+//
+// Single GPU, QFT: the closing swaps are folded into the stores with a
+// block-move layout (no extra pass).  Invariant before pass g (wires
+// 0..a0-1 done): positions [s0, s0+a0) hold wires 0..a0-1 in final order,
+// positions [s0+a0, s0+m) hold wires a0..m-1 descending (wire a0 on top;
+// s0 = lowest position of the range).  Pass g writes its block to
+// [s0+a0, s0+a0+a) ascending and shifts the rest up by a, so after the last
+// pass wire w sits at s0+w, which is where logical qubit lo+m-1-w lived:
+// the swapped labels land exactly on the canonical layout.  Every position
+// run stays contiguous, so each pass is one <= 5-D TMA box per tile.
 int fused_range(Handle *h, int lo, int m, int qft, int inverse)
 {
-    const int amax = 10;
+    static const int amax_env = getenv("QSIM_QFT_AMAX") ? atoi(getenv("QSIM_QFT_AMAX")) : 10;
+    const int amax = amax_env < 1 ? 1 : (amax_env > 10 ? 10 : amax_env);
     const int G = (m + amax - 1) / amax;
     std::vector<int> gsize(G, m / G);
     for (int g = 0; g < m % G; ++g) gsize[g]++;
-    // F: wire w -> the position now held by logical qubit lo+m-1-w (closing swaps);
-    // Hadamard: identity.
-    std::vector<int> a0s(G);
-    for (int g = 0, acc = 0; g < G; ++g) { a0s[g] = acc; acc += gsize[g]; }
-    bool relabelled = false;   // closing swaps already folded into a store
-    // physical position of wire w (before the fold: logical lo+w; after it:
-    // the position logical lo+m-1-w had, which is pos[lo+m-1-w] again since
-    // pos[] is left unchanged by the fold)
-    auto wire_pos = [&](int w) { return relabelled ? h->pos[lo + m - 1 - w] : h->pos[lo + w]; };
+    const bool block_moves = qft && h->world == 1;
+    if (block_moves) {
+        if (int rc = dist_canonicalize(h)) return rc;
+    }
+    const int s0 = h->n - lo - m;          // lowest position of the range (canonical)
+    std::vector<int> wp(m);                // current position of wire w
+    for (int w = 0; w < m; ++w) wp[w] = h->pos[lo + w];
+    int a0 = 0;
     for (int g = 0; g < G; ++g) {
-        const int a0 = a0s[g], a = gsize[g];
+        const int a = gsize[g];
         std::vector<int> act;
         for (int u = 0; u < a; ++u) act.push_back(lo + a0 + u);
         if (h->world > 1) {
-            int rc = dist_make_local(h, act);
-            if (rc) return rc;
+            if (int rc = dist_make_local(h, act)) return rc;
+            for (int w = 0; w < m; ++w) wp[w] = h->pos[lo + w];
         }
         // tile: active wires (tile bits 0..a-1) + passive low positions
         std::vector<int> tile_pos;
         std::vector<char> in_tile(h->nl, 0);
         for (int u = 0; u < a; ++u) {
-            tile_pos.push_back(wire_pos(a0 + u));
-            in_tile[wire_pos(a0 + u)] = 1;
+            tile_pos.push_back(wp[a0 + u]);
+            in_tile[wp[a0 + u]] = 1;
         }
-        const int want = std::max(9, std::min(a + 3, kTileMaxBits));
+        const int want = std::min(kTileMaxBits, h->nl);
         for (int p = 0; p < h->nl && (int)tile_pos.size() < want; ++p)
             if (!in_tile[p]) { tile_pos.push_back(p); in_tile[p] = 1; }
-        // output permutation: identity, or (first QFT pass, single rank) the
-        // closing swaps folded into the store
+        // output permutation of the local positions
         std::vector<int> perm(h->nl);
         for (int p = 0; p < h->nl; ++p) perm[p] = p;
-        bool fold = false;
-        if (qft && g == 0 && h->world == 1) {
-            std::vector<int> cand(perm);
-            for (int w = 0; w < m; ++w) cand[h->pos[lo + w]] = h->pos[lo + m - 1 - w];
-            // the store walks the 3 lowest output positions: they must be tile bits
-            bool ok = true;
-            std::vector<int> inv(h->nl);
-            for (int p = 0; p < h->nl; ++p) inv[cand[p]] = p;
-            for (int k = 0; k < 3 && k < h->nl; ++k) ok &= in_tile[inv[k]] != 0;
-            if (ok) { perm = cand; fold = true; }
+        if (block_moves) {
+            for (int w = a0 + a; w < m; ++w) perm[wp[w]] = wp[w] + a;   // rest block moves up
+            for (int u = 0; u < a; ++u) perm[wp[a0 + u]] = s0 + a0 + u;  // block to final spots
         }
+        bool moved_fixed = false;
+        for (int p = 0; p < h->nl; ++p) moved_fixed |= !in_tile[p] && perm[p] != p;
         TilePass tp = make_pass(h, tile_pos, perm);
         tp.a = a;
         tp.inverse = inverse;
@@ -335,7 +345,7 @@ int fused_range(Handle *h, int lo, int m, int qft, int inverse)
         tp.y_const = 0;
         if (qft) {
             for (int i = 0; i < a0; ++i) {
-                const int p = wire_pos(i);
+                const int p = wp[i];
                 if (p >= h->nl) {
                     tp.y_const += (uint64_t)((h->rank >> (p - h->nl)) & 1) << i;
                     continue;
@@ -351,20 +361,19 @@ int fused_range(Handle *h, int lo, int m, int qft, int inverse)
             }
         }
         plan_tile_maps(tp);
-        if (fold) {
+        if (moved_fixed) {
             if (ensure_scratch(h)) return QSIM_ENOMEM;
             launch_tile_pass(h, tp, h->psi, h->scratch);
             swap_buffers(h);
-            // the wires moved: wire w now sits where lo+m-1-w was; after the
-            // closing swaps logical qubit lo+t is wire m-1-t -> back to pos_in.
-            relabelled = true;
         } else {
             launch_tile_pass(h, tp, h->psi, h->psi);
         }
-        int rc = after_launch(h, "fused tile pass");
-        if (rc) return rc;
+        if (int rc = after_launch(h, "fused tile pass")) return rc;
+        for (int w = 0; w < m; ++w)
+            if (wp[w] < h->nl) wp[w] = perm[wp[w]];
+        a0 += a;
     }
-    if (qft && !relabelled) {
+    if (qft && !block_moves) {
         // closing swaps as a relabelling of the logical -> physical map
         for (int t = 0; t < m / 2; ++t) std::swap(h->pos[lo + t], h->pos[lo + m - 1 - t]);
     }

@@ -1,0 +1,354 @@
+// k_tma.cu -- TMA-pipelined, warp-specialised fused QFT / H pass (sm_100a).
+//
+// Same arithmetic as k_tile.cu (tile_body), different data movement:
+//   * a persistent CTA per SM (8 warps, 16 amplitudes per thread) streams
+//     tiles HBM -> shared memory with one cp.async.bulk.tensor (TMA) per tile
+//     into a 3-stage ring of 64 KiB buffers; completion is signalled on an
+//     mbarrier (complete_tx::bytes);
+//   * the warps read the tile from its TMA box layout, run the register maps
+//     (transposes in the same buffer), write the result in the output box
+//     layout; thread 0 issues the TMA store (bulk_group), waits until the
+//     previous tile's store has read its buffer and immediately refills that
+//     buffer with the load of the tile two steps ahead.
+// (No separate producer warp: at 224 registers per thread a 9th warp would
+// not fit the per-SM-sub-partition register file.)
+// So while a tile is being computed, the next two are in flight from HBM and
+// the previous one is being written back: the pass streams at HBM speed as
+// long as the FP64 + shared-memory work of a tile hides under its transfer
+// time.  The tile geometry (which positions form the box) comes from the
+// block-move pass plan in api.cu; positions outside the box are coordinates
+// of a <= 5-D tensor map (runs of consecutive positions).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "qsim_internal.h"
+#include "tile_common.cuh"
+
+namespace qs {
+
+namespace {
+
+using namespace tile;
+
+constexpr int kStages = 3;
+constexpr int kTmaTileBits = 12;                          // 4096 amplitudes
+constexpr uint32_t kTileBytes = 16u << kTmaTileBits;      // 64 KiB
+constexpr int kThreads = 256;
+
+struct TmaArgs {
+    // per tensor-map dim d (0..4): first tile-id bit and length of the fixed
+    // run it addresses (len 0: a box dim, coordinate 0)
+    int in_first[5], in_len[5];
+    int out_first[5], out_len[5];
+    // smem amplitude index of each tile bit in the load / store boxes
+    int in_rank[kTileMaxBits], out_rank[kTileMaxBits];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load(void *dst, const CUtensorMap *map, const int (&c)[5], uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)map), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_store(const CUtensorMap *map, const int (&c)[5], const void *src)
+{
+    asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+                     (uint64_t)map),
+                 "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(src))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_read()
+{
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void coords(const int (&first)[5], const int (&len)[5], uint64_t T, int (&c)[5])
+{
+#pragma unroll
+    for (int d = 0; d < 5; ++d)
+        c[d] = len[d] ? (int)((T >> first[d]) & ((1ull << len[d]) - 1)) : 0;
+}
+
+template <int NM>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_tile_tma(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
+               const __grid_constant__ TilePass tp, const __grid_constant__ TmaArgs ta, uint64_t ntiles)
+{
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    double2 *bufs = reinterpret_cast<double2 *>(smem_raw);                       // kStages x 4096
+    double2 *tab = bufs + kStages * (1u << kTmaTileBits);                          // 1024
+    uint64_t *full = reinterpret_cast<uint64_t *>(tab + 1024);                     // kStages
+    const uint32_t tid = threadIdx.x;
+    const double sg = tp.inverse ? -1.0 : 1.0;
+
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (uint32_t k = tid; k < 1024; k += blockDim.x) {
+        double s, c;
+        sincospi((double)k / 512.0, &s, &c);
+        tab[k] = make_double2(c, sg * s);
+    }
+    __syncthreads();
+    // prologue: the first two tiles of this CTA are requested right away
+    if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&in_map) : "memory");
+        for (uint64_t q = 0; q < kStages - 1; ++q) {
+            const uint64_t T = blockIdx.x + q * gridDim.x;
+            if (T >= ntiles) break;
+            int c[5];
+            coords(ta.in_first, ta.in_len, T, c);
+            mbar_expect_tx(&full[q], kTileBytes);
+            tma_load(bufs + (size_t)q * (1u << kTmaTileBits), &in_map, c, &full[q]);
+        }
+    }
+
+    // ---------------- compute warps
+    constexpr int tb = kTmaTileBits - kRegBits;   // 8 thread bits
+    uint32_t tpart[NM], stp[NM];
+#pragma unroll
+    for (int m = 0; m < NM; ++m) {
+        tpart[m] = thread_part(tp.map[m], tb, tid);
+        stp[m] = swz(tpart[m]);
+    }
+    // box-layout indices: map 0 reads the load box, the last map writes the store box
+    uint32_t lin = 0, lout = 0;
+    for (int t = 0; t < tb; ++t) {
+        lin |= ((tid >> t) & 1u) << ta.in_rank[tp.map[0].order[t]];
+        lout |= ((tid >> t) & 1u) << ta.out_rank[tp.map[NM - 1].order[t]];
+    }
+    uint32_t pin[kRegBits], pout[kRegBits];
+#pragma unroll
+    for (int b = 0; b < kRegBits; ++b) {
+        pin[b] = 1u << ta.in_rank[tp.map[0].win[b]];
+        pout[b] = 1u << ta.out_rank[tp.map[NM - 1].win[b]];
+    }
+    const bool twid = !tp.hadamard_only && tp.a > 0 && (tp.n_et > 0 || tp.n_ef > 0 || tp.y_const != 0);
+    const uint32_t amask = (1u << tp.a) - 1u;
+    const uint32_t Jt = tp.a > 0 ? (__brev(tpart[0] & amask) >> (32 - tp.a)) : 0u;
+    uint64_t yt = 0;
+    for (int e = 0; e < tp.n_et; ++e) yt += (uint64_t)((tpart[0] >> tp.et_bit[e]) & 1u) << tp.et_w[e];
+
+    uint64_t j = 0;
+    for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x, ++j) {
+        const int s = (int)(j % kStages);
+        double2 *buf = bufs + (size_t)s * (1u << kTmaTileBits);
+        mbar_wait(&full[s], (uint32_t)((j / kStages) & 1));
+        double2 v[NS];
+        {
+            uint32_t o[NS];
+            o[0] = lin;
+#pragma unroll
+            for (int b = 0; b < kRegBits; ++b)
+#pragma unroll
+                for (int q = 0; q < (1 << b); ++q) o[q | (1 << b)] = o[q] | pin[b];
+#pragma unroll
+            for (int k = 0; k < NS; ++k) v[k] = buf[o[k]];
+        }
+        tile_body<NM, true>(v, tp, tpart, stp, tab, buf, T, yt, Jt, twid, amask, sg);
+        {
+            uint32_t o[NS];
+            o[0] = lout;
+#pragma unroll
+            for (int b = 0; b < kRegBits; ++b)
+#pragma unroll
+                for (int q = 0; q < (1 << b); ++q) o[q | (1 << b)] = o[q] | pout[b];
+            tile_sync<true>();   // everybody is done reading this buffer
+#pragma unroll
+            for (int k = 0; k < NS; ++k) buf[o[k]] = v[k];
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tile_sync<true>();
+        if (tid == 0) {
+            int c[5];
+            coords(ta.out_first, ta.out_len, T, c);
+            tma_store(&out_map, c, buf);
+            // the previous tile's store has finished reading its buffer:
+            // refill it with the tile two steps ahead
+            bulk_wait_read<1>();
+            const uint64_t Tn = T + (uint64_t)(kStages - 1) * gridDim.x;
+            if (Tn < ntiles) {
+                const int sn = (int)((j + kStages - 1) % kStages);
+                coords(ta.in_first, ta.in_len, Tn, c);
+                mbar_expect_tx(&full[sn], kTileBytes);
+                tma_load(bufs + (size_t)sn * (1u << kTmaTileBits), &in_map, c, &full[sn]);
+            }
+        }
+    }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ host
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn()
+{
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+        else
+            cudaGetLastError();
+    }
+    return fn;
+}
+
+// Build the 5-D tensor map of one side (in or out).  pos_of_tile[b] = the
+// position of tile bit b on this side; fixed position p carries tile-id bit
+// fid[p] (-1 for tile positions).  Returns false if the geometry needs more
+// than 5 dims or a fixed run is not a consecutive tile-id range.
+bool build_side(const double2 *base, int nl, const std::vector<int> &pos_of_tile, const std::vector<int> &fid,
+                CUtensorMap &map, int (&first)[5], int (&len)[5], int *rank)
+{
+    const int tbits = (int)pos_of_tile.size();
+    std::vector<int> is_tile(nl, -1);
+    for (int b = 0; b < tbits; ++b) is_tile[pos_of_tile[b]] = b;
+    // ranks: tile bits ordered by position
+    {
+        std::vector<int> order(tbits);
+        for (int b = 0; b < tbits; ++b) order[b] = b;
+        std::sort(order.begin(), order.end(), [&](int x, int y) { return pos_of_tile[x] < pos_of_tile[y]; });
+        for (int r = 0; r < tbits; ++r) rank[order[r]] = r;
+    }
+    if (is_tile[0] < 0) return false;   // the innermost dim must be tile positions
+    cuuint64_t gdim[5], gstride[4];
+    cuuint32_t box[5], estr[5];
+    int nd = 0;
+    int p = 0;
+    while (p < nl) {
+        const bool tilep = is_tile[p] >= 0;
+        int q = p;
+        if (tilep) {
+            while (q < nl && is_tile[q] >= 0 && q - p < (nd == 0 ? 7 : 8)) ++q;
+        } else {
+            while (q < nl && is_tile[q] < 0 && fid[q] == fid[p] + (q - p)) ++q;
+        }
+        if (nd == 5) return false;
+        const int L = q - p;
+        if (nd == 0) {
+            gdim[0] = (cuuint64_t)2 << L;   // doubles
+            box[0] = 2u << L;
+        } else {
+            gdim[nd] = (cuuint64_t)1 << L;
+            box[nd] = tilep ? (1u << L) : 1u;
+            gstride[nd - 1] = (cuuint64_t)16 << p;
+        }
+        first[nd] = tilep ? 0 : fid[p];
+        len[nd] = tilep ? 0 : L;
+        ++nd;
+        p = q;
+    }
+    while (nd < 5) {
+        gdim[nd] = 1;
+        box[nd] = 1;
+        gstride[nd - 1] = (cuuint64_t)16 << nl;   // size-1 padding dims: any 16-B multiple
+        first[nd] = 0;
+        len[nd] = 0;
+        ++nd;
+    }
+    for (int d = 0; d < 5; ++d) estr[d] = 1;
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void *)base, gdim, gstride, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int NM>
+void launch_tma_nm(Handle *h, const CUtensorMap &im, const CUtensorMap &om, const TilePass &tp, const TmaArgs &ta)
+{
+    const size_t smem = (size_t)kStages * kTileBytes + 1024 * sizeof(double2) + kStages * sizeof(uint64_t);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_tile_tma<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    const uint64_t ntiles = 1ull << tp.nfix;
+    const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)h->num_sms);
+    prof_begin(h);
+    k_tile_tma<NM><<<grid, kThreads, smem, h->stream>>>(im, om, tp, ta, ntiles);
+    prof_end(h, "k_tile_tma", (1ull << (tp.tbits + tp.nfix)) * 32);
+}
+
+}  // namespace
+
+// Try the TMA path for a planned pass (tp as given to launch_tile_pass).
+// Returns false (nothing launched) when the geometry does not fit.
+bool launch_tile_pass_tma(Handle *h, const TilePass &tp_in, const double2 *in, double2 *out)
+{
+    if (tp_in.tbits != kTmaTileBits || getenv("QSIM_NO_TMA")) return false;
+    TilePass tp = tp_in;
+    finish_tile_pass(tp);
+    std::vector<int> fid_in(h->nl, -1), fid_out(h->nl, -1);
+    for (int f = 0; f < tp.nfix; ++f) {
+        fid_in[tp.fin_pos[f]] = f;
+        fid_out[tp.fout_pos[f]] = f;
+    }
+    std::vector<int> tin(tp.in_pos, tp.in_pos + tp.tbits), tout(tp.out_pos, tp.out_pos + tp.tbits);
+    CUtensorMap im, om;
+    TmaArgs ta;
+    std::memset(&ta, 0, sizeof ta);
+    if (!build_side(in, h->nl, tin, fid_in, im, ta.in_first, ta.in_len, ta.in_rank)) return false;
+    if (!build_side(out, h->nl, tout, fid_out, om, ta.out_first, ta.out_len, ta.out_rank)) return false;
+    switch (tp.nmaps) {
+    case 1: launch_tma_nm<1>(h, im, om, tp, ta); break;
+    case 2: launch_tma_nm<2>(h, im, om, tp, ta); break;
+    case 3: launch_tma_nm<3>(h, im, om, tp, ta); break;
+    case 4: launch_tma_nm<4>(h, im, om, tp, ta); break;
+    default: launch_tma_nm<5>(h, im, om, tp, ta); break;
+    }
+    return true;
+}
+
+}  // namespace qs

@@ -111,8 +111,12 @@ struct TilePass {
 };
 // in -> out (may alias when the pass does not move fixed bits between tiles)
 void launch_tile_pass(Handle *h, const TilePass &tp, const double2 *in, double2 *out);
-// host planner helpers (k_tile.cu): fill tp.map[] from tbits/a/in_pos/out_pos
+// host planner helpers (k_tile.cu): fill tp.map[] from tbits/a/in_pos/out_pos;
+// derived constants (swizzle masks, twiddle weights)
 void plan_tile_maps(TilePass &tp);
+void finish_tile_pass(TilePass &tp);
+// TMA-pipelined variant (k_tma.cu); false = geometry unsupported, nothing launched
+bool launch_tile_pass_tma(Handle *h, const TilePass &tp, const double2 *in, double2 *out);
 
 // --------------------------------------------------------------- handle
 struct Handle {
