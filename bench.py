@@ -227,6 +227,7 @@ def main():
     barrier()
     launches = Q.qsim_launch_count(h) - l0
     prof = Q.qsim_profile_json(h)
+    per_launch = prof.pop("_launches", [])
     Q.qsim_profile(h, False)
     clocks = sampler.stop()
     ms = e0.elapsed_time(e1) / args.steps
@@ -303,6 +304,7 @@ def main():
             "gpu_launches": launches,
             "clocks": clocks,
             "kernels": prof,
+            "step_launches_ms": [round(x[1], 4) for x in per_launch[: len(per_launch) // max(args.steps, 1)]],
         }
         print(json.dumps(line), flush=True)
     Q.qsim_destroy(h)

@@ -40,7 +40,7 @@ using namespace tile;
 // The pass kernel.  NM = number of register maps (compile time, so that all
 // per-map values live in registers and every slot index is static).
 template <int NM>
-__global__ void __launch_bounds__(256, 1) k_tile_pass(const __grid_constant__ TilePass tp,
+__global__ void __launch_bounds__(1 << (kTileMaxBits - kRegBits), 1) k_tile_pass(const __grid_constant__ TilePass tp,
                                                    const double2 *in, double2 *out, uint64_t ntiles)
 {
     extern __shared__ double2 smem[];
@@ -162,7 +162,11 @@ void plan_tile_maps(TilePass &tp)
     const int nstage = (tp.a + kRegBits - 1) / kRegBits;
     for (int s = 0; s < nstage; ++s) {
         TileMap m;
+        // the last window ends at the last active wire (already transformed
+        // wires fill it up) so that passive tile bits stay thread bits: the
+        // gather / scatter maps then walk the lowest positions
         int w0 = s * kRegBits;
+        if (w0 + kRegBits > tp.a) w0 = std::max(0, tp.a - kRegBits);
         if (w0 + kRegBits > tp.tbits) w0 = tp.tbits - kRegBits;
         for (int k = 0; k < kRegBits; ++k) m.win[k] = w0 + k;
         m.ustart = s * kRegBits;
@@ -241,7 +245,8 @@ void launch_tile_pass(Handle *h, const TilePass &tp_in, const double2 *in, doubl
     case 2: launch_nm<2>(h, tp, in, out); break;
     case 3: launch_nm<3>(h, tp, in, out); break;
     case 4: launch_nm<4>(h, tp, in, out); break;
-    default: launch_nm<5>(h, tp, in, out); break;
+    case 5: launch_nm<5>(h, tp, in, out); break;
+    default: launch_nm<6>(h, tp, in, out); break;
     }
 }
 

@@ -37,7 +37,7 @@ using namespace tile;
 constexpr int kStages = 3;
 constexpr int kTmaTileBits = 12;                          // 4096 amplitudes
 constexpr uint32_t kTileBytes = 16u << kTmaTileBits;      // 64 KiB
-constexpr int kThreads = 256;
+constexpr int kThreads = 1 << (kTmaTileBits - kRegBits);
 
 struct TmaArgs {
     // per tensor-map dim d (0..4): first tile-id bit and length of the fixed
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int k = 0; k < NS; ++k) v[k] = buf[o[k]];
         }
-        tile_body<NM, true>(v, tp, tpart, stp, tab, buf, T, yt, Jt, twid, amask, sg);
+        tile_body<NM, false>(v, tp, tpart, stp, tab, buf, T, yt, Jt, twid, amask, sg);
         {
             uint32_t o[NS];
             o[0] = lout;
@@ -196,18 +196,208 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int b = 0; b < kRegBits; ++b)
 #pragma unroll
                 for (int q = 0; q < (1 << b); ++q) o[q | (1 << b)] = o[q] | pout[b];
-            tile_sync<true>();   // everybody is done reading this buffer
+            tile_sync<false>();   // everybody is done reading this buffer
 #pragma unroll
             for (int k = 0; k < NS; ++k) buf[o[k]] = v[k];
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        tile_sync<true>();
+        tile_sync<false>();
         if (tid == 0) {
             int c[5];
             coords(ta.out_first, ta.out_len, T, c);
             tma_store(&out_map, c, buf);
             // the previous tile's store has finished reading its buffer:
             // refill it with the tile two steps ahead
+            bulk_wait_read<1>();
+            const uint64_t Tn = T + (uint64_t)(kStages - 1) * gridDim.x;
+            if (Tn < ntiles) {
+                const int sn = (int)((j + kStages - 1) % kStages);
+                coords(ta.in_first, ta.in_len, Tn, c);
+                mbar_expect_tx(&full[sn], kTileBytes);
+                tma_load(bufs + (size_t)sn * (1u << kTmaTileBits), &in_map, c, &full[sn]);
+            }
+        }
+    }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// Specialised QFT / H pass: the number of active wires A, the direction and
+// H-only mode are compile-time, so the register windows, the wires each
+// window transforms and the R_1..R_3 rotations are static: no runtime
+// branches around the register updates (no phi moves) and the rotation by
+// -+i is a free swap/negation.  Window s holds tile bits [w0, w0+4) with
+// w0 = 4s, except the last window, which ends at wire A-1 (already
+// transformed wires fill it up, so the passive tile bits stay thread bits).
+template <int A, bool INV, bool HONLY>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_qft_tma(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
+              const __grid_constant__ TilePass tp, const __grid_constant__ TmaArgs ta, uint64_t ntiles)
+{
+    static_assert(kRegBits == 4 && kTmaTileBits == 12 && A >= 4 && A <= 10, "window layout");
+    constexpr int NST = (A + 3) / 4;   // register windows
+    constexpr double SG = INV ? -1.0 : 1.0;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    double2 *bufs = reinterpret_cast<double2 *>(smem_raw);
+    double2 *tab = bufs + kStages * (1u << kTmaTileBits);
+    uint64_t *full = reinterpret_cast<uint64_t *>(tab + 1024);
+    const uint32_t tid = threadIdx.x;
+
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (uint32_t k = tid; k < 1024; k += blockDim.x) {
+        double sn, cs;
+        sincospi((double)k / 512.0, &sn, &cs);
+        tab[k] = make_double2(cs, SG * sn);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&in_map) : "memory");
+        for (uint64_t q = 0; q < kStages - 1; ++q) {
+            const uint64_t T = blockIdx.x + q * gridDim.x;
+            if (T >= ntiles) break;
+            int c[5];
+            coords(ta.in_first, ta.in_len, T, c);
+            mbar_expect_tx(&full[q], kTileBytes);
+            tma_load(bufs + (size_t)q * (1u << kTmaTileBits), &in_map, c, &full[q]);
+        }
+    }
+
+    constexpr int tb = kTmaTileBits - kRegBits;
+    uint32_t tpart[NST], stp[NST];
+#pragma unroll
+    for (int m = 0; m < NST; ++m) {
+        tpart[m] = thread_part(tp.map[m], tb, tid);
+        stp[m] = swz(tpart[m]);
+    }
+    uint32_t lin = 0, lout = 0;
+    for (int t = 0; t < tb; ++t) {
+        lin |= ((tid >> t) & 1u) << ta.in_rank[tp.map[0].order[t]];
+        lout |= ((tid >> t) & 1u) << ta.out_rank[tp.map[NST - 1].order[t]];
+    }
+    uint32_t pin[kRegBits], pout[kRegBits];
+#pragma unroll
+    for (int b = 0; b < kRegBits; ++b) {
+        pin[b] = 1u << ta.in_rank[tp.map[0].win[b]];
+        pout[b] = 1u << ta.out_rank[tp.map[NST - 1].win[b]];
+    }
+    // table indices of the per-thread phases exp(i pi z_t / 2^u) (wires of
+    // windows >= 1: the earlier wires that are thread bits); tile-independent
+    uint32_t pidx[A > 4 ? A : 5];
+#pragma unroll
+    for (int u = 4; u < A; ++u) pidx[u] = ((tpart[u / 4] & ((1u << u) - 1u)) << (9 - u)) & 1023u;
+    const bool twid = !HONLY && (tp.n_et > 0 || tp.n_ef > 0 || tp.y_const != 0);
+    constexpr uint32_t amask = (1u << A) - 1u;
+    const uint32_t Jt = __brev(tpart[0] & amask) >> (32 - A);
+    uint64_t yt = 0;
+    for (int e = 0; e < tp.n_et; ++e) yt += (uint64_t)((tpart[0] >> tp.et_bit[e]) & 1u) << tp.et_w[e];
+
+    uint64_t j = 0;
+    for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x, ++j) {
+        const int st = (int)(j % kStages);
+        double2 *buf = bufs + (size_t)st * (1u << kTmaTileBits);
+        mbar_wait(&full[st], (uint32_t)((j / kStages) & 1));
+        double2 v[NS];
+        {
+            uint32_t o[NS];
+            o[0] = lin;
+#pragma unroll
+            for (int b = 0; b < kRegBits; ++b)
+#pragma unroll
+                for (int q = 0; q < (1 << b); ++q) o[q | (1 << b)] = o[q] | pin[b];
+#pragma unroll
+            for (int k = 0; k < NS; ++k) v[k] = buf[o[k]];
+        }
+        // twiddle exp(2 pi i Y J / 2^W) of the earlier blocks' R_d gates and
+        // the 2^(-A/2) normalisation: J = Jt + sum_b k_b 2^(A-1-b), so the
+        // window-bit factors are beta_3, beta_2 = beta_3^2, ...
+        if (twid) {
+            uint64_t Y = tp.y_const + yt;
+            for (int e = 0; e < tp.n_ef; ++e) Y += ((T >> tp.ef_bit[e]) & 1u) << tp.ef_w[e];
+            const double2 Ar = root_of_unity(Y * Jt, tp.W, tab, tp.tw);
+            const double2 As = make_double2(Ar.x * tp.scale, Ar.y * tp.scale);
+#pragma unroll
+            for (int k = 0; k < NS; ++k) v[k] = cmul(v[k], As);
+            double2 beta = root_of_unity(Y << (A - 4), tp.W, tab, tp.tw);
+#pragma unroll
+            for (int b = 3; b >= 0; --b) {
+#pragma unroll
+                for (int k = 0; k < NS; ++k)
+                    if (k & (1 << b)) v[k] = cmul(v[k], beta);
+                if (b) beta = cmul(beta, beta);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < NS; ++k) v[k] = make_double2(v[k].x * tp.scale, v[k].y * tp.scale);
+        }
+#pragma unroll
+        for (int s = 0; s < NST; ++s) {
+            if (s > 0) {
+                uint32_t o[NS];
+                o[0] = stp[s - 1];
+#pragma unroll
+                for (int b = 0; b < kRegBits; ++b)
+#pragma unroll
+                    for (int q = 0; q < (1 << b); ++q) o[q | (1 << b)] = o[q] ^ tp.wswz[s - 1][b];
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < NS; ++k) buf[o[k]] = v[k];
+                o[0] = stp[s];
+#pragma unroll
+                for (int b = 0; b < kRegBits; ++b)
+#pragma unroll
+                    for (int q = 0; q < (1 << b); ++q) o[q | (1 << b)] = o[q] ^ tp.wswz[s][b];
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < NS; ++k) v[k] = buf[o[k]];
+            }
+            const int w0 = (4 * s + 4 <= A) ? 4 * s : A - 4;
+#pragma unroll
+            for (int rb = 0; rb < 4; ++rb) {
+                const int u = w0 + rb;
+                if (u < 4 * s) continue;   // carried wire (already transformed)
+                if (!HONLY) {
+                    if (u >= 4) {
+                        const double2 P = tab[pidx[u]];
+#pragma unroll
+                        for (int k = 0; k < NS; ++k)
+                            if (k & (1 << rb)) v[k] = cmul(v[k], P);
+                    }
+#pragma unroll
+                    for (int k = 0; k < NS; ++k) {
+                        if (!(k & (1 << rb))) continue;
+#pragma unroll
+                        for (int r2 = 0; r2 < rb; ++r2)
+                            if (k & (1 << r2)) v[k] = rot_c<INV>(v[k], rb - r2);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < NS; ++k) {
+                    if (k & (1 << rb)) continue;
+                    const double2 x = v[k], y = v[k | (1 << rb)];
+                    v[k] = make_double2(x.x + y.x, x.y + y.y);
+                    v[k | (1 << rb)] = make_double2(x.x - y.x, x.y - y.y);
+                }
+            }
+        }
+        {
+            uint32_t o[NS];
+            o[0] = lout;
+#pragma unroll
+            for (int b = 0; b < kRegBits; ++b)
+#pragma unroll
+                for (int q = 0; q < (1 << b); ++q) o[q | (1 << b)] = o[q] | pout[b];
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < NS; ++k) buf[o[k]] = v[k];
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            int c[5];
+            coords(ta.out_first, ta.out_len, T, c);
+            tma_store(&out_map, c, buf);
             bulk_wait_read<1>();
             const uint64_t Tn = T + (uint64_t)(kStages - 1) * gridDim.x;
             if (Tn < ntiles) {
@@ -321,6 +511,31 @@ void launch_tma_nm(Handle *h, const CUtensorMap &im, const CUtensorMap &om, cons
     prof_end(h, "k_tile_tma", (1ull << (tp.tbits + tp.nfix)) * 32);
 }
 
+template <int A, bool INV, bool HONLY>
+void launch_fixed(Handle *h, const CUtensorMap &im, const CUtensorMap &om, const TilePass &tp, const TmaArgs &ta)
+{
+    const size_t smem = (size_t)kStages * kTileBytes + 1024 * sizeof(double2) + kStages * sizeof(uint64_t);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_qft_tma<A, INV, HONLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    const uint64_t ntiles = 1ull << tp.nfix;
+    const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)h->num_sms);
+    prof_begin(h);
+    k_qft_tma<A, INV, HONLY><<<grid, kThreads, smem, h->stream>>>(im, om, tp, ta, ntiles);
+    prof_end(h, "k_qft_tma", (1ull << (tp.tbits + tp.nfix)) * 32);
+}
+
+template <int A>
+bool launch_fixed_a(Handle *h, const CUtensorMap &im, const CUtensorMap &om, const TilePass &tp, const TmaArgs &ta)
+{
+    if (tp.hadamard_only) launch_fixed<A, false, true>(h, im, om, tp, ta);
+    else if (tp.inverse) launch_fixed<A, true, false>(h, im, om, tp, ta);
+    else launch_fixed<A, false, false>(h, im, om, tp, ta);
+    return true;
+}
+
 }  // namespace
 
 // Try the TMA path for a planned pass (tp as given to launch_tile_pass).
@@ -341,12 +556,27 @@ bool launch_tile_pass_tma(Handle *h, const TilePass &tp_in, const double2 *in, d
     std::memset(&ta, 0, sizeof ta);
     if (!build_side(in, h->nl, tin, fid_in, im, ta.in_first, ta.in_len, ta.in_rank)) return false;
     if (!build_side(out, h->nl, tout, fid_out, om, ta.out_first, ta.out_len, ta.out_rank)) return false;
+    // specialised kernel: 4..10 active wires, windows as planned, early tile
+    // bits outside window 0
+    const int nst = (tp.a + 3) / 4;
+    if (!getenv("QSIM_NO_FIXED") && tp.a >= 4 && tp.a <= 10 && tp.nmaps == nst && tp.twiddle_fast) {
+        switch (tp.a) {
+        case 4: return launch_fixed_a<4>(h, im, om, tp, ta);
+        case 5: return launch_fixed_a<5>(h, im, om, tp, ta);
+        case 6: return launch_fixed_a<6>(h, im, om, tp, ta);
+        case 7: return launch_fixed_a<7>(h, im, om, tp, ta);
+        case 8: return launch_fixed_a<8>(h, im, om, tp, ta);
+        case 9: return launch_fixed_a<9>(h, im, om, tp, ta);
+        default: return launch_fixed_a<10>(h, im, om, tp, ta);
+        }
+    }
     switch (tp.nmaps) {
     case 1: launch_tma_nm<1>(h, im, om, tp, ta); break;
     case 2: launch_tma_nm<2>(h, im, om, tp, ta); break;
     case 3: launch_tma_nm<3>(h, im, om, tp, ta); break;
     case 4: launch_tma_nm<4>(h, im, om, tp, ta); break;
-    default: launch_tma_nm<5>(h, im, om, tp, ta); break;
+    case 5: launch_tma_nm<5>(h, im, om, tp, ta); break;
+    default: launch_tma_nm<6>(h, im, om, tp, ta); break;
     }
     return true;
 }

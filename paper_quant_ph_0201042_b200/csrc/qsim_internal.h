@@ -77,7 +77,7 @@ void launch_grover(Handle *h, uint64_t mark_local, int mark_rank, int iters, dou
 // folded into the store).  With a = 0 the pass is a pure bit permutation.
 constexpr int kTileMaxBits = 12;   // <= 4096 amplitudes = 64 KiB of smem
 constexpr int kRegBits = 4;        // 16 amplitudes per thread
-constexpr int kMaxMaps = 5;
+constexpr int kMaxMaps = 6;
 
 struct TileMap {
     int win[kRegBits];             // tile bits held in registers (slot bit b <-> tile bit win[b])

@@ -47,6 +47,21 @@ __device__ __forceinline__ double2 root_of_unity(uint64_t t, int W, const double
     return p;
 }
 
+// compile-time-direction rotation c * exp(+-i pi / 2^d), d = 1, 2, 3
+template <bool INV>
+__device__ __forceinline__ double2 rot_c(double2 c, int d)
+{
+    if (d == 1) return INV ? make_double2(c.y, -c.x) : make_double2(-c.y, c.x);
+    if (d == 2) {
+        const double r = 0.70710678118654752440;
+        return INV ? make_double2((c.x + c.y) * r, (c.y - c.x) * r) : make_double2((c.x - c.y) * r, (c.y + c.x) * r);
+    }
+    return cmul(c, make_double2(0.92387953251128675613, INV ? -0.38268343236508977173 : 0.38268343236508977173));
+}
+
+__device__ __forceinline__ void tile_store(double2 *buf, uint32_t i, double2 v) { buf[i] = v; }
+__device__ __forceinline__ double2 tile_load(const double2 *buf, uint32_t i) { return buf[i]; }
+
 // c * exp(+-i pi / 2^d) for d = 1, 2, 3 (sg = +-1: direction of the transform)
 __device__ __forceinline__ double2 rot(double2 c, int d, double sg)
 {
