@@ -1,0 +1,124 @@
+#!/usr/bin/env python3
+"""Time every BASELINE.json config through the C-ABI on one GPU.
+
+Prints one JSON line per config: circuit time (CUDA events on the library's
+stream, state resident in HBM), per-kernel device time from the library's
+own profiler, and the effective per-gate bandwidth of the unfused gate model.
+Not the driver's bench (bench.py times configs[2]); this is the evidence
+table for DESIGN.md §7.  Usage: python tools/bench_configs.py [cfg ...]
+"""
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_quant_ph_0201042_b200 import qsim as Q  # noqa: E402
+from paper_quant_ph_0201042_b200 import workloads as W  # noqa: E402
+
+
+def timed(h, fn, reps=1):
+    stream = torch.cuda.ExternalStream(Q.qsim_get_stream(h))
+    Q.qsim_profile(h, True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record(stream)
+    out = None
+    for _ in range(reps):
+        out = fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / reps
+    prof = Q.qsim_profile_json(h)
+    prof.pop("_launches", None)
+    Q.qsim_profile(h, False)
+    return e0.elapsed_time(e1) / reps, wall * 1e3, prof, out
+
+
+def report(name, n, ms, wall_ms, prof, gate_bytes=None, extra=None):
+    line = {"config": name, "n": n, "device_ms": round(ms, 4), "wall_ms": round(wall_ms, 4),
+            "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 4),
+                            "GBps": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] else None}
+                        for k, v in prof.items()}}
+    if gate_bytes:
+        line["effective_GBps_per_gate"] = round(gate_bytes / (ms * 1e-3) / 1e9, 1)
+    if extra:
+        line.update(extra)
+    print(json.dumps(line), flush=True)
+
+
+def cfg0():
+    h = Q.qsim_create(10)
+    W.run_cfg0(h, 10, 1, 200)     # warm-up
+    ms, wall, prof, _ = timed(h, lambda: W.run_cfg0(h, 10, 1, 200), reps=3)
+    report("configs[0] random circuit n=10, 200 gates", 10, ms, wall, prof)
+    Q.qsim_destroy(h)
+
+
+def cfg1():
+    n = 20
+    h = Q.qsim_create(n)
+    W.run_cfg1(h, n, 2, 10)
+    ms, wall, prof, out = timed(h, lambda: W.run_cfg1(h, n, 2))
+    k, trace = out
+    gb = 804 * (2 * n + 2) * (1 << (n + 5)) / 2   # literal: 2n H sweeps per iteration (+ flips)
+    report("configs[1] Grover n=20, 804 iterations", n, ms, wall, prof, gb,
+           {"P_final": float(trace[-1]), "per_iteration_us": round(ms * 1e3 / 804, 3)})
+    Q.qsim_destroy(h)
+
+
+def cfg2(n=28):
+    h = Q.qsim_create(n)
+    Q.qsim_init_gaussian(h, 3)
+    Q.qsim_qft(h, 0, n, False)
+    ms, wall, prof, _ = timed(h, lambda: Q.qsim_qft(h, 0, n, False), reps=5)
+    gb = n * (1 << (n + 5)) + n * (n - 1) // 2 * (1 << (n + 3)) + n // 2 * (1 << (n + 4))
+    report(f"configs[2] QFT n={n}", n, ms, wall, prof, gb)
+    Q.qsim_destroy(h)
+
+
+def cfg3(sigma):
+    ne, nw = 20, 10
+    h = Q.qsim_create(ne + nw)
+    ms, wall, prof, P = timed(h, lambda: W.run_cfg3(h, ne, nw, 1007, 4, sigma))
+    n = ne + nw
+    gb = (2 * ne) * (1 << (n + 5)) + ne * (ne - 1) // 2 * (1 << (n + 3)) + ne // 2 * (1 << (n + 4)) \
+        + (1 << (n + 5))
+    report(f"configs[3] Shor N=1007 n=30 sigma={sigma}", n, ms, wall, prof, gb,
+           {"P_sum": float(P.sum()), "P_max": float(P.max())})
+    Q.qsim_destroy(h)
+
+
+def cfg4(n=32, layers=20):
+    h = Q.qsim_create(n)
+    ms, wall, prof, ev = timed(h, lambda: W.run_cfg4(h, n, layers, 5, 1e-3, 1e-4))
+    gates = layers * (n + (n - 1) // 2)
+    report(f"configs[4] noisy brickwork n={n} layers={layers}", n, ms, wall, prof,
+           layers * n * (1 << (n + 5)) + layers * ((n - 1) // 2) * (1 << (n + 4)),
+           {"events": ev, "gates": gates})
+    Q.qsim_destroy(h)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["0", "1", "2", "3", "3n", "4s"]
+    for w in which:
+        if w == "0":
+            cfg0()
+        elif w == "1":
+            cfg1()
+        elif w == "2":
+            cfg2()
+        elif w == "3":
+            cfg3(0.0)
+        elif w == "3n":
+            cfg3(1e-3)
+        elif w == "4s":
+            cfg4(26, 20)
+        elif w == "4":
+            cfg4(32, 20)
