@@ -109,6 +109,12 @@ int qsim_sync(qsim_t *h);
  * can record CUDA events on it (plumbing for timing; do not destroy it). */
 void *qsim_get_stream(qsim_t *h);
 
+/* Gate fusion (default on for shards of >= 2^9 amplitudes): single-qubit
+ * and controlled gates are queued and applied as fused tile passes (one HBM
+ * read + write for a run of gates) when anything else is called or at
+ * qsim_sync.  enable = 0 runs every gate as its own kernel (flushes first). */
+int qsim_set_fusion(qsim_t *h, int enable);
+
 /* Per-launch profiling: with enable = 1 every kernel launch of h is
  * bracketed by CUDA events on h's stream (records are reset by each call).
  * qsim_profile_json synchronises and returns, aggregated per kernel name,

@@ -211,31 +211,53 @@ bool local_controls(const Handle *h, uint64_t cmask, uint64_t cvals, uint64_t &l
 
 bool is_diag(const double2 U[4]) { return U[1].x == 0 && U[1].y == 0 && U[2].x == 0 && U[2].y == 0; }
 
-// Core gate application on logical target q with logical controls.
+// Immediate (unfused) application of a queued op.
+void run_op_now(Handle *h, const QOp &op)
+{
+    if (op.diag) {
+        if (op.tpos >= 0) launch_apply_diag(h, op.tpos, op.cmask, op.cval, op.u[0], op.u[3]);
+        else if (!(op.u[3].x == 1.0 && op.u[3].y == 0.0)) launch_phase_mask(h, op.cmask, op.cval, op.u[3]);
+    } else {
+        launch_apply_2x2(h, op.tpos, op.cmask, op.cval, op.u);
+    }
+}
+
+// Core gate application on logical target q with logical controls: the gate
+// is translated to physical local positions (rank-bit controls / targets are
+// resolved here) and queued; the queue is fused into tile passes at the next
+// flush (or run immediately when fusion is off / the shard is tiny).
 int apply_gate(Handle *h, uint64_t cmask, uint64_t cvals, int q, const double2 U[4])
 {
-    if (is_diag(U)) {
-        // diagonal gates need no communication: global target bit is a rank bit
-        uint64_t lm, lv;
-        if (!local_controls(h, cmask, cvals, lm, lv)) return QSIM_OK;
-        const int p = h->pos[q];
-        if (p < h->nl) {
-            launch_apply_diag(h, p, lm, lv, U[0], U[3]);
-        } else {
-            const int b = (h->rank >> (p - h->nl)) & 1;
-            const double2 d = b ? U[3] : U[0];
-            if (!(d.x == 1.0 && d.y == 0.0)) launch_phase_mask(h, lm, lv, d);
-        }
-        return after_launch(h, "diagonal gate");
-    }
-    if (!is_local(h, q)) {
-        int rc = dist_make_local(h, std::vector<int>{q});
-        if (rc) return rc;
+    QOp op;
+    op.diag = is_diag(U);
+    for (int k = 0; k < 4; ++k) op.u[k] = U[k];
+    if (!op.diag && !is_local(h, q)) {
+        if (int rc = flush_queue(h)) return rc;
+        if (int rc = dist_make_local(h, std::vector<int>{q})) return rc;
     }
     uint64_t lm, lv;
     if (!local_controls(h, cmask, cvals, lm, lv)) return QSIM_OK;
-    launch_apply_2x2(h, h->pos[q], lm, lv, U);
-    return after_launch(h, "2x2 gate");
+    op.cmask = lm;
+    op.cval = lv;
+    const int p = h->pos[q];
+    if (p < h->nl) {
+        op.tpos = p;
+    } else {
+        // diagonal gate on a rank bit: a constant phase under the controls
+        const int b = (h->rank >> (p - h->nl)) & 1;
+        const double2 d = b ? U[3] : U[0];
+        if (d.x == 1.0 && d.y == 0.0) return QSIM_OK;
+        op.tpos = -1;
+        op.u[0] = make_double2(1.0, 0.0);
+        op.u[3] = d;
+    }
+    if (h->fuse && h->nl >= 9) {
+        h->queue.push_back(op);
+        if (h->queue.size() >= 4096) return flush_queue(h);
+        return QSIM_OK;
+    }
+    run_op_now(h, op);
+    return after_launch(h, "gate");
 }
 
 int check_qubit(Handle *h, int q)
@@ -383,6 +405,175 @@ int fused_range(Handle *h, int lo, int m, int qft, int inverse)
 }
 
 }  // namespace
+
+// ---------------------------------------------------------------- gate queue
+// Pack the queued gates into fused passes (k_ops.cu) and run them.
+//
+// Greedy, order-preserving up to commutation of gates on disjoint qubits:
+// a pass collects, in queue order, every gate whose non-diagonal target is
+// (or can still become) one of its <= amax "active" positions; a gate that
+// cannot join blocks all of its positions for the rest of the scan, so no
+// later gate on those positions overtakes it.  The tile = active positions +
+// the lowest other positions (passive, for contiguous runs), <= 12 bits.
+int qs::flush_queue(Handle *h)
+{
+    if (h->queue.empty()) return QSIM_OK;
+    std::vector<QOp> rem;
+    rem.swap(h->queue);
+    const int nl = h->nl;
+    const int tbits = std::min(kTileMaxBits, nl);
+    const int amax = nl <= kTileMaxBits ? nl : kTileMaxBits - 3;
+    std::vector<GOp> hops;
+    while (!rem.empty()) {
+        std::vector<int> act;                 // active positions (tile bits 0..)
+        std::vector<char> is_act(nl, 0), blocked(nl, 0);
+        std::vector<QOp> take, left;
+        for (const QOp &op : rem) {
+            uint64_t touch = op.cmask;
+            if (op.tpos >= 0) touch |= 1ull << op.tpos;
+            bool blk = false;
+            for (int p = 0; p < nl; ++p)
+                if (((touch >> p) & 1) && blocked[p]) blk = true;
+            bool ok = !blk;
+            if (ok && !op.diag && !is_act[op.tpos]) {
+                if ((int)act.size() < amax) { act.push_back(op.tpos); is_act[op.tpos] = 1; }
+                else ok = false;
+            }
+            if (ok) take.push_back(op);
+            else {
+                left.push_back(op);
+                for (int p = 0; p < nl; ++p)
+                    if ((touch >> p) & 1) blocked[p] = 1;
+            }
+        }
+        rem.swap(left);
+        // tile: active + passive lowest positions
+        std::vector<int> tile(act);
+        std::vector<int> tbit_of(nl, -1);
+        for (size_t b = 0; b < act.size(); ++b) tbit_of[act[b]] = (int)b;
+        for (int p = 0; p < nl && (int)tile.size() < tbits; ++p)
+            if (tbit_of[p] < 0) { tbit_of[p] = (int)tile.size(); tile.push_back(p); }
+        OpsPass P;
+        std::memset(&P, 0, sizeof P);
+        P.tbits = tbits;
+        for (int b = 0; b < tbits; ++b) P.in_pos[b] = tile[b];
+        std::vector<int> fix_of(nl, -1);
+        for (int p = 0; p < nl; ++p)
+            if (tbit_of[p] < 0) { fix_of[p] = P.nfix; P.fin_pos[P.nfix++] = p; }
+        // segments: a register window of 4 tile bits covering the next dense targets
+        std::vector<std::vector<int>> wins;
+        std::vector<int> seg_of(take.size());
+        {
+            std::vector<int> cur;
+            for (size_t i = 0; i < take.size(); ++i) {
+                if (!take[i].diag) {
+                    const int t = tbit_of[take[i].tpos];
+                    if (std::find(cur.begin(), cur.end(), t) == cur.end()) {
+                        if (!wins.empty() || !cur.empty()) {}
+                        // new window: this target + the next distinct dense targets
+                        cur.clear();
+                        cur.push_back(t);
+                        for (size_t j = i + 1; j < take.size() && (int)cur.size() < kRegBits; ++j) {
+                            if (take[j].diag) continue;
+                            const int t2 = tbit_of[take[j].tpos];
+                            if (std::find(cur.begin(), cur.end(), t2) == cur.end()) cur.push_back(t2);
+                        }
+                        for (int b = 0; b < tbits && (int)cur.size() < kRegBits; ++b)
+                            if (std::find(cur.begin(), cur.end(), b) == cur.end() && tile[b] >= kRegBits) cur.push_back(b);
+                        for (int b = 0; b < tbits && (int)cur.size() < kRegBits; ++b)
+                            if (std::find(cur.begin(), cur.end(), b) == cur.end()) cur.push_back(b);
+                        std::sort(cur.begin(), cur.end());
+                        wins.push_back(cur);
+                    }
+                }
+                if (wins.empty()) {
+                    std::vector<int> w;
+                    for (int b = tbits - kRegBits; b < tbits; ++b) w.push_back(b);
+                    wins.push_back(w);
+                }
+                seg_of[i] = (int)wins.size() - 1;
+            }
+            if (wins.empty()) {
+                std::vector<int> w;
+                for (int b = tbits - kRegBits; b < tbits; ++b) w.push_back(b);
+                wins.push_back(w);
+            }
+        }
+        // split into chunks of <= kMaxSegs segments (each chunk = one launch)
+        size_t op0 = 0;
+        for (size_t s0 = 0; s0 < wins.size(); s0 += kMaxSegs) {
+            const size_t s1 = std::min(wins.size(), s0 + kMaxSegs);
+            P.nseg = (int)(s1 - s0);
+            hops.clear();
+            size_t i = op0;
+            for (size_t s = s0; s < s1; ++s) {
+                OpsSeg &sg = P.seg[s - s0];
+                for (int b = 0; b < kRegBits; ++b) sg.map.win[b] = wins[s][b];
+                // thread order: ascending tile bits, first/last segment by position
+                std::vector<int> rest;
+                for (int b = 0; b < tbits; ++b)
+                    if (std::find(wins[s].begin(), wins[s].end(), b) == wins[s].end()) rest.push_back(b);
+                if (s == s0 || s + 1 == s1)
+                    std::stable_sort(rest.begin(), rest.end(), [&](int x, int y) { return tile[x] < tile[y]; });
+                for (size_t t = 0; t < rest.size(); ++t) sg.map.order[t] = rest[t];
+                sg.op_begin = (int)hops.size();
+                for (; i < take.size() && seg_of[i] == (int)s; ++i) {
+                    const QOp &q = take[i];
+                    GOp g;
+                    std::memset(&g, 0, sizeof g);
+                    g.kind = q.diag ? GOP_DIAG : GOP_DENSE;
+                    for (int k = 0; k < 4; ++k) g.u[k] = q.u[k];
+                    g.rb = 0;
+                    g.tbit = -1;
+                    g.fbit = -1;
+                    if (!q.diag) {
+                        const int t = tbit_of[q.tpos];
+                        for (int b = 0; b < kRegBits; ++b)
+                            if (wins[s][b] == t) g.rb = b;
+                    } else if (q.tpos >= 0) {
+                        if (tbit_of[q.tpos] >= 0) g.tbit = tbit_of[q.tpos];
+                        else g.fbit = fix_of[q.tpos];
+                    }
+                    for (int p = 0; p < nl; ++p) {
+                        if (!((q.cmask >> p) & 1)) continue;
+                        const uint64_t want = (q.cval >> p) & 1;
+                        if (tbit_of[p] >= 0) {
+                            g.cm |= 1u << tbit_of[p];
+                            g.cv |= (uint32_t)want << tbit_of[p];
+                        } else {
+                            g.fm |= 1ull << fix_of[p];
+                            g.fv |= want << fix_of[p];
+                        }
+                    }
+                    hops.push_back(g);
+                }
+                sg.op_end = (int)hops.size();
+            }
+            op0 = i;
+            P.nops = (int)hops.size();
+            if (hops.size() > h->d_ops_cap) {
+                if (h->d_ops) {
+                    cudaStreamSynchronize(h->stream);
+                    cudaFree(h->d_ops);
+                }
+                h->d_ops_cap = std::max<size_t>(hops.size(), 4096);
+                if (cudaMalloc(&h->d_ops, h->d_ops_cap * sizeof(GOp)) != cudaSuccess) {
+                    cudaGetLastError();
+                    h->d_ops = nullptr;
+                    h->d_ops_cap = 0;
+                    h->poisoned = 1;
+                    return fail(h, QSIM_ENOMEM, "gate-list buffer");
+                }
+            }
+            // the op list is copied on the stream; the host vector lives until
+            // the copy has been enqueued and is synchronous for pageable memory
+            cudaMemcpyAsync(h->d_ops, hops.data(), hops.size() * sizeof(GOp), cudaMemcpyHostToDevice, h->stream);
+            launch_ops_pass(h, P, h->d_ops);
+            if (int rc = after_launch(h, "fused gate pass")) return rc;
+        }
+    }
+    return QSIM_OK;
+}
 
 // Local bit permutation pass: new position of old local position p is perm[p].
 void qs::permute_local(Handle *h, const std::vector<int> &perm)
@@ -563,9 +754,18 @@ void qsim_destroy(qsim_t *h)
 
 void *qsim_get_stream(qsim_t *h) { return h ? (void *)h->stream : nullptr; }
 
+int qsim_set_fusion(qsim_t *h, int enable)
+{
+    QS_CHECK_HANDLE(h);
+    if (int rc = flush_queue(h)) return rc;
+    h->fuse = enable ? 1 : 0;
+    return QSIM_OK;
+}
+
 int qsim_profile(qsim_t *h, int enable)
 {
     QS_CHECK_HANDLE(h);
+    if (int rc = flush_queue(h)) return rc;
     cudaStreamSynchronize(h->stream);
     h->prof.clear();
     h->ev_used = 0;
@@ -577,6 +777,7 @@ int qsim_profile(qsim_t *h, int enable)
 const char *qsim_profile_json(qsim_t *h)
 {
     if (!h) return "{}";
+    flush_queue(h);
     cudaStreamSynchronize(h->stream);
     struct Agg { double ms = 0; uint64_t bytes = 0, n = 0; };
     std::vector<std::pair<std::string, Agg>> agg;
@@ -613,6 +814,7 @@ const char *qsim_profile_json(qsim_t *h)
 int qsim_sync(qsim_t *h)
 {
     QS_CHECK_HANDLE(h);
+    if (int rc = flush_queue(h)) return rc;
     return check_cuda(h, cudaStreamSynchronize(h->stream), "qsim_sync");
 }
 
@@ -620,6 +822,7 @@ int qsim_sync(qsim_t *h)
 int qsim_set_basis(qsim_t *h, uint64_t idx)
 {
     QS_CHECK_HANDLE(h);
+    h->queue.clear();   // the state is overwritten
     if (h->n < 64 && idx >> h->n) return fail(h, QSIM_ERANGE, "basis index >= 2^n");
     for (int q = 0; q < h->n; ++q) h->pos[q] = h->n - 1 - q;
     launch_zero(h);
@@ -630,6 +833,7 @@ int qsim_set_basis(qsim_t *h, uint64_t idx)
 int qsim_init_gaussian(qsim_t *h, uint64_t seed)
 {
     QS_CHECK_HANDLE(h);
+    h->queue.clear();   // the state is overwritten
     for (int q = 0; q < h->n; ++q) h->pos[q] = h->n - 1 - q;
     launch_init_gaussian(h, seed);
     double s = 0.0;
@@ -642,6 +846,7 @@ int qsim_init_gaussian(qsim_t *h, uint64_t seed)
 static int copy_state(qsim_t *h, uint64_t off, uint64_t cnt, qsim_c128 *host, bool to_dev)
 {
     QS_CHECK_HANDLE(h);
+    if (int rc = flush_queue(h)) return rc;
     const uint64_t dim = (uint64_t)1 << h->n;
     if (off > dim || cnt > dim - off) return fail(h, QSIM_ERANGE, "state slice outside [0, 2^n)");
     int rc = dist_canonicalize(h);
@@ -735,6 +940,7 @@ int qsim_swap(qsim_t *h, int q1, int q2)
 int qsim_hadamard(qsim_t *h, int lo, int m)
 {
     QS_CHECK_HANDLE(h);
+    if (int rc = flush_queue(h)) return rc;
     if (lo < 0 || m < 0 || lo + m > h->n) return fail(h, QSIM_ERANGE, "range outside [0, n)");
     if (m == 0) return QSIM_OK;
     if (h->nl >= 9 && m <= h->nl) return fused_range(h, lo, m, 0, 0);
@@ -748,6 +954,7 @@ int qsim_hadamard(qsim_t *h, int lo, int m)
 int qsim_qft(qsim_t *h, int lo, int m, int inverse)
 {
     QS_CHECK_HANDLE(h);
+    if (int rc = flush_queue(h)) return rc;
     if (lo < 0 || m < 0 || lo + m > h->n) return fail(h, QSIM_ERANGE, "range outside [0, n)");
     if (m == 0) return QSIM_OK;
     const double sgn = inverse ? -1.0 : 1.0;
@@ -790,6 +997,7 @@ int qsim_qft(qsim_t *h, int lo, int m, int inverse)
 int qsim_phase_flip(qsim_t *h, uint64_t idx)
 {
     QS_CHECK_HANDLE(h);
+    if (int rc = flush_queue(h)) return rc;
     if (h->n < 64 && idx >> h->n) return fail(h, QSIM_ERANGE, "index >= 2^n");
     // physical location of logical index idx
     uint64_t phys = 0;
@@ -803,6 +1011,7 @@ int qsim_phase_flip(qsim_t *h, uint64_t idx)
 int qsim_grover(qsim_t *h, uint64_t mark, int iters, double *trace)
 {
     QS_CHECK_HANDLE(h);
+    if (int rc = flush_queue(h)) return rc;
     if (h->n < 64 && mark >> h->n) return fail(h, QSIM_ERANGE, "mark >= 2^n");
     if (iters < 0) return fail(h, QSIM_EINVAL, "iters < 0");
     if (h->world > 1) return fail(h, QSIM_EINVAL, "qsim_grover runs on a single-GPU handle");
@@ -835,6 +1044,7 @@ static uint64_t gcd64(uint64_t a, uint64_t b)
 int qsim_apply_perm(qsim_t *h, const qsim_perm_t *f)
 {
     QS_CHECK_HANDLE(h);
+    if (int rc = flush_queue(h)) return rc;
     if (!f) return fail(h, QSIM_EINVAL, "null permutation");
     if (f->kind < 0 || f->kind > 2) return fail(h, QSIM_EINVAL, "unknown permutation kind");
     if (f->m < 1 || f->lo < 0 || f->lo + f->m > h->n) return fail(h, QSIM_ERANGE, "target register outside [0, n)");
@@ -940,6 +1150,7 @@ int qsim_inject_errors(qsim_t *h, uint64_t seed, const qsim_noise_t *model, qsim
 int qsim_norm(qsim_t *h, double *out)
 {
     QS_CHECK_HANDLE(h);
+    if (int rc = flush_queue(h)) return rc;
     if (!out) return QSIM_EINVAL;
     launch_norm(h, h->d_red);
     if (int rc = after_launch(h, "norm")) return rc;
@@ -958,6 +1169,7 @@ int qsim_norm(qsim_t *h, double *out)
 int qsim_probs(qsim_t *h, int lo, int m, double *out)
 {
     QS_CHECK_HANDLE(h);
+    if (int rc = flush_queue(h)) return rc;
     if (!out) return QSIM_EINVAL;
     if (lo < 0 || m < 1 || m > 26 || lo + m > h->n) return fail(h, QSIM_ERANGE, "range outside [0, n) or m > 26");
     if (int rc = dist_canonicalize(h)) return rc;
@@ -1006,6 +1218,7 @@ int qsim_probs(qsim_t *h, int lo, int m, double *out)
 int qsim_prob_index(qsim_t *h, uint64_t idx, double *out)
 {
     QS_CHECK_HANDLE(h);
+    if (int rc = flush_queue(h)) return rc;
     if (!out) return QSIM_EINVAL;
     if (h->n < 64 && idx >> h->n) return fail(h, QSIM_ERANGE, "index >= 2^n");
     if (int rc = dist_canonicalize(h)) return rc;
@@ -1028,6 +1241,7 @@ int qsim_prob_index(qsim_t *h, uint64_t idx, double *out)
 int qsim_measure(qsim_t *h, double r, uint64_t *idx)
 {
     QS_CHECK_HANDLE(h);
+    if (int rc = flush_queue(h)) return rc;
     if (!idx) return QSIM_EINVAL;
     if (!(r >= 0.0 && r < 1.0)) return fail(h, QSIM_EINVAL, "r must be in [0, 1)");
     if (int rc = dist_canonicalize(h)) return rc;

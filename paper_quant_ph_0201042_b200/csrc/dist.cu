@@ -150,6 +150,7 @@ static int run_steps(Handle *h, const std::vector<Step> &steps)
 int dist_make_local(Handle *h, const std::vector<int> &need)
 {
     if (h->world == 1) return QSIM_OK;
+    if (int rc = flush_queue(h)) return rc;
     std::vector<int> pos(h->pos, h->pos + h->n);
     std::vector<Step> steps;
     if (plan_make_local(h->n, h->nl, pos, need, steps)) return fail(h, QSIM_EINVAL, "too many qubits requested local");
@@ -158,6 +159,7 @@ int dist_make_local(Handle *h, const std::vector<int> &need)
 
 int dist_canonicalize(Handle *h)
 {
+    if (int rc = flush_queue(h)) return rc;
     if (h->world > 1) {
         std::vector<int> pos(h->pos, h->pos + h->n);
         std::vector<Step> steps;

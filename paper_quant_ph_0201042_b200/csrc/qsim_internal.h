@@ -118,6 +118,41 @@ void finish_tile_pass(TilePass &tp);
 // TMA-pipelined variant (k_tma.cu); false = geometry unsupported, nothing launched
 bool launch_tile_pass_tma(Handle *h, const TilePass &tp, const double2 *in, double2 *out);
 
+// Fused gate-list passes (k_ops.cu): ops of one pass, applied per tile.
+enum { GOP_DENSE = 0, GOP_DIAG = 1 };
+struct GOp {
+    int kind;          // GOP_DENSE / GOP_DIAG
+    int rb;            // dense: register bit of the target in its segment's window
+    int tbit;          // diag: tile bit of the target (used when fbit < 0 and tbit >= 0)
+    int fbit;          // diag: tile-id bit of a fixed target, or -1; tbit = fbit = -1: constant phase u[3]
+    uint32_t cm, cv;   // controls on tile bits (tile-index mask / values)
+    uint64_t fm, fv;   // controls on fixed bits (tile-id mask / values)
+    double2 u[4];      // dense U (u11 u12 u21 u22) or diag(u[0], u[3])
+};
+constexpr int kOpsSmem = 64;   // ops cached in shared memory per CTA
+constexpr int kMaxSegs = 48;
+struct OpsSeg {
+    TileMap map;       // register window + thread order
+    int op_begin, op_end;
+};
+struct OpsPass {
+    int tbits;
+    int in_pos[kTileMaxBits];   // tile bit -> local position (in place: same on output)
+    int nfix;
+    int fin_pos[kMaxFixedBits];
+    int nops, nseg;
+    OpsSeg seg[kMaxSegs];
+};
+void launch_ops_pass(Handle *h, const OpsPass &P, const GOp *d_ops);
+
+// A queued gate in physical local positions (api.cu gate queue).
+struct QOp {
+    int diag;          // 1: diagonal (u[1] = u[2] = 0)
+    int tpos;          // target local position; -1 for a constant phase (diag only)
+    uint64_t cmask, cval;   // controls on local positions
+    double2 u[4];
+};
+
 // --------------------------------------------------------------- handle
 struct Handle {
     int n = 0;              // qubits
@@ -154,6 +189,11 @@ struct Handle {
     size_t ev_used = 0;
     cudaEvent_t pending = nullptr;
     std::string prof_json;
+    // gate queue (fused into k_ops passes at the next flush)
+    std::vector<QOp> queue;
+    int fuse = 1;
+    GOp *d_ops = nullptr;
+    size_t d_ops_cap = 0;
 
     uint64_t local_dim() const { return (uint64_t)1 << nl; }
 };
@@ -181,6 +221,8 @@ int dist_make_local(Handle *h, const std::vector<int> &need);  // make logical q
 int dist_canonicalize(Handle *h);                                // pos[q] = n-1-q everywhere
 int dist_allgather_doubles(Handle *h, const double *d_in, double *d_out, size_t count);
 int dist_allreduce_sum_host(Handle *h, double *host, size_t count);  // fixed rank order
+// run every queued gate (fused passes); called before anything that reads or moves data
+int flush_queue(Handle *h);
 // local bit-permutation pass (api.cu): new position of old local position p is perm[p]
 void permute_local(Handle *h, const std::vector<int> &perm);
 

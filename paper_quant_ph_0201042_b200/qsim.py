@@ -105,6 +105,7 @@ _sig("qsim_prob_index", _i32, _H, _u64, C.POINTER(_f64))
 _sig("qsim_measure", _i32, _H, _f64, C.POINTER(_u64))
 _sig("qsim_philox_draw", None, _u64, _u32, _u64, _u32, _p)
 _sig("qsim_get_stream", _p, _H)
+_sig("qsim_set_fusion", _i32, _H, _i32)
 _sig("qsim_profile", _i32, _H, _i32)
 _sig("qsim_profile_json", C.c_char_p, _H)
 _sig("qsim_plan_make_local", _i32, _i32, _i32, _p, _p, _i32, _p, _i32)
@@ -164,6 +165,10 @@ def qsim_sync(h) -> None:
 
 def qsim_get_stream(h) -> int:
     return lib.qsim_get_stream(h) or 0
+
+
+def qsim_set_fusion(h, enable: bool) -> None:
+    _chk(h, lib.qsim_set_fusion(h, int(bool(enable))))
 
 
 def qsim_profile(h, enable: bool) -> None:

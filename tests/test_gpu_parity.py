@@ -379,3 +379,51 @@ def test_memory_bytes():
     assert Q.qsim_memory_bytes(20) == 16777216
     assert Q.qsim_memory_bytes(30) == 17179869184
     assert Q.qsim_memory_bytes(1) == 32
+
+
+# ------------------------------------------------------------------ gate fusion
+@pytest.mark.parametrize("n,ngates", [(9, 120), (13, 300), (17, 400), (20, 150)])
+def test_fused_gate_passes_match_oracle(reg, n, ngates):
+    """Random mix of dense, controlled (1-3 controls, both values), diagonal
+    and controlled-diagonal gates: the fused tile passes (gate queue) and the
+    unfused kernels both equal the oracle."""
+    rng = np.random.default_rng(1000 + n)
+    psi = rand_state(n, 50 + n)
+    hf = reg(n, psi)
+    hu = reg(n, psi)
+    Q.qsim_set_fusion(hu, False)
+    ref = psi.copy()
+    for _ in range(ngates):
+        q = int(rng.integers(n))
+        kind = rng.integers(4)
+        if kind == 0:
+            U = rand_mat(rng) / 1.5
+        elif kind == 1:
+            U = np.diag(np.exp(1j * rng.uniform(0, 6.3, 2)))
+        elif kind == 2:
+            a = O.haar_angles(7, int(rng.integers(1 << 20)))
+            U = O.mat_angles(O.HAAR, a)
+        else:
+            U = np.array([[0, 1], [1, 0]], complex)
+        others = [c for c in range(n) if c != q]
+        k = int(rng.integers(0, 4))
+        ctrl = rng.choice(others, size=k, replace=False) if k else []
+        mask = sum(1 << int(c) for c in ctrl)
+        vals = sum(int(rng.integers(2)) << int(c) for c in ctrl)
+        for h in (hf, hu):
+            Q.qsim_apply_ctrl(h, mask, vals, q, U) if mask else Q.qsim_apply_1q(h, q, U)
+        O.apply_ctrl(ref, mask, vals, q, U) if mask else O.apply_1q(ref, q, U)
+    assert maxdiff(get(hf, n), ref) < TOL
+    assert maxdiff(get(hu, n), ref) < TOL
+
+
+def test_fusion_is_a_single_pass_for_small_registers(reg):
+    """configs[0]: all 200 gates of the n = 10 circuit fuse into one launch."""
+    h = reg(10)
+    Q.qsim_sync(h)
+    l0 = Q.qsim_launch_count(h)
+    W.run_cfg0(h, n=10, seed=1, ngates=200)
+    Q.qsim_sync(h)
+    assert Q.qsim_launch_count(h) - l0 <= 3
+    ref, _, _ = O.cfg0(10, 1, 200)
+    assert maxdiff(get(h, 10), ref) < TOL
