@@ -87,6 +87,15 @@ int qsim_create(int n, int ngpus, qsim_t **out);
 int qsim_create_dist(int n, int world, int rank, int device, const void *nccl_id,
                      qsim_t **out);
 
+/* All `world` ranks in this process (world a power of two): one shard per
+ * rank on devices[r] (devices may be NULL: the current device for every
+ * rank; ranks may share a device).  The returned group handle accepts every
+ * call; each call runs on all ranks, shard exchanges are device-to-device
+ * copies (peer copies over NVLink between GPUs) instead of NCCL, and
+ * qsim_get_state / qsim_set_state address every slice.  Same layout and
+ * exchange plan as qsim_create_dist. */
+int qsim_create_group(int n, int world, const int *devices, qsim_t **out);
+
 /* Writes a fresh ncclUniqueId (128 bytes) into out128. */
 int qsim_nccl_unique_id(void *out128);
 

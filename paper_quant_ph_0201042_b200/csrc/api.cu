@@ -222,42 +222,59 @@ void run_op_now(Handle *h, const QOp &op)
     }
 }
 
-// Core gate application on logical target q with logical controls: the gate
-// is translated to physical local positions (rank-bit controls / targets are
-// resolved here) and queued; the queue is fused into tile passes at the next
-// flush (or run immediately when fusion is off / the shard is tiny).
-int apply_gate(Handle *h, uint64_t cmask, uint64_t cvals, int q, const double2 U[4])
+// A member's failure is reported on the handle the caller holds.
+int lift(Handle *top, const Ranks &R, int rc)
 {
-    QOp op;
-    op.diag = is_diag(U);
-    for (int k = 0; k < 4; ++k) op.u[k] = U[k];
-    if (!op.diag && !is_local(h, q)) {
-        if (int rc = flush_queue(h)) return rc;
-        if (int rc = dist_make_local(h, std::vector<int>{q})) return rc;
+    if (rc == QSIM_OK || R.size() == 1) return rc;
+    for (Handle *m : R) {
+        if (!m->err.empty()) top->err = m->err;
+        if (m->poisoned) top->poisoned = 1;
     }
-    uint64_t lm, lv;
-    if (!local_controls(h, cmask, cvals, lm, lv)) return QSIM_OK;
-    op.cmask = lm;
-    op.cval = lv;
-    const int p = h->pos[q];
-    if (p < h->nl) {
-        op.tpos = p;
-    } else {
-        // diagonal gate on a rank bit: a constant phase under the controls
-        const int b = (h->rank >> (p - h->nl)) & 1;
-        const double2 d = b ? U[3] : U[0];
-        if (d.x == 1.0 && d.y == 0.0) return QSIM_OK;
-        op.tpos = -1;
-        op.u[0] = make_double2(1.0, 0.0);
-        op.u[3] = d;
+    return rc;
+}
+
+// Core gate application on logical target q with logical controls, on every
+// rank of R: a non-diagonal gate on a rank-bit qubit first makes it local
+// (dist.cu); then each rank translates the gate to physical local positions
+// (controls on rank bits are decided per rank, a diagonal gate on a rank bit
+// becomes a constant phase) and queues it; the queue is fused into tile
+// passes at the next flush (or run at once when fusion is off / the shard is
+// tiny).
+int apply_gate(const Ranks &R, uint64_t cmask, uint64_t cvals, int q, const double2 U[4])
+{
+    const int diag = is_diag(U);
+    if (!diag && !is_local(R[0], q))
+        if (int rc = dist_make_local(R, std::vector<int>{q})) return rc;
+    for (Handle *h : R) {
+        QOp op;
+        op.diag = diag;
+        for (int k = 0; k < 4; ++k) op.u[k] = U[k];
+        uint64_t lm, lv;
+        if (!local_controls(h, cmask, cvals, lm, lv)) continue;
+        op.cmask = lm;
+        op.cval = lv;
+        const int p = h->pos[q];
+        if (p < h->nl) {
+            op.tpos = p;
+        } else {
+            // diagonal gate on a rank bit: a constant phase under the controls
+            const int b = (h->rank >> (p - h->nl)) & 1;
+            const double2 d = b ? U[3] : U[0];
+            if (d.x == 1.0 && d.y == 0.0) continue;
+            op.tpos = -1;
+            op.u[0] = make_double2(1.0, 0.0);
+            op.u[3] = d;
+        }
+        if (h->fuse && h->nl >= 9) {
+            h->queue.push_back(op);
+            if (h->queue.size() >= 4096)
+                if (int rc = flush_queue(h)) return rc;
+            continue;
+        }
+        run_op_now(h, op);
+        if (int rc = after_launch(h, "gate")) return rc;
     }
-    if (h->fuse && h->nl >= 9) {
-        h->queue.push_back(op);
-        if (h->queue.size() >= 4096) return flush_queue(h);
-        return QSIM_OK;
-    }
-    run_op_now(h, op);
-    return after_launch(h, "gate");
+    return QSIM_OK;
 }
 
 int check_qubit(Handle *h, int q)
@@ -298,12 +315,13 @@ TilePass make_pass(const Handle *h, const std::vector<int> &tile_pos, const std:
     return tp;
 }
 
+
 // Fused H / QFT on the wires [lo, lo+m) (logical).  qft = 0: Hadamard transform.
 //
 // Wires are cut into G blocks of <= amax consecutive wires; pass g applies
-// every gate of block g (see k_tile.cu).  A pass reads a tile of 2^12
-// amplitudes: the block's wires + the lowest other positions ("passive", so
-// the tile moves in runs of >= 2^(12-a) contiguous amplitudes).
+// every gate of block g (see k_tile.cu / k_tma.cu).  A pass reads tiles of
+// 2^12 amplitudes: the block's wires + the lowest other positions
+// ("passive", so a tile moves in runs of >= 2^(12-a) contiguous amplitudes).
 //
 // Single GPU, QFT: the closing swaps are folded into the stores with a
 // block-move layout (no extra pass).  Invariant before pass g (wires
@@ -314,92 +332,101 @@ TilePass make_pass(const Handle *h, const std::vector<int> &tile_pos, const std:
 // pass wire w sits at s0+w, which is where logical qubit lo+m-1-w lived:
 // the swapped labels land exactly on the canonical layout.  Every position
 // run stays contiguous, so each pass is one <= 5-D TMA box per tile.
-int fused_range(Handle *h, int lo, int m, int qft, int inverse)
+// Several ranks: before each pass the block's wires are made local (shard
+// exchanges), passes run in place, and the closing swaps are a relabelling.
+int fused_range(const Ranks &R, int lo, int m, int qft, int inverse)
 {
     // default 7: a 2^12 tile then carries >= 5 passive bits, i.e. 512-byte runs, which
     // the TMA streams at ~96% of HBM peak (10 wires -> 64-byte runs, ~70%)
     static const int amax_env = getenv("QSIM_QFT_AMAX") ? atoi(getenv("QSIM_QFT_AMAX")) : 7;
     const int amax = amax_env < 1 ? 1 : (amax_env > 10 ? 10 : amax_env);
+    Handle *h0 = R[0];
     const int G = (m + amax - 1) / amax;
     std::vector<int> gsize(G, m / G);
     for (int g = 0; g < m % G; ++g) gsize[g]++;
-    const bool block_moves = qft && h->world == 1;
+    const bool block_moves = qft && h0->world == 1;
     if (block_moves) {
-        if (int rc = dist_canonicalize(h)) return rc;
+        if (int rc = dist_canonicalize(R)) return rc;
+    } else {
+        if (int rc = flush_all(R)) return rc;
     }
-    const int s0 = h->n - lo - m;          // lowest position of the range (canonical)
-    std::vector<int> wp(m);                // current position of wire w
-    for (int w = 0; w < m; ++w) wp[w] = h->pos[lo + w];
+    const int nl = h0->nl;
+    const int s0 = h0->n - lo - m;         // lowest position of the range (canonical)
+    std::vector<int> wp(m);                // current position of wire w (same on every rank)
+    for (int w = 0; w < m; ++w) wp[w] = h0->pos[lo + w];
     int a0 = 0;
     for (int g = 0; g < G; ++g) {
         const int a = gsize[g];
         std::vector<int> act;
         for (int u = 0; u < a; ++u) act.push_back(lo + a0 + u);
-        if (h->world > 1) {
-            if (int rc = dist_make_local(h, act)) return rc;
-            for (int w = 0; w < m; ++w) wp[w] = h->pos[lo + w];
+        if (h0->world > 1) {
+            if (int rc = dist_make_local(R, act)) return rc;
+            for (int w = 0; w < m; ++w) wp[w] = h0->pos[lo + w];
         }
         // tile: active wires (tile bits 0..a-1) + passive low positions
         std::vector<int> tile_pos;
-        std::vector<char> in_tile(h->nl, 0);
+        std::vector<char> in_tile(nl, 0);
         for (int u = 0; u < a; ++u) {
             tile_pos.push_back(wp[a0 + u]);
             in_tile[wp[a0 + u]] = 1;
         }
-        const int want = std::min(kTileMaxBits, h->nl);
-        for (int p = 0; p < h->nl && (int)tile_pos.size() < want; ++p)
+        const int want = std::min(kTileMaxBits, nl);
+        for (int p = 0; p < nl && (int)tile_pos.size() < want; ++p)
             if (!in_tile[p]) { tile_pos.push_back(p); in_tile[p] = 1; }
         // output permutation of the local positions
-        std::vector<int> perm(h->nl);
-        for (int p = 0; p < h->nl; ++p) perm[p] = p;
+        std::vector<int> perm(nl);
+        for (int p = 0; p < nl; ++p) perm[p] = p;
         if (block_moves) {
             for (int w = a0 + a; w < m; ++w) perm[wp[w]] = wp[w] + a;   // rest block moves up
             for (int u = 0; u < a; ++u) perm[wp[a0 + u]] = s0 + a0 + u;  // block to final spots
         }
         bool moved_fixed = false;
-        for (int p = 0; p < h->nl; ++p) moved_fixed |= !in_tile[p] && perm[p] != p;
-        TilePass tp = make_pass(h, tile_pos, perm);
-        tp.a = a;
-        tp.inverse = inverse;
-        tp.hadamard_only = !qft;
-        tp.scale = std::ldexp(1.0, -(a / 2));
-        if (a & 1) tp.scale *= M_SQRT1_2;
-        tp.W = a0 + a;
-        tp.n_et = tp.n_ef = 0;
-        tp.y_const = 0;
-        if (qft) {
-            for (int i = 0; i < a0; ++i) {
-                const int p = wp[i];
-                if (p >= h->nl) {
-                    tp.y_const += (uint64_t)((h->rank >> (p - h->nl)) & 1) << i;
-                    continue;
-                }
-                int b = -1;
-                for (int t = 0; t < tp.tbits; ++t) if (tp.in_pos[t] == p) b = t;
-                if (b >= 0) { tp.et_bit[tp.n_et] = b; tp.et_w[tp.n_et] = i; tp.n_et++; }
-                else {
-                    int f = -1;
-                    for (int t = 0; t < tp.nfix; ++t) if (tp.fin_pos[t] == p) f = t;
-                    tp.ef_bit[tp.n_ef] = f; tp.ef_w[tp.n_ef] = i; tp.n_ef++;
+        for (int p = 0; p < nl; ++p) moved_fixed |= !in_tile[p] && perm[p] != p;
+        for (Handle *h : R) {
+            TilePass tp = make_pass(h, tile_pos, perm);
+            tp.a = a;
+            tp.inverse = inverse;
+            tp.hadamard_only = !qft;
+            tp.scale = std::ldexp(1.0, -(a / 2));
+            if (a & 1) tp.scale *= M_SQRT1_2;
+            tp.W = a0 + a;
+            tp.n_et = tp.n_ef = 0;
+            tp.y_const = 0;
+            if (qft) {
+                for (int i = 0; i < a0; ++i) {
+                    const int p = wp[i];
+                    if (p >= nl) {   // an earlier wire on a rank bit: constant for this rank
+                        tp.y_const += (uint64_t)((h->rank >> (p - nl)) & 1) << i;
+                        continue;
+                    }
+                    int b = -1;
+                    for (int t = 0; t < tp.tbits; ++t) if (tp.in_pos[t] == p) b = t;
+                    if (b >= 0) { tp.et_bit[tp.n_et] = b; tp.et_w[tp.n_et] = i; tp.n_et++; }
+                    else {
+                        int f = -1;
+                        for (int t = 0; t < tp.nfix; ++t) if (tp.fin_pos[t] == p) f = t;
+                        tp.ef_bit[tp.n_ef] = f; tp.ef_w[tp.n_ef] = i; tp.n_ef++;
+                    }
                 }
             }
+            plan_tile_maps(tp);
+            if (moved_fixed) {
+                if (ensure_scratch(h)) return QSIM_ENOMEM;
+                launch_tile_pass(h, tp, h->psi, h->scratch);
+                swap_buffers(h);
+            } else {
+                launch_tile_pass(h, tp, h->psi, h->psi);
+            }
+            if (int rc = after_launch(h, "fused tile pass")) return rc;
         }
-        plan_tile_maps(tp);
-        if (moved_fixed) {
-            if (ensure_scratch(h)) return QSIM_ENOMEM;
-            launch_tile_pass(h, tp, h->psi, h->scratch);
-            swap_buffers(h);
-        } else {
-            launch_tile_pass(h, tp, h->psi, h->psi);
-        }
-        if (int rc = after_launch(h, "fused tile pass")) return rc;
         for (int w = 0; w < m; ++w)
-            if (wp[w] < h->nl) wp[w] = perm[wp[w]];
+            if (wp[w] < nl) wp[w] = perm[wp[w]];
         a0 += a;
     }
     if (qft && !block_moves) {
         // closing swaps as a relabelling of the logical -> physical map
-        for (int t = 0; t < m / 2; ++t) std::swap(h->pos[lo + t], h->pos[lo + m - 1 - t]);
+        for (Handle *h : R)
+            for (int t = 0; t < m / 2; ++t) std::swap(h->pos[lo + t], h->pos[lo + m - 1 - t]);
     }
     return QSIM_OK;
 }
@@ -622,7 +649,13 @@ uint64_t qsim_memory_bytes(int n) { return (n < 0 || n > 59) ? 0 : (uint64_t)1 <
 
 const char *qsim_last_error(const qsim_t *h) { return h ? h->err.c_str() : g_create_error.c_str(); }
 
-uint64_t qsim_launch_count(const qsim_t *h) { return h ? h->launches : 0; }
+uint64_t qsim_launch_count(const qsim_t *h)
+{
+    if (!h) return 0;
+    uint64_t s = h->launches;
+    for (const Handle *m : h->members) s += m->launches;
+    return s;
+}
 
 void qsim_philox_draw(uint64_t seed, uint32_t tag, uint64_t i, uint32_t j, uint64_t out[2])
 {
@@ -690,7 +723,8 @@ int qsim_create(int n, int ngpus, qsim_t **out)
     if (!out) return QSIM_EINVAL;
     if (ngpus != 1) {
         *out = nullptr;
-        return fail(nullptr, QSIM_EINVAL, "qsim_create drives one GPU; use qsim_create_dist (one process per GPU)");
+        return fail(nullptr, QSIM_EINVAL,
+                    "qsim_create drives one GPU; use qsim_create_dist (one process per GPU) or qsim_create_group");
     }
     return create_common(n, 1, 0, -1, out);
 }
@@ -722,6 +756,41 @@ int qsim_create_dist(int n, int world, int rank, int device, const void *nccl_id
     return QSIM_OK;
 }
 
+int qsim_create_group(int n, int world, const int *devices, qsim_t **out)
+{
+    if (!out) return QSIM_EINVAL;
+    *out = nullptr;
+    if (world < 1 || (world & (world - 1))) return fail(nullptr, QSIM_EINVAL, "world must be a power of two");
+    qsim_t *g = new qsim_t();
+    g->n = n;
+    g->world = world;
+    while ((1 << g->kglob) < world) ++g->kglob;
+    g->nl = n - g->kglob;
+    for (int q = 0; q < n && q < kMaxQubits; ++q) g->pos[q] = n - 1 - q;
+    for (int r = 0; r < world; ++r) {
+        qsim_t *m = nullptr;
+        int rc = create_common(n, world, r, devices ? devices[r] : -1, &m);
+        if (rc) {
+            qsim_destroy(g);
+            return rc;
+        }
+        m->grp = g;
+        g->members.push_back(m);
+    }
+    // peer access between distinct member devices (NVLink peer copies)
+    for (Handle *a : g->members)
+        for (Handle *b : g->members)
+            if (a->device != b->device) {
+                cudaSetDevice(a->device);
+                cudaDeviceEnablePeerAccess(b->device, 0);
+                cudaGetLastError();
+            }
+    g->device = g->members[0]->device;
+    g->stream = g->members[0]->stream;
+    *out = g;
+    return QSIM_OK;
+}
+
 int qsim_nccl_unique_id(void *out128)
 {
 #ifndef QSIM_NO_NCCL
@@ -738,6 +807,12 @@ int qsim_nccl_unique_id(void *out128)
 void qsim_destroy(qsim_t *h)
 {
     if (!h) return;
+    if (!h->members.empty()) {
+        for (Handle *m : h->members) qsim_destroy(static_cast<qsim_t *>(m));
+        h->members.clear();
+        delete h;
+        return;
+    }
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
 #ifndef QSIM_NO_NCCL
@@ -747,6 +822,7 @@ void qsim_destroy(qsim_t *h)
     if (h->scratch) cudaFree(h->scratch);
     if (h->d_red) cudaFree(h->d_red);
     if (h->h_red) cudaFreeHost(h->h_red);
+    if (h->d_ops) cudaFree(h->d_ops);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
@@ -757,31 +833,37 @@ void *qsim_get_stream(qsim_t *h) { return h ? (void *)h->stream : nullptr; }
 int qsim_set_fusion(qsim_t *h, int enable)
 {
     QS_CHECK_HANDLE(h);
-    if (int rc = flush_queue(h)) return rc;
-    h->fuse = enable ? 1 : 0;
+    const Ranks R = ranks_of(h);
+    for (Handle *m : R) {
+        if (int rc = flush_queue(m)) return lift(h, R, rc);
+        m->fuse = enable ? 1 : 0;
+    }
     return QSIM_OK;
 }
 
+// profiling reports the first rank of a group
 int qsim_profile(qsim_t *h, int enable)
 {
     QS_CHECK_HANDLE(h);
-    if (int rc = flush_queue(h)) return rc;
-    cudaStreamSynchronize(h->stream);
-    h->prof.clear();
-    h->ev_used = 0;
-    h->pending = nullptr;
-    h->prof_on = enable;
+    Handle *m = ranks_of(h)[0];
+    if (int rc = flush_queue(m)) return rc;
+    cudaStreamSynchronize(m->stream);
+    m->prof.clear();
+    m->ev_used = 0;
+    m->pending = nullptr;
+    m->prof_on = enable;
     return QSIM_OK;
 }
 
 const char *qsim_profile_json(qsim_t *h)
 {
     if (!h) return "{}";
-    flush_queue(h);
-    cudaStreamSynchronize(h->stream);
+    Handle *m = ranks_of(h)[0];
+    flush_queue(m);
+    cudaStreamSynchronize(m->stream);
     struct Agg { double ms = 0; uint64_t bytes = 0, n = 0; };
     std::vector<std::pair<std::string, Agg>> agg;
-    for (const auto &r : h->prof) {
+    for (const auto &r : m->prof) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, r.a, r.b);
         size_t k = 0;
@@ -793,10 +875,10 @@ const char *qsim_profile_json(qsim_t *h)
     }
     std::string js = "{\"_launches\": [";
     char buf[256];
-    for (size_t k = 0; k < h->prof.size() && k < 4096; ++k) {
+    for (size_t k = 0; k < m->prof.size() && k < 4096; ++k) {
         float ms = 0.f;
-        cudaEventElapsedTime(&ms, h->prof[k].a, h->prof[k].b);
-        std::snprintf(buf, sizeof buf, "%s[\"%s\", %.5f]", k ? ", " : "", h->prof[k].name, ms);
+        cudaEventElapsedTime(&ms, m->prof[k].a, m->prof[k].b);
+        std::snprintf(buf, sizeof buf, "%s[\"%s\", %.5f]", k ? ", " : "", m->prof[k].name, ms);
         js += buf;
     }
     js += "]";
@@ -814,52 +896,91 @@ const char *qsim_profile_json(qsim_t *h)
 int qsim_sync(qsim_t *h)
 {
     QS_CHECK_HANDLE(h);
-    if (int rc = flush_queue(h)) return rc;
-    return check_cuda(h, cudaStreamSynchronize(h->stream), "qsim_sync");
+    const Ranks R = ranks_of(h);
+    for (Handle *m : R) {
+        if (int rc = flush_queue(m)) return lift(h, R, rc);
+        if (int rc = check_cuda(m, cudaStreamSynchronize(m->stream), "qsim_sync")) return lift(h, R, rc);
+    }
+    return QSIM_OK;
 }
 
 // ----------------------------------------------------------------- preparation
 int qsim_set_basis(qsim_t *h, uint64_t idx)
 {
     QS_CHECK_HANDLE(h);
-    h->queue.clear();   // the state is overwritten
     if (h->n < 64 && idx >> h->n) return fail(h, QSIM_ERANGE, "basis index >= 2^n");
-    for (int q = 0; q < h->n; ++q) h->pos[q] = h->n - 1 - q;
-    launch_zero(h);
-    if ((int)(idx >> h->nl) == h->rank) launch_set_one(h, idx & (h->local_dim() - 1));
-    return after_launch(h, "set_basis");
+    const Ranks R = ranks_of(h);
+    for (Handle *m : R) {
+        m->queue.clear();   // the state is overwritten
+        for (int q = 0; q < m->n; ++q) m->pos[q] = m->n - 1 - q;
+        launch_zero(m);
+        if ((int)(idx >> m->nl) == m->rank) launch_set_one(m, idx & (m->local_dim() - 1));
+        if (int rc = after_launch(m, "set_basis")) return lift(h, R, rc);
+    }
+    return QSIM_OK;
+}
+
+// sum |alpha|^2 over all ranks (fixed order)
+static int global_norm(qsim_t *h, const Ranks &R, double *out)
+{
+    std::vector<std::vector<double>> parts(R.size(), std::vector<double>(1, 0.0));
+    for (size_t i = 0; i < R.size(); ++i) {
+        Handle *m = R[i];
+        if (int rc = flush_queue(m)) return lift(h, R, rc);
+        launch_norm(m, m->d_red);
+        if (int rc = after_launch(m, "norm")) return lift(h, R, rc);
+        if (int rc = check_cuda(m, cudaMemcpyAsync(m->h_red, m->d_red, sizeof(double), cudaMemcpyDeviceToHost, m->stream), "norm"))
+            return lift(h, R, rc);
+        if (int rc = check_cuda(m, cudaStreamSynchronize(m->stream), "norm")) return lift(h, R, rc);
+        parts[i][0] = m->h_red[0];
+    }
+    return lift(h, R, dist_sum_host(R, parts, out, 1));
 }
 
 int qsim_init_gaussian(qsim_t *h, uint64_t seed)
 {
     QS_CHECK_HANDLE(h);
-    h->queue.clear();   // the state is overwritten
-    for (int q = 0; q < h->n; ++q) h->pos[q] = h->n - 1 - q;
-    launch_init_gaussian(h, seed);
+    const Ranks R = ranks_of(h);
+    for (Handle *m : R) {
+        m->queue.clear();   // the state is overwritten
+        for (int q = 0; q < m->n; ++q) m->pos[q] = m->n - 1 - q;
+        launch_init_gaussian(m, seed);
+    }
     double s = 0.0;
-    int rc = qsim_norm(h, &s);
-    if (rc) return rc;
-    launch_scale(h, 1.0 / std::sqrt(s));
-    return after_launch(h, "init_gaussian");
+    if (int rc = global_norm(h, R, &s)) return rc;
+    for (Handle *m : R) {
+        launch_scale(m, 1.0 / std::sqrt(s));
+        if (int rc = after_launch(m, "init_gaussian")) return lift(h, R, rc);
+    }
+    return QSIM_OK;
 }
 
 static int copy_state(qsim_t *h, uint64_t off, uint64_t cnt, qsim_c128 *host, bool to_dev)
 {
     QS_CHECK_HANDLE(h);
-    if (int rc = flush_queue(h)) return rc;
     const uint64_t dim = (uint64_t)1 << h->n;
     if (off > dim || cnt > dim - off) return fail(h, QSIM_ERANGE, "state slice outside [0, 2^n)");
-    int rc = dist_canonicalize(h);
-    if (rc) return rc;
-    const uint64_t lo = (uint64_t)h->rank << h->nl, hi = lo + h->local_dim();
-    if (cnt && (off < lo || off + cnt > hi)) return fail(h, QSIM_ERANGE, "slice not owned by this rank");
-    cudaError_t e;
-    if (to_dev)
-        e = cudaMemcpyAsync(h->psi + (off - lo), host, cnt * sizeof(double2), cudaMemcpyHostToDevice, h->stream);
-    else
-        e = cudaMemcpyAsync(host, h->psi + (off - lo), cnt * sizeof(double2), cudaMemcpyDeviceToHost, h->stream);
-    if (e != cudaSuccess) return check_cuda(h, e, "state copy");
-    return check_cuda(h, cudaStreamSynchronize(h->stream), "state copy");
+    const Ranks R = ranks_of(h);
+    if (int rc = dist_canonicalize(R)) return lift(h, R, rc);
+    // an in-process group owns every slice; a process rank only its own
+    if (R.size() == 1 && cnt) {
+        Handle *m = R[0];
+        const uint64_t lo = (uint64_t)m->rank << m->nl, hi = lo + m->local_dim();
+        if (off < lo || off + cnt > hi) return fail(h, QSIM_ERANGE, "slice not owned by this rank");
+    }
+    for (Handle *m : R) {
+        const uint64_t lo = (uint64_t)m->rank << m->nl, hi = lo + m->local_dim();
+        const uint64_t a = std::max(off, lo), b = std::min(off + cnt, hi);
+        if (a >= b) continue;
+        cudaError_t e;
+        if (to_dev)
+            e = cudaMemcpyAsync(m->psi + (a - lo), host + (a - off), (b - a) * sizeof(double2), cudaMemcpyHostToDevice, m->stream);
+        else
+            e = cudaMemcpyAsync(host + (a - off), m->psi + (a - lo), (b - a) * sizeof(double2), cudaMemcpyDeviceToHost, m->stream);
+        if (e != cudaSuccess) return lift(h, R, check_cuda(m, e, "state copy"));
+        if (int rc = check_cuda(m, cudaStreamSynchronize(m->stream), "state copy")) return lift(h, R, rc);
+    }
+    return QSIM_OK;
 }
 
 int qsim_set_state(qsim_t *h, uint64_t off, uint64_t cnt, const qsim_c128 *host)
@@ -879,7 +1000,8 @@ int qsim_apply_1q(qsim_t *h, int q, const qsim_c128 U[4])
     if (int rc = check_qubit(h, q)) return rc;
     double2 M[4];
     for (int k = 0; k < 4; ++k) M[k] = make_double2(U[k].re, U[k].im);
-    return apply_gate(h, 0, 0, q, M);
+    const Ranks R = ranks_of(h);
+    return lift(h, R, apply_gate(R, 0, 0, q, M));
 }
 
 int qsim_apply_ctrl(qsim_t *h, uint64_t cmask, uint64_t cvals, int q, const qsim_c128 U[4])
@@ -889,7 +1011,8 @@ int qsim_apply_ctrl(qsim_t *h, uint64_t cmask, uint64_t cvals, int q, const qsim
     if (int rc = check_ctrl(h, cmask, cvals, q)) return rc;
     double2 M[4];
     for (int k = 0; k < 4; ++k) M[k] = make_double2(U[k].re, U[k].im);
-    return apply_gate(h, cmask, cvals, q, M);
+    const Ranks R = ranks_of(h);
+    return lift(h, R, apply_gate(R, cmask, cvals, q, M));
 }
 
 int qsim_apply_angles(qsim_t *h, int kind, const double *ang, uint64_t cmask, uint64_t cvals, int q)
@@ -901,7 +1024,8 @@ int qsim_apply_angles(qsim_t *h, int kind, const double *ang, uint64_t cmask, ui
     double2 U[4];
     angle_matrix(h, kind, ang, h->gcount, U);
     h->gcount++;
-    return apply_gate(h, cmask, cvals, q, U);
+    const Ranks R = ranks_of(h);
+    return lift(h, R, apply_gate(R, cmask, cvals, q, U));
 }
 
 int qsim_set_gate_noise(qsim_t *h, uint64_t seed, double sigma)
@@ -932,38 +1056,40 @@ int qsim_swap(qsim_t *h, int q1, int q2)
     QS_CHECK_HANDLE(h);
     if (int rc = check_qubit(h, q1)) return rc;
     if (int rc = check_qubit(h, q2)) return rc;
-    // a SWAP is a relabelling of the logical -> physical map (no data moves)
-    std::swap(h->pos[q1], h->pos[q2]);
+    // a SWAP is a relabelling of the logical -> physical map (no data moves;
+    // queued gates already carry physical positions)
+    for (Handle *m : ranks_of(h)) std::swap(m->pos[q1], m->pos[q2]);
     return QSIM_OK;
 }
 
 int qsim_hadamard(qsim_t *h, int lo, int m)
 {
     QS_CHECK_HANDLE(h);
-    if (int rc = flush_queue(h)) return rc;
     if (lo < 0 || m < 0 || lo + m > h->n) return fail(h, QSIM_ERANGE, "range outside [0, n)");
     if (m == 0) return QSIM_OK;
-    if (h->nl >= 9 && m <= h->nl) return fused_range(h, lo, m, 0, 0);
+    const Ranks R = ranks_of(h);
+    if (h->nl >= 9 && m <= h->nl) return lift(h, R, fused_range(R, lo, m, 0, 0));
     const double r = M_SQRT1_2;
     double2 H[4] = {make_double2(r, 0), make_double2(r, 0), make_double2(r, 0), make_double2(-r, 0)};
     for (int q = lo; q < lo + m; ++q)
-        if (int rc = apply_gate(h, 0, 0, q, H)) return rc;
+        if (int rc = apply_gate(R, 0, 0, q, H)) return lift(h, R, rc);
     return QSIM_OK;
 }
 
 int qsim_qft(qsim_t *h, int lo, int m, int inverse)
 {
     QS_CHECK_HANDLE(h);
-    if (int rc = flush_queue(h)) return rc;
     if (lo < 0 || m < 0 || lo + m > h->n) return fail(h, QSIM_ERANGE, "range outside [0, n)");
     if (m == 0) return QSIM_OK;
+    const Ranks R = ranks_of(h);
     const double sgn = inverse ? -1.0 : 1.0;
     if (h->sigma == 0.0 && h->nl >= 9 && m <= h->nl) {
         // noiseless: fused passes (constant gates, R25)
         h->gcount += (uint64_t)m + (uint64_t)m * (m - 1) / 2;
-        return fused_range(h, lo, m, 1, inverse);
+        return lift(h, R, fused_range(R, lo, m, 1, inverse));
     }
-    // gate by gate (angle forms with operational noise, R14/R15)
+    // gate by gate (angle forms with operational noise, R14/R15): the gate
+    // queue fuses them into tile passes
     const double r = M_SQRT1_2;
     const double2 H[4] = {make_double2(r, 0), make_double2(r, 0), make_double2(r, 0), make_double2(-r, 0)};
     for (int j = 0; j < m; ++j) {
@@ -972,7 +1098,7 @@ int qsim_qft(qsim_t *h, int lo, int m, int inverse)
             const double ang[2] = {M_PI / 4.0, M_PI};
             rc = qsim_apply_angles(h, QSIM_GATE_RP, ang, 0, 0, lo + j);
         } else {
-            rc = apply_gate(h, 0, 0, lo + j, H);
+            rc = lift(h, R, apply_gate(R, 0, 0, lo + j, H));
             h->gcount++;
         }
         if (rc) return rc;
@@ -982,40 +1108,45 @@ int qsim_qft(qsim_t *h, int lo, int m, int inverse)
             if (h->sigma > 0.0) {
                 rc = qsim_apply_angles(h, QSIM_GATE_P1, &phi, cm, cm, lo + j);
             } else {
-                double2 R[4] = {make_double2(1, 0), make_double2(0, 0), make_double2(0, 0),
-                                make_double2(std::cos(phi), std::sin(phi))};
-                rc = apply_gate(h, cm, cm, lo + j, R);
+                double2 Rd[4] = {make_double2(1, 0), make_double2(0, 0), make_double2(0, 0),
+                                 make_double2(std::cos(phi), std::sin(phi))};
+                rc = lift(h, R, apply_gate(R, cm, cm, lo + j, Rd));
                 h->gcount++;
             }
             if (rc) return rc;
         }
     }
-    for (int j = 0; j < m / 2; ++j) std::swap(h->pos[lo + j], h->pos[lo + m - 1 - j]);
+    for (Handle *mm : R)
+        for (int j = 0; j < m / 2; ++j) std::swap(mm->pos[lo + j], mm->pos[lo + m - 1 - j]);
     return QSIM_OK;
 }
 
 int qsim_phase_flip(qsim_t *h, uint64_t idx)
 {
     QS_CHECK_HANDLE(h);
-    if (int rc = flush_queue(h)) return rc;
     if (h->n < 64 && idx >> h->n) return fail(h, QSIM_ERANGE, "index >= 2^n");
-    // physical location of logical index idx
-    uint64_t phys = 0;
-    for (int q = 0; q < h->n; ++q) phys |= ((idx >> (h->n - 1 - q)) & 1) << h->pos[q];
-    if ((int)(phys >> h->nl) != h->rank) return QSIM_OK;
-    const uint64_t mask = h->local_dim() - 1;
-    launch_phase_mask(h, mask, phys & mask, make_double2(-1.0, 0.0));
-    return after_launch(h, "phase_flip");
+    const Ranks R = ranks_of(h);
+    for (Handle *m : R) {
+        if (int rc = flush_queue(m)) return lift(h, R, rc);
+        // physical location of logical index idx
+        uint64_t phys = 0;
+        for (int q = 0; q < m->n; ++q) phys |= ((idx >> (m->n - 1 - q)) & 1) << m->pos[q];
+        if ((int)(phys >> m->nl) != m->rank) continue;
+        const uint64_t mask = m->local_dim() - 1;
+        launch_phase_mask(m, mask, phys & mask, make_double2(-1.0, 0.0));
+        if (int rc = after_launch(m, "phase_flip")) return lift(h, R, rc);
+    }
+    return QSIM_OK;
 }
 
 int qsim_grover(qsim_t *h, uint64_t mark, int iters, double *trace)
 {
     QS_CHECK_HANDLE(h);
-    if (int rc = flush_queue(h)) return rc;
     if (h->n < 64 && mark >> h->n) return fail(h, QSIM_ERANGE, "mark >= 2^n");
     if (iters < 0) return fail(h, QSIM_EINVAL, "iters < 0");
     if (h->world > 1) return fail(h, QSIM_EINVAL, "qsim_grover runs on a single-GPU handle");
-    if (int rc = dist_canonicalize(h)) return rc;
+    const Ranks R = ranks_of(h);
+    if (int rc = dist_canonicalize(R)) return rc;
     double *d_trace = nullptr;
     if (trace && iters > 0) {
         if (cudaMalloc(&d_trace, sizeof(double) * iters) != cudaSuccess) {
@@ -1044,7 +1175,6 @@ static uint64_t gcd64(uint64_t a, uint64_t b)
 int qsim_apply_perm(qsim_t *h, const qsim_perm_t *f)
 {
     QS_CHECK_HANDLE(h);
-    if (int rc = flush_queue(h)) return rc;
     if (!f) return fail(h, QSIM_EINVAL, "null permutation");
     if (f->kind < 0 || f->kind > 2) return fail(h, QSIM_EINVAL, "unknown permutation kind");
     if (f->m < 1 || f->lo < 0 || f->lo + f->m > h->n) return fail(h, QSIM_ERANGE, "target register outside [0, n)");
@@ -1052,11 +1182,6 @@ int qsim_apply_perm(qsim_t *h, const qsim_perm_t *f)
     if (f->ctrl_mask & treg) return fail(h, QSIM_EINVAL, "control overlaps the target register");
     if (f->ctrl_vals & ~f->ctrl_mask) return fail(h, QSIM_EINVAL, "ctrl_vals outside ctrl_mask");
     if (h->n < 64 && (f->ctrl_mask >> h->n)) return fail(h, QSIM_ERANGE, "control mask has qubits >= n");
-    PermDesc d;
-    std::memset(&d, 0, sizeof d);
-    d.kind = f->kind;
-    d.wm = f->m;
-    uint32_t *d_table = nullptr;
     if (f->kind == QSIM_PERM_TABLE) {
         if (f->m > 24 || !f->table) return fail(h, QSIM_EINVAL, "TABLE needs m <= 24 and a table");
         const uint64_t len = 1ull << f->m;
@@ -1065,21 +1190,12 @@ int qsim_apply_perm(qsim_t *h, const qsim_perm_t *f)
             if (f->table[v] >= len || seen[f->table[v]]) return fail(h, QSIM_ENOTBIJ, "table is not a bijection");
             seen[f->table[v]] = 1;
         }
-        if (cudaMalloc(&d_table, sizeof(uint32_t) * len) != cudaSuccess) {
-            cudaGetLastError();
-            return fail(h, QSIM_ENOMEM, "cannot allocate the permutation table");
-        }
-        cudaMemcpyAsync(d_table, f->table, sizeof(uint32_t) * len, cudaMemcpyHostToDevice, h->stream);
-        d.d_table = d_table;
     } else {
         const uint64_t N = f->modulus;
         if (N < 2 || N >= (1ull << 32) || (f->m < 64 && N > (1ull << f->m)))
             return fail(h, QSIM_EINVAL, "modulus must be in [2, min(2^m, 2^32))");
         const uint64_t c = f->kind == QSIM_PERM_MODMUL ? f->mult : f->base;
         if (gcd64(c % N, N) != 1) return fail(h, QSIM_ENOTBIJ, "multiplier not coprime to the modulus");
-        d.mult = f->mult;
-        d.base = f->base;
-        d.modulus = N;
         if (f->kind == QSIM_PERM_MODEXP) {
             if (f->em < 1 || f->em > 40 || f->elo < 0 || f->elo + f->em > h->n)
                 return fail(h, QSIM_ERANGE, "exponent register outside [0, n)");
@@ -1087,31 +1203,50 @@ int qsim_apply_perm(qsim_t *h, const qsim_perm_t *f)
             if (ereg & (treg | f->ctrl_mask)) return fail(h, QSIM_EINVAL, "exponent register overlaps");
         }
     }
-    // the work register must be local
+    const Ranks R = ranks_of(h);
+    if (int rc = flush_all(R)) return lift(h, R, rc);
+    // the work register must be local (exponent / control qubits may be rank bits)
     std::vector<int> need;
     for (int q = f->lo; q < f->lo + f->m; ++q) need.push_back(q);
-    if (int rc = dist_make_local(h, need)) { if (d_table) cudaFree(d_table); return rc; }
-    // work value bit b (LSB) <-> logical qubit lo+m-1-b
-    for (int b = 0; b < f->m; ++b) d.wpos[b] = h->pos[f->lo + f->m - 1 - b];
-    if (f->kind == QSIM_PERM_MODEXP) {
-        d.em = f->em;
-        for (int b = 0; b < f->em; ++b) {
-            const int p = h->pos[f->elo + f->em - 1 - b];
-            d.epos[b] = p < h->nl ? p : -1 - (p - h->nl);
+    if (int rc = dist_make_local(R, need)) return lift(h, R, rc);
+    for (Handle *m : R) {
+        PermDesc d;
+        std::memset(&d, 0, sizeof d);
+        d.kind = f->kind;
+        d.wm = f->m;
+        d.mult = f->mult;
+        d.base = f->base;
+        d.modulus = f->modulus;
+        // work value bit b (LSB) <-> logical qubit lo+m-1-b
+        for (int b = 0; b < f->m; ++b) d.wpos[b] = m->pos[f->lo + f->m - 1 - b];
+        if (f->kind == QSIM_PERM_MODEXP) {
+            d.em = f->em;
+            for (int b = 0; b < f->em; ++b) {
+                const int p = m->pos[f->elo + f->em - 1 - b];
+                d.epos[b] = p < m->nl ? p : -1 - (p - m->nl);
+            }
         }
+        uint64_t lm, lv;
+        if (!local_controls(m, f->ctrl_mask, f->ctrl_vals, lm, lv)) continue;
+        d.cmask = lm;
+        d.cval = lv;
+        d.rank_bits = (uint64_t)m->rank;
+        uint32_t *d_table = nullptr;
+        if (f->kind == QSIM_PERM_TABLE) {
+            const uint64_t len = 1ull << f->m;
+            if (cudaMalloc(&d_table, sizeof(uint32_t) * len) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(h, QSIM_ENOMEM, "cannot allocate the permutation table");
+            }
+            cudaMemcpyAsync(d_table, f->table, sizeof(uint32_t) * len, cudaMemcpyHostToDevice, m->stream);
+            d.d_table = d_table;
+        }
+        launch_perm(m, d);
+        int rc = after_launch(m, "permutation");
+        if (d_table) { cudaStreamSynchronize(m->stream); cudaFree(d_table); }
+        if (rc) return lift(h, R, rc);
     }
-    uint64_t lm, lv;
-    if (!local_controls(h, f->ctrl_mask, f->ctrl_vals, lm, lv)) {
-        if (d_table) { cudaStreamSynchronize(h->stream); cudaFree(d_table); }
-        return QSIM_OK;
-    }
-    d.cmask = lm;
-    d.cval = lv;
-    d.rank_bits = (uint64_t)h->rank;
-    launch_perm(h, d);
-    int rc = after_launch(h, "permutation");
-    if (d_table) { cudaStreamSynchronize(h->stream); cudaFree(d_table); }
-    return rc;
+    return QSIM_OK;
 }
 
 // ----------------------------------------------------------------- decoherence
@@ -1121,6 +1256,7 @@ int qsim_inject_errors(qsim_t *h, uint64_t seed, const qsim_noise_t *model, qsim
     QS_CHECK_HANDLE(h);
     if (!model) return fail(h, QSIM_EINVAL, "null noise model");
     if (!(model->p >= 0.0 && model->p <= 1.0)) return fail(h, QSIM_EINVAL, "p must be in [0, 1]");
+    const Ranks R = ranks_of(h);
     int count = 0;
     for (int q = 0; q < h->n; ++q) {
         if (!((model->qubit_mask >> q) & 1)) continue;
@@ -1133,7 +1269,7 @@ int qsim_inject_errors(qsim_t *h, uint64_t seed, const qsim_noise_t *model, qsim
         if (which == 1) { P[0] = make_double2(0, 0); P[1] = make_double2(1, 0); P[2] = make_double2(1, 0); P[3] = make_double2(0, 0); }
         else if (which == 2) { P[0] = make_double2(0, 0); P[1] = make_double2(0, -1); P[2] = make_double2(0, 1); P[3] = make_double2(0, 0); }
         else { P[0] = make_double2(1, 0); P[1] = make_double2(0, 0); P[2] = make_double2(0, 0); P[3] = make_double2(-1, 0); }
-        if (int rc = apply_gate(h, 0, 0, q, P)) return rc;
+        if (int rc = apply_gate(R, 0, 0, q, P)) return lift(h, R, rc);
         if (ev && count < cap) {
             ev[count].epoch = model->epoch;
             ev[count].qubit = q;
@@ -1150,151 +1286,143 @@ int qsim_inject_errors(qsim_t *h, uint64_t seed, const qsim_noise_t *model, qsim
 int qsim_norm(qsim_t *h, double *out)
 {
     QS_CHECK_HANDLE(h);
-    if (int rc = flush_queue(h)) return rc;
     if (!out) return QSIM_EINVAL;
-    launch_norm(h, h->d_red);
-    if (int rc = after_launch(h, "norm")) return rc;
-    double s = 0.0;
-    if (int rc = check_cuda(h, cudaMemcpyAsync(h->h_red, h->d_red, sizeof(double), cudaMemcpyDeviceToHost, h->stream), "norm"))
-        return rc;
-    if (int rc = check_cuda(h, cudaStreamSynchronize(h->stream), "norm")) return rc;
-    s = h->h_red[0];
-    if (h->world > 1) {
-        if (int rc = dist_allreduce_sum_host(h, &s, 1)) return rc;
-    }
-    *out = s;
-    return QSIM_OK;
+    return global_norm(h, ranks_of(h), out);
 }
 
 int qsim_probs(qsim_t *h, int lo, int m, double *out)
 {
     QS_CHECK_HANDLE(h);
-    if (int rc = flush_queue(h)) return rc;
     if (!out) return QSIM_EINVAL;
     if (lo < 0 || m < 1 || m > 26 || lo + m > h->n) return fail(h, QSIM_ERANGE, "range outside [0, n) or m > 26");
-    if (int rc = dist_canonicalize(h)) return rc;
+    const Ranks R = ranks_of(h);
+    if (int rc = dist_canonicalize(R)) return lift(h, R, rc);
     // canonical: value bit b <-> position n-lo-m+b; local part [pl, min(nl, pl+m))
+    const int nl = h->nl;
     const int pl = h->n - lo - m;
     const int ph = pl + m;   // exclusive
     const uint64_t ny = 1ull << m;
-    if (ph <= h->nl) {
-        ensure_red(h, ny + (1 << 16));
-        double *d_out = h->d_red + h->red_cap - ny;   // tail of the workspace
-        (void)d_out;
-        double *d_res = nullptr;
-        if (cudaMalloc(&d_res, ny * sizeof(double)) != cudaSuccess) { cudaGetLastError(); return fail(h, QSIM_ENOMEM, "probs buffer"); }
-        launch_probs_contig(h, pl, m, d_res);
-        int rc = after_launch(h, "probs");
-        if (!rc) rc = check_cuda(h, cudaMemcpyAsync(out, d_res, ny * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "probs");
-        if (!rc) rc = check_cuda(h, cudaStreamSynchronize(h->stream), "probs");
-        cudaFree(d_res);
-        if (rc) return rc;
-        if (h->world > 1) return dist_allreduce_sum_host(h, out, ny);
-        return QSIM_OK;
-    }
-    // part of the sub-register is on rank bits
-    const int mloc = pl < h->nl ? h->nl - pl : 0;
+    const int mloc = ph <= nl ? m : (pl < nl ? nl - pl : 0);
     const uint64_t nyl = 1ull << mloc;
-    std::vector<double> part(nyl);
-    double *d_res = nullptr;
-    if (cudaMalloc(&d_res, nyl * sizeof(double)) != cudaSuccess) { cudaGetLastError(); return fail(h, QSIM_ENOMEM, "probs buffer"); }
-    if (mloc > 0) launch_probs_contig(h, pl, mloc, d_res);
-    else launch_norm(h, d_res);
-    int rc = after_launch(h, "probs");
-    if (!rc) rc = check_cuda(h, cudaMemcpyAsync(part.data(), d_res, nyl * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "probs");
-    if (!rc) rc = check_cuda(h, cudaStreamSynchronize(h->stream), "probs");
-    cudaFree(d_res);
-    if (rc) return rc;
-    // place this rank's partial at y = (rank bits of the range) << mloc | y_loc
-    std::vector<double> full(ny, 0.0);
-    const int gl = pl > h->nl ? pl - h->nl : 0;       // first rank bit in the range
-    const int gh = ph - h->nl;                          // exclusive
-    const uint64_t yhi = ((uint64_t)h->rank >> gl) & ((1ull << (gh - gl)) - 1);
-    for (uint64_t y = 0; y < nyl; ++y) full[(yhi << mloc) | y] = part[y];
-    std::memcpy(out, full.data(), ny * sizeof(double));
-    return dist_allreduce_sum_host(h, out, ny);
+    std::vector<std::vector<double>> parts(R.size(), std::vector<double>(ny, 0.0));
+    for (size_t i = 0; i < R.size(); ++i) {
+        Handle *hm = R[i];
+        double *d_res = nullptr;
+        if (cudaMalloc(&d_res, nyl * sizeof(double)) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(h, QSIM_ENOMEM, "probs buffer");
+        }
+        if (mloc > 0) launch_probs_contig(hm, pl, mloc, d_res);
+        else launch_norm(hm, d_res);
+        int rc = after_launch(hm, "probs");
+        std::vector<double> part(nyl);
+        if (!rc) rc = check_cuda(hm, cudaMemcpyAsync(part.data(), d_res, nyl * sizeof(double), cudaMemcpyDeviceToHost, hm->stream), "probs");
+        if (!rc) rc = check_cuda(hm, cudaStreamSynchronize(hm->stream), "probs");
+        cudaFree(d_res);
+        if (rc) return lift(h, R, rc);
+        // y = (rank bits inside the range) << mloc | y_loc
+        uint64_t yhi = 0;
+        if (ph > nl) {
+            const int gl = pl > nl ? pl - nl : 0;
+            const int gh = ph - nl;
+            yhi = ((uint64_t)hm->rank >> gl) & ((1ull << (gh - gl)) - 1);
+        }
+        for (uint64_t y = 0; y < nyl; ++y) parts[i][(yhi << mloc) | y] = part[y];
+    }
+    return lift(h, R, dist_sum_host(R, parts, out, ny));
 }
 
 int qsim_prob_index(qsim_t *h, uint64_t idx, double *out)
 {
     QS_CHECK_HANDLE(h);
-    if (int rc = flush_queue(h)) return rc;
     if (!out) return QSIM_EINVAL;
     if (h->n < 64 && idx >> h->n) return fail(h, QSIM_ERANGE, "index >= 2^n");
-    if (int rc = dist_canonicalize(h)) return rc;
-    double v = 0.0;
-    if ((int)(idx >> h->nl) == h->rank) {
+    const Ranks R = ranks_of(h);
+    if (int rc = dist_canonicalize(R)) return lift(h, R, rc);
+    std::vector<std::vector<double>> parts(R.size(), std::vector<double>(1, 0.0));
+    for (size_t i = 0; i < R.size(); ++i) {
+        Handle *m = R[i];
+        if ((int)(idx >> m->nl) != m->rank) continue;
         double2 a;
-        if (int rc = check_cuda(h, cudaMemcpyAsync(&a, h->psi + (idx & (h->local_dim() - 1)), sizeof a,
-                                                   cudaMemcpyDeviceToHost, h->stream), "prob_index"))
-            return rc;
-        if (int rc = check_cuda(h, cudaStreamSynchronize(h->stream), "prob_index")) return rc;
-        v = a.x * a.x + a.y * a.y;
+        if (int rc = check_cuda(m, cudaMemcpyAsync(&a, m->psi + (idx & (m->local_dim() - 1)), sizeof a,
+                                                   cudaMemcpyDeviceToHost, m->stream), "prob_index"))
+            return lift(h, R, rc);
+        if (int rc = check_cuda(m, cudaStreamSynchronize(m->stream), "prob_index")) return lift(h, R, rc);
+        parts[i][0] = a.x * a.x + a.y * a.y;
     }
-    if (h->world > 1) {
-        if (int rc = dist_allreduce_sum_host(h, &v, 1)) return rc;
-    }
-    *out = v;
-    return QSIM_OK;
+    return lift(h, R, dist_sum_host(R, parts, out, 1));
 }
 
 int qsim_measure(qsim_t *h, double r, uint64_t *idx)
 {
     QS_CHECK_HANDLE(h);
-    if (int rc = flush_queue(h)) return rc;
     if (!idx) return QSIM_EINVAL;
     if (!(r >= 0.0 && r < 1.0)) return fail(h, QSIM_EINVAL, "r must be in [0, 1)");
-    if (int rc = dist_canonicalize(h)) return rc;
-    const int bb = h->nl < 16 ? h->nl : 16;
-    const uint64_t nb = h->local_dim() >> bb;
-    double *d_blk = nullptr;
-    if (cudaMalloc(&d_blk, nb * sizeof(double)) != cudaSuccess) { cudaGetLastError(); return fail(h, QSIM_ENOMEM, "measure buffer"); }
-    launch_block_abs2(h, bb, d_blk);
-    int rc = after_launch(h, "measure");
-    std::vector<double> blk(nb * h->world, 0.0);
-    if (!rc) rc = check_cuda(h, cudaMemcpyAsync(blk.data() + nb * h->rank, d_blk, nb * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "measure");
-    if (!rc) rc = check_cuda(h, cudaStreamSynchronize(h->stream), "measure");
-    cudaFree(d_blk);
-    if (rc) return rc;
-    if (h->world > 1) {
-        if (int rc2 = dist_allreduce_sum_host(h, blk.data(), blk.size())) return rc2;
+    const Ranks R = ranks_of(h);
+    if (int rc = dist_canonicalize(R)) return lift(h, R, rc);
+    const int nl = h->nl;
+    const int bb = nl < 16 ? nl : 16;
+    const uint64_t nb = (1ull << nl) >> bb;
+    const uint64_t total = nb * h->world;
+    // block sums of every rank, placed at the rank's blocks
+    std::vector<std::vector<double>> parts(R.size(), std::vector<double>(total, 0.0));
+    for (size_t i = 0; i < R.size(); ++i) {
+        Handle *m = R[i];
+        double *d_blk = nullptr;
+        if (cudaMalloc(&d_blk, nb * sizeof(double)) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(h, QSIM_ENOMEM, "measure buffer");
+        }
+        launch_block_abs2(m, bb, d_blk);
+        int rc = after_launch(m, "measure");
+        if (!rc) rc = check_cuda(m, cudaMemcpyAsync(parts[i].data() + nb * m->rank, d_blk, nb * sizeof(double),
+                                                    cudaMemcpyDeviceToHost, m->stream), "measure");
+        if (!rc) rc = check_cuda(m, cudaStreamSynchronize(m->stream), "measure");
+        cudaFree(d_blk);
+        if (rc) return lift(h, R, rc);
     }
-    // sequential scan over block sums (fixed order), then inside one block
+    std::vector<double> blk(total);
+    if (int rc = dist_sum_host(R, parts, blk.data(), total)) return lift(h, R, rc);
+    // sequential scan over block sums (fixed order), then inside one block (R22)
     double acc = 0.0;
     int64_t sel = -1, last_nz_blk = -1;
-    for (uint64_t b = 0; b < blk.size(); ++b) {
+    for (uint64_t b = 0; b < total; ++b) {
         if (blk[b] != 0.0) last_nz_blk = (int64_t)b;
-        if (sel < 0 && r < acc + blk[b]) { sel = (int64_t)b; break; }
+        if (r < acc + blk[b]) { sel = (int64_t)b; break; }
         acc += blk[b];
     }
     const uint64_t blen = 1ull << bb;
     bool fallback = false;
-    if (sel < 0) { sel = last_nz_blk < 0 ? 0 : last_nz_blk; fallback = true; }
-    const int owner = (int)(((uint64_t)sel * blen) >> h->nl);
-    uint64_t result = 0;
-    std::vector<double2> amp(blen);
-    if (owner == h->rank) {
-        const uint64_t loc = ((uint64_t)sel * blen) & (h->local_dim() - 1);
-        rc = check_cuda(h, cudaMemcpyAsync(amp.data(), h->psi + loc, blen * sizeof(double2), cudaMemcpyDeviceToHost, h->stream), "measure");
-        if (!rc) rc = check_cuda(h, cudaStreamSynchronize(h->stream), "measure");
-        if (rc) return rc;
-        uint64_t last_nz = 0;
+    if (sel < 0) {
+        for (uint64_t b = 0; b < total; ++b) if (blk[b] != 0.0) last_nz_blk = (int64_t)b;
+        sel = last_nz_blk < 0 ? 0 : last_nz_blk;
+        fallback = true;
+    }
+    const int owner = (int)(((uint64_t)sel * blen) >> nl);
+    std::vector<std::vector<double>> res(R.size(), std::vector<double>(1, 0.0));
+    for (size_t i = 0; i < R.size(); ++i) {
+        Handle *m = R[i];
+        if (m->rank != owner) continue;
+        std::vector<double2> amp(blen);
+        const uint64_t loc = ((uint64_t)sel * blen) & (m->local_dim() - 1);
+        int rc = check_cuda(m, cudaMemcpyAsync(amp.data(), m->psi + loc, blen * sizeof(double2), cudaMemcpyDeviceToHost, m->stream), "measure");
+        if (!rc) rc = check_cuda(m, cudaStreamSynchronize(m->stream), "measure");
+        if (rc) return lift(h, R, rc);
+        uint64_t last_nz = 0, result = 0;
         bool found = false;
-        for (uint64_t i = 0; i < blen; ++i) {
-            const double p = amp[i].x * amp[i].x + amp[i].y * amp[i].y;
-            if (p != 0.0) last_nz = i;
-            acc += p;
-            if (!fallback && r < acc) { result = i; found = true; break; }
+        double a2 = acc;
+        for (uint64_t k = 0; k < blen; ++k) {
+            const double p = amp[k].x * amp[k].x + amp[k].y * amp[k].y;
+            if (p != 0.0) last_nz = k;
+            a2 += p;
+            if (!fallback && r < a2) { result = k; found = true; break; }
         }
         if (!found) result = last_nz;
-        result += (uint64_t)sel * blen;
+        res[i][0] = (double)(result + (uint64_t)sel * blen);
     }
-    if (h->world > 1) {
-        double v = owner == h->rank ? (double)result : 0.0;
-        if (int rc2 = dist_allreduce_sum_host(h, &v, 1)) return rc2;
-        result = (uint64_t)v;
-    }
-    *idx = result;
+    double v = 0.0;
+    if (int rc = dist_sum_host(R, res, &v, 1)) return lift(h, R, rc);
+    *idx = (uint64_t)v;
     return QSIM_OK;
 }
 

@@ -102,8 +102,20 @@ static int plan_canonical_globals(int n, int nl, std::vector<int> &pos, std::vec
     return QSIM_OK;
 }
 
-// Swap global position g with the top local position nl-1 (collective).
-static int exchange_top(Handle *h, int g)
+// ---------------------------------------------------------------- transport
+// XCHG g: rank r swaps the half of its shard whose top local bit differs from
+// its rank bit g with rank r ^ 2^(g-nl) (whose half has the other top bit),
+// so afterwards the qubits at position g and nl-1 have traded places.
+//
+//  * multi-process world (one rank per process): ncclSend + ncclRecv of the
+//    contiguous S/2 half in one group, received into the scratch shard and
+//    copied back;
+//  * in-process group (qsim_create_group): the lower rank of each pair swaps
+//    the two halves directly with device-to-device copies (peer copies over
+//    NVLink when the members live on different GPUs), ordered against both
+//    members' streams with events.
+
+static int exchange_nccl(Handle *h, int g)
 {
 #ifndef QSIM_NO_NCCL
     const int gb = g - h->nl;
@@ -118,13 +130,6 @@ static int exchange_top(Handle *h, int g)
     if (int rc = nccl_check(h, ncclGroupEnd(), "ncclGroupEnd")) return rc;
     cudaError_t e = cudaMemcpyAsync(mine, h->scratch, half * sizeof(double2), cudaMemcpyDeviceToDevice, h->stream);
     if (e != cudaSuccess) return check_cuda(h, e, "exchange copy");
-    // bookkeeping: the qubits at g and nl-1 trade places
-    int qg = -1, qt = -1;
-    for (int q = 0; q < h->n; ++q) {
-        if (h->pos[q] == g) qg = q;
-        if (h->pos[q] == h->nl - 1) qt = q;
-    }
-    std::swap(h->pos[qg], h->pos[qt]);
     return QSIM_OK;
 #else
     (void)g;
@@ -132,78 +137,125 @@ static int exchange_top(Handle *h, int g)
 #endif
 }
 
-static int run_steps(Handle *h, const std::vector<Step> &steps)
+static int exchange_pair(Handle *A, Handle *B, int g)
 {
+    // A = lower rank (bit g = 0): its half with top bit 1 <-> B's half with top bit 0
+    const uint64_t half = A->local_dim() >> 1;
+    if (int rc = ensure_scratch(A)) return rc;
+    double2 *ha = A->psi + half, *hb = B->psi;
+    cudaEvent_t eb, ea;
+    cudaEventCreateWithFlags(&eb, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ea, cudaEventDisableTiming);
+    cudaEventRecord(eb, B->stream);
+    cudaStreamWaitEvent(A->stream, eb, 0);
+    const size_t bytes = half * sizeof(double2);
+    cudaMemcpyAsync(A->scratch, ha, bytes, cudaMemcpyDefault, A->stream);
+    cudaMemcpyAsync(ha, hb, bytes, cudaMemcpyDefault, A->stream);
+    cudaMemcpyAsync(hb, A->scratch, bytes, cudaMemcpyDefault, A->stream);
+    cudaEventRecord(ea, A->stream);
+    cudaStreamWaitEvent(B->stream, ea, 0);
+    cudaEventDestroy(eb);
+    cudaEventDestroy(ea);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? QSIM_OK : check_cuda(A, e, "group exchange");
+}
+
+static int run_steps(const Ranks &R, const std::vector<Step> &steps)
+{
+    const bool group = R.size() > 1;
     for (const Step &st : steps) {
         if (st.kind == STEP_LSWAP) {
-            launch_swap_local(h, st.a, st.b);
+            for (Handle *h : R) launch_swap_local(h, st.a, st.b);
+        } else if (group) {
+            const int gb = st.a - R[0]->nl;
+            for (size_t r = 0; r < R.size(); ++r) {
+                const size_t p = r ^ ((size_t)1 << gb);
+                if (r < p)
+                    if (int rc = exchange_pair(R[r], R[p], st.a)) return rc;
+            }
+        } else {
+            if (int rc = exchange_nccl(R[0], st.a)) return rc;
+        }
+        for (Handle *h : R) {
             std::vector<int> pos(h->pos, h->pos + h->n);
             apply_step(pos, h->nl, st);
             for (int q = 0; q < h->n; ++q) h->pos[q] = pos[q];
-        } else {
-            if (int rc = exchange_top(h, st.a)) return rc;
         }
     }
     return QSIM_OK;
 }
 
-int dist_make_local(Handle *h, const std::vector<int> &need)
+int flush_all(const Ranks &R)
 {
+    for (Handle *h : R)
+        if (int rc = flush_queue(h)) return rc;
+    return QSIM_OK;
+}
+
+int dist_make_local(const Ranks &R, const std::vector<int> &need)
+{
+    Handle *h = R[0];
     if (h->world == 1) return QSIM_OK;
-    if (int rc = flush_queue(h)) return rc;
+    bool all_local = true;
+    for (int q : need) all_local &= h->pos[q] < h->nl;
+    if (all_local) return QSIM_OK;
+    if (int rc = flush_all(R)) return rc;
     std::vector<int> pos(h->pos, h->pos + h->n);
     std::vector<Step> steps;
     if (plan_make_local(h->n, h->nl, pos, need, steps)) return fail(h, QSIM_EINVAL, "too many qubits requested local");
-    return run_steps(h, steps);
+    return run_steps(R, steps);
 }
 
-int dist_canonicalize(Handle *h)
+int dist_canonicalize(const Ranks &R)
 {
-    if (int rc = flush_queue(h)) return rc;
-    if (h->world > 1) {
-        std::vector<int> pos(h->pos, h->pos + h->n);
+    if (int rc = flush_all(R)) return rc;
+    Handle *h0 = R[0];
+    if (h0->world > 1) {
+        std::vector<int> pos(h0->pos, h0->pos + h0->n);
         std::vector<Step> steps;
-        if (plan_canonical_globals(h->n, h->nl, pos, steps)) return fail(h, QSIM_EINVAL, "canonicalize plan");
-        if (int rc = run_steps(h, steps)) return rc;
+        if (plan_canonical_globals(h0->n, h0->nl, pos, steps)) return fail(h0, QSIM_EINVAL, "canonicalize plan");
+        if (int rc = run_steps(R, steps)) return rc;
     }
     bool canon = true;
-    for (int q = 0; q < h->n; ++q) canon &= h->pos[q] == h->n - 1 - q;
+    for (int q = 0; q < h0->n; ++q) canon &= h0->pos[q] == h0->n - 1 - q;
     if (canon) return QSIM_OK;
-    std::vector<int> perm(h->nl);
-    for (int q = 0; q < h->n; ++q) {
-        const int p = h->pos[q];
-        if (p < h->nl) perm[p] = h->n - 1 - q;
+    std::vector<int> perm(h0->nl);
+    for (int q = 0; q < h0->n; ++q) {
+        const int p = h0->pos[q];
+        if (p < h0->nl) perm[p] = h0->n - 1 - q;
     }
-    permute_local(h, perm);
-    for (int q = 0; q < h->n; ++q) h->pos[q] = h->n - 1 - q;
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return check_cuda(h, e, "canonicalize");
-    return h->poisoned ? fail(h, QSIM_ECUDA, h->err) : QSIM_OK;
+    for (Handle *h : R) {
+        permute_local(h, perm);
+        for (int q = 0; q < h->n; ++q) h->pos[q] = h->n - 1 - q;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return check_cuda(h, e, "canonicalize");
+        if (h->poisoned) return fail(h, QSIM_ECUDA, h->err);
+    }
+    return QSIM_OK;
 }
 
-int dist_allgather_doubles(Handle *h, const double *d_in, double *d_out, size_t count)
+int dist_sum_host(const Ranks &R, const std::vector<std::vector<double>> &parts, double *out, size_t count)
 {
+    Handle *h = R[0];
+    if (R.size() > 1 || h->world == 1) {
+        // all ranks are here: fixed rank order
+        std::vector<double> acc(count, 0.0);
+        for (size_t r = 0; r < R.size(); ++r)
+            for (size_t i = 0; i < count; ++i) acc[i] += parts[r][i];
+        std::memcpy(out, acc.data(), count * sizeof(double));
+        return QSIM_OK;
+    }
 #ifndef QSIM_NO_NCCL
-    return nccl_check(h, ncclAllGather(d_in, d_out, count, ncclDouble, h->comm, h->stream), "ncclAllGather");
-#else
-    (void)d_in; (void)d_out; (void)count;
-    return fail(h, QSIM_ENCCL, "built without NCCL");
-#endif
-}
-
-// Sum a host vector over ranks in fixed rank order (allgather + host sum).
-int dist_allreduce_sum_host(Handle *h, double *host, size_t count)
-{
-    if (h->world == 1) return QSIM_OK;
+    // one rank of a multi-process world: allgather, then the same fixed-order sum
     double *d_in = nullptr, *d_out = nullptr;
     if (cudaMalloc(&d_in, count * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&d_out, count * h->world * sizeof(double)) != cudaSuccess) {
         cudaGetLastError();
         if (d_in) cudaFree(d_in);
-        return fail(h, QSIM_ENOMEM, "allreduce buffers");
+        return fail(h, QSIM_ENOMEM, "allgather buffers");
     }
-    cudaMemcpyAsync(d_in, host, count * sizeof(double), cudaMemcpyHostToDevice, h->stream);
-    int rc = dist_allgather_doubles(h, d_in, d_out, count);
+    cudaMemcpyAsync(d_in, parts[0].data(), count * sizeof(double), cudaMemcpyHostToDevice, h->stream);
+    int rc = nccl_check(h, ncclAllGather(d_in, d_out, count, ncclDouble, h->comm, h->stream), "ncclAllGather");
     std::vector<double> all(count * h->world);
     if (!rc) rc = check_cuda(h, cudaMemcpyAsync(all.data(), d_out, all.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "allgather copy");
     if (!rc) rc = check_cuda(h, cudaStreamSynchronize(h->stream), "allgather");
@@ -213,9 +265,12 @@ int dist_allreduce_sum_host(Handle *h, double *host, size_t count)
     for (size_t i = 0; i < count; ++i) {
         double s = 0.0;
         for (int r = 0; r < h->world; ++r) s += all[(size_t)r * count + i];
-        host[i] = s;
+        out[i] = s;
     }
     return QSIM_OK;
+#else
+    return fail(h, QSIM_ENCCL, "built without NCCL");
+#endif
 }
 
 }  // namespace qs

@@ -194,6 +194,10 @@ struct Handle {
     int fuse = 1;
     GOp *d_ops = nullptr;
     size_t d_ops_cap = 0;
+    // in-process rank group (qsim_create_group): the group handle owns the
+    // member handles (one shard each); members point back at the group
+    std::vector<Handle *> members;
+    Handle *grp = nullptr;
 
     uint64_t local_dim() const { return (uint64_t)1 << nl; }
 };
@@ -216,13 +220,20 @@ inline void swap_buffers(Handle *h)
     h->scratch = t;
 }
 
-// distributed layer (dist.cu)
-int dist_make_local(Handle *h, const std::vector<int> &need);  // make logical qubits local
-int dist_canonicalize(Handle *h);                                // pos[q] = n-1-q everywhere
-int dist_allgather_doubles(Handle *h, const double *d_in, double *d_out, size_t count);
-int dist_allreduce_sum_host(Handle *h, double *host, size_t count);  // fixed rank order
+// The rank shards this process drives: one handle (single GPU, or one rank
+// of a multi-process NCCL world), or every member of an in-process group.
+using Ranks = std::vector<Handle *>;
+inline Ranks ranks_of(Handle *h) { return h->members.empty() ? Ranks{h} : h->members; }
+
+// distributed layer (dist.cu): every step runs on all ranks of R in lock step
+int dist_make_local(const Ranks &R, const std::vector<int> &need);   // make logical qubits local
+int dist_canonicalize(const Ranks &R);                               // pos[q] = n-1-q everywhere
+// per-rank host partials -> the sum over all ranks of the world, in rank order
+// (parts[i] belongs to R[i]); out may alias parts[0]
+int dist_sum_host(const Ranks &R, const std::vector<std::vector<double>> &parts, double *out, size_t count);
 // run every queued gate (fused passes); called before anything that reads or moves data
 int flush_queue(Handle *h);
+int flush_all(const Ranks &R);
 // local bit-permutation pass (api.cu): new position of old local position p is perm[p]
 void permute_local(Handle *h, const std::vector<int> &perm);
 

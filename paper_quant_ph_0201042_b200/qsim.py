@@ -77,6 +77,7 @@ def _sig(name, res, *args):
 _sig("qsim_create", _i32, _i32, _i32, C.POINTER(_H))
 _sig("qsim_create_dist", _i32, _i32, _i32, _i32, _i32, _p, C.POINTER(_H))
 _sig("qsim_nccl_unique_id", _i32, _p)
+_sig("qsim_create_group", _i32, _i32, _i32, _p, C.POINTER(_H))
 _sig("qsim_destroy", None, _H)
 _sig("qsim_last_error", C.c_char_p, _H)
 _sig("qsim_memory_bytes", _u64, _i32)
@@ -133,6 +134,15 @@ def qsim_create_dist(n: int, world: int, rank: int, device: int, nccl_id: bytes)
     h = _H()
     buf = C.create_string_buffer(bytes(nccl_id), 128)
     _chk(None, lib.qsim_create_dist(n, world, rank, device, buf, C.byref(h)))
+    return h
+
+
+def qsim_create_group(n: int, world: int, devices=None):
+    h = _H()
+    dev = None
+    if devices is not None:
+        dev = np.ascontiguousarray(np.asarray(devices, dtype=np.int32))
+    _chk(None, lib.qsim_create_group(n, world, dev.ctypes.data if dev is not None else None, C.byref(h)))
     return h
 
 
