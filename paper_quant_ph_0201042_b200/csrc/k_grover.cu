@@ -11,6 +11,9 @@
 // and records |alpha_k|^2 for this iteration.  At n = 20 the 16 MiB state
 // stays resident in the 126 MB L2, so an iteration costs one L2 read+write
 // of the state plus one launch.
+#include <cooperative_groups.h>
+#include <cstdlib>
+
 #include "qsim_internal.h"
 
 namespace qs {
@@ -102,12 +105,121 @@ __global__ void __launch_bounds__(kThreads) k_grover_iter(double2 *__restrict__ 
     }
 }
 
+// Persistent variant for states that fit in shared memory across the GPU
+// (n <= 20: 2^20 amplitudes = 128 CTAs x 8192 x 16 B): one cooperative
+// launch runs every iteration; each CTA keeps its contiguous chunk of the
+// state in shared memory for the whole search, so an iteration costs no
+// DRAM/L2 traffic for the state -- only the block partial sums
+// (double-buffered by iteration parity) and one grid barrier.  Every block
+// reduces the partials in the same fixed order, so all blocks compute the
+// identical mean.
+namespace cg = cooperative_groups;
+
+constexpr int kPersistThreads = 512;
+
+__global__ void __launch_bounds__(kPersistThreads) k_grover_persist(double2 *__restrict__ psi, uint64_t N, uint64_t chunk,
+                                                                    uint64_t k, int iters, double *__restrict__ trace,
+                                                                    double2 *__restrict__ part, double2 *__restrict__ akbuf)
+{
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double2 st[];
+    __shared__ double2 sh[32];
+    __shared__ double2 s_mean;
+    const unsigned nb = gridDim.x;
+    const uint64_t base = (uint64_t)blockIdx.x * chunk;
+    const bool own_k = k >= base && k < base + chunk;
+    const uint32_t kl = (uint32_t)(k - base);
+    double2 acc = make_double2(0.0, 0.0);
+    for (uint32_t i = threadIdx.x; i < chunk; i += blockDim.x) {
+        const double2 a = psi[base + i];
+        st[i] = a;
+        acc.x += a.x;
+        acc.y += a.y;
+    }
+    auto publish = [&](int p, double2 a) {
+        const double2 s = block_sum2(a, sh);
+        if (threadIdx.x == 0) part[(size_t)p * nb + blockIdx.x] = s;
+        grid.sync();
+        if (threadIdx.x < 32) {
+            double2 t = make_double2(0.0, 0.0);
+            for (unsigned b = threadIdx.x; b < nb; b += 32) {
+                const double2 q = __ldcg(&part[(size_t)p * nb + b]);
+                t.x += q.x;
+                t.y += q.y;
+            }
+            t = warp_sum2(t);
+            if (threadIdx.x == 0) {
+                const double2 ak = __ldcg(&akbuf[p]);
+                const double inv = 1.0 / (double)N;
+                s_mean = make_double2((t.x - 2.0 * ak.x) * inv, (t.y - 2.0 * ak.y) * inv);
+            }
+        }
+        __syncthreads();
+    };
+    __syncthreads();
+    if (own_k && threadIdx.x == 0) akbuf[0] = st[kl];
+    publish(0, acc);
+    for (int t = 0; t < iters; ++t) {
+        const int p = (t + 1) & 1;
+        const double2 mean = s_mean;
+        const double m2x = 2.0 * mean.x, m2y = 2.0 * mean.y;
+        acc = make_double2(0.0, 0.0);
+        for (uint32_t i = threadIdx.x; i < chunk; i += blockDim.x) {
+            double2 a = st[i];
+            if (own_k && i == kl) { a.x = -a.x; a.y = -a.y; }   // V_{f_k}
+            a = make_double2(m2x - a.x, m2y - a.y);             // 2|s><s| - I
+            st[i] = a;
+            acc.x += a.x;
+            acc.y += a.y;
+        }
+        __syncthreads();
+        if (own_k && threadIdx.x == 0) {
+            const double2 ak = st[kl];
+            akbuf[p] = ak;
+            if (trace) trace[t] = fma(ak.x, ak.x, ak.y * ak.y);
+        }
+        publish(p, acc);
+    }
+    for (uint32_t i = threadIdx.x; i < chunk; i += blockDim.x) psi[base + i] = st[i];
+}
+
 }  // namespace
+
+static bool try_persist(Handle *h, uint64_t mark, int iters, double *d_trace)
+{
+    const uint64_t N = h->local_dim();
+    // the largest power-of-two grid that is co-resident (one CTA per SM)
+    uint64_t blocks = 1;
+    while (blocks * 2 <= (uint64_t)h->num_sms && blocks * 2 <= N / kPersistThreads) blocks *= 2;
+    const uint64_t chunk = N / blocks;
+    const size_t smem = chunk * sizeof(double2);
+    if (smem > 200 * 1024 || blocks > kMaxBlocks) return false;
+    cudaFuncSetAttribute(k_grover_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grover_persist, kPersistThreads, smem);
+    if (per_sm < 1 || blocks > (uint64_t)per_sm * h->num_sms) return false;
+    ensure_red(h, 8 + 4 * (size_t)blocks + 8);
+    double2 *part = reinterpret_cast<double2 *>(h->d_red + 8);
+    double2 *akbuf = part + 2 * blocks;
+    void *args[] = {(void *)&h->psi, (void *)&N,      (void *)&chunk, (void *)&mark,
+                    (void *)&iters,  (void *)&d_trace, (void *)&part,  (void *)&akbuf};
+    prof_begin(h);
+    cudaError_t e = cudaLaunchCooperativeKernel((void *)k_grover_persist, dim3((unsigned)blocks), dim3(kPersistThreads),
+                                                args, smem, h->stream);
+    prof_end(h, "k_grover_persist", N * 32);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return true;
+}
 
 void launch_grover(Handle *h, uint64_t mark_local, int mark_rank, int iters, double *d_trace)
 {
     (void)mark_rank;
     const uint64_t N = h->local_dim();
+    // whole state in registers: <= 16 amplitudes per thread over the resident grid
+    if (!getenv("QSIM_NO_GROVER_PERSIST") && N >= 4096 && try_persist(h, mark_local, iters, d_trace)) return;
     unsigned blocks = (unsigned)h->num_sms * 4;
     if (blocks > kMaxBlocks) blocks = kMaxBlocks;
     uint64_t chunk = (N + blocks - 1) / blocks;
