@@ -548,25 +548,37 @@ int qs::flush_queue(Handle *h)
                     const QOp &q = take[i];
                     GOp g;
                     std::memset(&g, 0, sizeof g);
-                    g.kind = q.diag ? GOP_DIAG : GOP_DENSE;
                     for (int k = 0; k < 4; ++k) g.u[k] = q.u[k];
-                    g.rb = 0;
-                    g.tbit = -1;
-                    g.fbit = -1;
-                    if (!q.diag) {
-                        const int t = tbit_of[q.tpos];
+                    auto win_idx = [&](int t) {
                         for (int b = 0; b < kRegBits; ++b)
-                            if (wins[s][b] == t) g.rb = b;
-                    } else if (q.tpos >= 0) {
-                        if (tbit_of[q.tpos] >= 0) g.tbit = tbit_of[q.tpos];
-                        else g.fbit = fix_of[q.tpos];
+                            if (wins[s][b] == t) return b;
+                        return -1;
+                    };
+                    if (!q.diag) {
+                        g.kind = GOP_DENSE;
+                        g.rb = (uint8_t)win_idx(tbit_of[q.tpos]);
+                    } else if (q.tpos < 0) {
+                        g.kind = GOP_PHASE;
+                    } else if (tbit_of[q.tpos] >= 0) {
+                        const int w = win_idx(tbit_of[q.tpos]);
+                        if (w >= 0) { g.kind = GOP_DIAGW; g.rb = (uint8_t)w; }
+                        else { g.kind = GOP_DIAGT; g.tb = 1u << tbit_of[q.tpos]; }
+                    } else {
+                        g.kind = GOP_DIAGF;
+                        g.fbit = (uint32_t)fix_of[q.tpos];
                     }
                     for (int p = 0; p < nl; ++p) {
                         if (!((q.cmask >> p) & 1)) continue;
                         const uint64_t want = (q.cval >> p) & 1;
                         if (tbit_of[p] >= 0) {
-                            g.cm |= 1u << tbit_of[p];
-                            g.cv |= (uint32_t)want << tbit_of[p];
+                            const int w = win_idx(tbit_of[p]);
+                            if (w >= 0) {
+                                g.wm |= (uint8_t)(1u << w);
+                                g.wv |= (uint8_t)(want << w);
+                            } else {
+                                g.tm |= 1u << tbit_of[p];
+                                g.tv |= (uint32_t)want << tbit_of[p];
+                            }
                         } else {
                             g.fm |= 1ull << fix_of[p];
                             g.fv |= want << fix_of[p];

@@ -21,38 +21,6 @@ namespace {
 
 using namespace tile;
 
-__device__ __forceinline__ double2 cfma2(double2 u, double2 x, double2 v, double2 y)
-{
-    double re = fma(u.x, x.x, -u.y * x.y);
-    double im = fma(u.x, x.y, u.y * x.x);
-    re = fma(v.x, y.x, re);
-    re = fma(-v.y, y.y, re);
-    im = fma(v.x, y.y, im);
-    im = fma(v.y, y.x, im);
-    return make_double2(re, im);
-}
-
-// dense 2x2 on register bit RB for every slot pair passing the tile controls
-template <int RB>
-__device__ __forceinline__ void dense_rb(double2 (&v)[NS], const GOp &op, uint32_t tpart, const uint32_t (&wb)[kRegBits])
-{
-    const double2 u0 = op.u[0], u1 = op.u[1], u2 = op.u[2], u3 = op.u[3];
-#pragma unroll
-    for (int k = 0; k < NS; ++k) {
-        if (k & (1 << RB)) continue;
-        if (op.cm) {
-            uint32_t ti = tpart;
-#pragma unroll
-            for (int b = 0; b < kRegBits; ++b)
-                if (k & (1 << b)) ti |= wb[b];
-            if ((ti & op.cm) != op.cv) continue;
-        }
-        const double2 x = v[k], y = v[k | (1 << RB)];
-        v[k] = cfma2(u0, x, u1, y);
-        v[k | (1 << RB)] = cfma2(u2, x, u3, y);
-    }
-}
-
 __global__ void __launch_bounds__(256, 1) k_ops_pass(const __grid_constant__ OpsPass P, const GOp *__restrict__ ops,
                                                      const double2 *in, double2 *out, uint64_t ntiles)
 {
@@ -124,34 +92,7 @@ __global__ void __launch_bounds__(256, 1) k_ops_pass(const __grid_constant__ Ops
 #pragma unroll
                 for (int k = 0; k < NS; ++k) v[k] = tile_buf[o[k]];
             }
-            for (int i = sg.op_begin; i < sg.op_end; ++i) {
-                const GOp &op = i < kOpsSmem ? sops[i] : ops[i];
-                if ((T & op.fm) != op.fv) continue;          // controls on fixed bits (uniform)
-                if (op.kind == GOP_DENSE) {
-                    switch (op.rb) {
-                    case 0: dense_rb<0>(v, op, tpart, wb); break;
-                    case 1: dense_rb<1>(v, op, tpart, wb); break;
-                    case 2: dense_rb<2>(v, op, tpart, wb); break;
-                    default: dense_rb<3>(v, op, tpart, wb); break;
-                    }
-                } else {
-                    // diagonal diag(d0, d1) on tile bit op.tbit (or a fixed bit:
-                    // the value then comes from the tile id)
-                    const double2 d0 = op.u[0], d1 = op.u[3];
-                    const int fb = op.fbit;
-                    const uint32_t fixed_val = fb >= 0 ? (uint32_t)((T >> fb) & 1u) : 0u;
-#pragma unroll
-                    for (int k = 0; k < NS; ++k) {
-                        uint32_t ti = tpart;
-#pragma unroll
-                        for (int b = 0; b < kRegBits; ++b)
-                            if (k & (1 << b)) ti |= wb[b];
-                        if ((ti & op.cm) != op.cv) continue;
-                        const uint32_t bit = fb >= 0 ? fixed_val : (op.tbit >= 0 ? (ti >> op.tbit) & 1u : 1u);
-                        v[k] = cmul(v[k], bit ? d1 : d0);
-                    }
-                }
-            }
+            run_ops(v, P.nops <= kOpsSmem ? sops : ops, sg.op_begin, sg.op_end, T, tpart);
             prev_tpart = tpart;
             prev_stp = stp;
 #pragma unroll
@@ -179,6 +120,7 @@ __global__ void __launch_bounds__(256, 1) k_ops_pass(const __grid_constant__ Ops
 
 void launch_ops_pass(Handle *h, const OpsPass &P, const GOp *d_ops)
 {
+    if (launch_ops_pass_tma(h, P, d_ops)) return;
     const size_t smem = (sizeof(double2) << P.tbits);
     static bool attr = false;
     if (!attr) {

@@ -119,17 +119,23 @@ void finish_tile_pass(TilePass &tp);
 bool launch_tile_pass_tma(Handle *h, const TilePass &tp, const double2 *in, double2 *out);
 
 // Fused gate-list passes (k_ops.cu): ops of one pass, applied per tile.
-enum { GOP_DENSE = 0, GOP_DIAG = 1 };
+// Op kinds (encoded per segment on the host, so the kernel's per-op work is
+// a few uniform tests and statically indexed register updates):
+//   DENSE   2x2 on window bit rb          DIAGW  diag(d0, d1) on window bit rb
+//   DIAGT   diag on a thread-part bit     DIAGF  diag on a fixed (tile-id) bit
+//   PHASE   constant phase u[3]
+// Controls: wm/wv on the 4 window bits (slot index), tm/tv on the other tile
+// bits (thread part), fm/fv on fixed bits (tile id).
+enum { GOP_DENSE = 0, GOP_DIAGW = 1, GOP_DIAGT = 2, GOP_DIAGF = 3, GOP_PHASE = 4 };
 struct GOp {
-    int kind;          // GOP_DENSE / GOP_DIAG
-    int rb;            // dense: register bit of the target in its segment's window
-    int tbit;          // diag: tile bit of the target (used when fbit < 0 and tbit >= 0)
-    int fbit;          // diag: tile-id bit of a fixed target, or -1; tbit = fbit = -1: constant phase u[3]
-    uint32_t cm, cv;   // controls on tile bits (tile-index mask / values)
+    uint8_t kind, rb, wm, wv;
+    uint32_t tm, tv;   // controls on non-window tile bits
+    uint32_t tb;       // DIAGT: mask of the target tile bit
+    uint32_t fbit;     // DIAGF: tile-id bit of the target
     uint64_t fm, fv;   // controls on fixed bits (tile-id mask / values)
     double2 u[4];      // dense U (u11 u12 u21 u22) or diag(u[0], u[3])
 };
-constexpr int kOpsSmem = 64;   // ops cached in shared memory per CTA
+constexpr int kOpsSmem = 64;   // ops cached in static shared memory by k_ops_pass
 constexpr int kMaxSegs = 48;
 struct OpsSeg {
     TileMap map;       // register window + thread order
@@ -144,6 +150,7 @@ struct OpsPass {
     OpsSeg seg[kMaxSegs];
 };
 void launch_ops_pass(Handle *h, const OpsPass &P, const GOp *d_ops);
+bool launch_ops_pass_tma(Handle *h, const OpsPass &P, const GOp *d_ops);   // k_tma.cu
 
 // A queued gate in physical local positions (api.cu gate queue).
 struct QOp {
