@@ -150,14 +150,17 @@ void launch_norm(Handle *h, double *d_out)
     // chunks of 2^12 (or the whole shard if smaller), then one tree over them
     const int bb = h->nl < 12 ? h->nl : 12;
     const uint64_t nb = h->local_dim() >> bb;
-    ensure_red(h, nb + 8);
+    // d_out may live in the reduction workspace: keep it valid across a regrow
+    const bool in_ws = h->d_red && d_out >= h->d_red && d_out < h->d_red + h->red_cap;
+    const size_t off = in_ws ? (size_t)(d_out - h->d_red) : 0;
+    ensure_red(h, nb + (nb >> 10) + 16);
+    if (in_ws) d_out = h->d_red + off;
     launch_block_abs2(h, bb, h->d_red + 8);
     if (nb <= (1u << 20)) {
         sum_tree(h, h->d_red + 8, nb, d_out);
     } else {
         // two levels (n_local > 32)
         const uint64_t nb2 = nb >> 10;
-        ensure_red(h, nb + nb2 + 8);
         prof_begin(h);
         k_sum_doubles<<<(unsigned)nb2, 1024, 0, h->stream>>>(h->d_red + 8, 1024, 1024, h->d_red + 8 + nb);
         prof_end(h, "k_sum_doubles", nb * 8);

@@ -427,3 +427,55 @@ def test_fusion_is_a_single_pass_for_small_registers(reg):
     assert Q.qsim_launch_count(h) - l0 <= 3
     ref, _, _ = O.cfg0(10, 1, 200)
     assert maxdiff(get(h, 10), ref) < TOL
+
+
+# ------------------------------------------------------------------ full-size configs
+def test_cfg1_full_size_oracle_parity(reg):
+    """configs[1] exactly as specified (n = 20, 804 iterations) against the
+    oracle's literal -H_n V_f0 H_n V_fk circuit, element by
+    element, trace and final state."""
+    n = 20
+    h = reg(n)
+    k, trace = W.run_cfg1(h, n=n, seed=2)
+    ref, rtrace = O.cfg1(n=n, seed=2, iters=804)
+    assert np.max(np.abs(trace - rtrace)) < TOL
+    assert maxdiff(get(h, n), ref) < TOL
+
+
+def _cfg4_inverse(h, n, layers, seed, sigma, events):
+    """Apply the exact inverse of configs[4] (same noise realisation) through
+    the C-ABI, with matrices built by the oracle's own angle code."""
+    import math as _m
+    g0s, g = [], 0
+    for l in range(layers):
+        g0s.append(g)
+        g += n + len(range(l & 1, n - 1, 2))
+    byl = {}
+    for (l, q, k) in events:
+        byl.setdefault(l, []).append((q, k))
+    for l in reversed(range(layers)):
+        for (q, k) in reversed(byl.get(l, [])):
+            Q.qsim_apply_1q(h, q, O.pauli(k))              # Paulis are involutions
+        g0 = g0s[l]
+        cnots = list(range(l & 1, n - 1, 2))
+        for i, c in reversed(list(enumerate(cnots))):
+            U = O.mat_angles(O.RP, [_m.pi / 2, _m.pi], seed=seed, sigma=sigma, g=g0 + n + i)
+            Q.qsim_apply_ctrl(h, 1 << c, 1 << c, c + 1, U.conj().T)
+        for q in reversed(range(n)):
+            U = O.mat_angles(O.HAAR, O.haar_angles(seed, l * n + q), seed=seed, sigma=sigma, g=g0 + q)
+            Q.qsim_apply_1q(h, q, U.conj().T)
+
+
+@pytest.mark.parametrize("n", [20, 32])
+def test_cfg4_mirror_returns_to_zero(reg, n):
+    """configs[4] (n = 32 is the full single-GPU size, 64 GiB): the circuit
+    followed by its exact inverse built from the oracle's matrices returns to
+    |0..0> -- pins every noisy gate applied by the GPU at a size the oracle
+    cannot simulate; the norm stays 1 to 1e-12 throughout."""
+    layers, seed, sigma, p = 20, 5, 1e-3, 1e-4 if n == 32 else 0.02
+    h = reg(n)
+    ev = W.run_cfg4(h, n=n, layers=layers, seed=seed, sigma=sigma, p=p)
+    assert abs(Q.qsim_norm(h) - 1) < 1e-12
+    _cfg4_inverse(h, n, layers, seed, sigma, ev)
+    assert Q.qsim_prob_index(h, 0) > 1 - 1e-10
+    assert abs(Q.qsim_norm(h) - 1) < 1e-12
