@@ -21,7 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 TAG_GATE, TAG_HAAR, TAG_PAIR, TAG_OPNOISE, TAG_MARK = 1, 2, 3, 4, 5
-TAG_BASE, TAG_GAUSS, TAG_PAULI, TAG_MEASURE = 6, 7, 8, 9
+TAG_BASE, TAG_GAUSS, TAG_PAULI, TAG_MEASURE, TAG_SHOR = 6, 7, 8, 9, 10
 RP, P1, HAAR = 0, 1, 2
 
 
@@ -92,6 +92,11 @@ _sig("orc_shor_base", _u64, _u64, _u64)
 _sig("orc_cfg3", None, _p, _i32, _i32, _u64, _u64, _u64, _f64, _p)
 _sig("orc_cfg4", _i32, _p, _i32, _i32, _u64, _f64, _f64, _p, _i32)
 _sig("orc_inject_paulis", None, _p, _i32, _u64, _u64, _u64, _f64, _p, _i32, _p)
+_sig("orc_shor_prob_succ", _f64, _u64, _u64)
+_sig("orc_shor_semantic_state", None, _p, _i32, _u64, _u64, _u64)
+_sig("orc_shor_candidates", _i32, _u64, _i32, _u64, _p, _i32)
+_sig("orc_shor_try", _u64, _u64, _u64, _u64, _i32)
+_sig("orc_shor_run", _i32, _u64, _i32, _u64, _u64, _i32, _i32, C.POINTER(_u64))
 
 
 def _ptr(a: np.ndarray) -> int:
@@ -315,3 +320,35 @@ def cfg4(n=32, layers=20, seed=5, sigma=1e-3, p=1e-4, cap=4096):
     ev = np.zeros(3 * cap, np.int32)
     nev = _lib.orc_cfg4(_state(psi), n, layers, seed, sigma, p, _ptr(ev), cap)
     return psi, [tuple(int(x) for x in ev[3 * i: 3 * i + 3]) for i in range(min(nev, cap))]
+
+
+# ---------------------------------------------------------------- Shor (row f3)
+def shor_prob_succ(n, phi) -> float:
+    """Prob_succ(n) of PAPER.md:907-920 (natural logarithms)."""
+    return _lib.orc_shor_prob_succ(n, phi)
+
+
+def shor_semantic_state(m, x, N, v):
+    """Uniform superposition over {a < 2^m : x^a = v mod N}."""
+    psi = np.zeros(1 << m, np.complex128)
+    _lib.orc_shor_semantic_state(_state(psi), m, x, N, v)
+    return psi
+
+
+def shor_candidates(y, m, N):
+    """Convergent denominators r < N of y/2^m within 1/2^(m+1)."""
+    out = np.zeros(64, np.uint64)
+    k = _lib.orc_shor_candidates(y, m, N, _ptr(out), 64)
+    return [int(v) for v in out[:k]]
+
+
+def shor_try(N, x, r, gcd_check=False) -> int:
+    """Steps 4-5 for one candidate r (GCD check 979-981)."""
+    return _lib.orc_shor_try(N, x, r, int(bool(gcd_check)))
+
+
+def shor_run(N, m, seed, run, improved=False, max_iter=200):
+    """One factoring run; returns (iterations, factor)."""
+    f = C.c_uint64(0)
+    t = _lib.orc_shor_run(N, m, seed, run, int(bool(improved)), max_iter, C.byref(f))
+    return t, f.value

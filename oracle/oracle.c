@@ -39,7 +39,7 @@ typedef double complex cplx;
 /* ------------------------------------------------------------------------ */
 
 enum { TAG_GATE = 1, TAG_HAAR = 2, TAG_PAIR = 3, TAG_OPNOISE = 4, TAG_MARK = 5,
-       TAG_BASE = 6, TAG_GAUSS = 7, TAG_PAULI = 8, TAG_MEASURE = 9 };
+       TAG_BASE = 6, TAG_GAUSS = 7, TAG_PAULI = 8, TAG_MEASURE = 9, TAG_SHOR = 10 };
 
 /* One Philox4x32 round: two 32x32->64 multiplies, xor with key. */
 static void philox_round(uint32_t c[4], const uint32_t k[2])
@@ -703,4 +703,139 @@ int orc_cfg4(cplx *psi, int n, int layers, uint64_t seed, double sigma, double p
         orc_inject_paulis(psi, n, seed, (uint64_t)l, all, p, ev, cap, &nev);
     }
     return nev;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Shor's factoring, semantic mode and classical post-processing             */
+/* (PAPER.md:827-859 algorithm box; 896-903 semantic mode; 907-920           */
+/* Prob_succ; 969-998 improvements).  SURVEY.md §8(f) row f3.                */
+/* ------------------------------------------------------------------------ */
+
+/* Prob_succ(n) = (1 - phi/(n-1)) + phi/(n-1) * (1/2 * 4/pi^2 * e^-gamma / log log n),
+ * natural logarithms. */
+double orc_shor_prob_succ(uint64_t n, uint64_t phi)
+{
+    const double gamma = 0.57721566490153286061;
+    const double f = (double)phi / (double)(n - 1);
+    return (1.0 - f) + f * (0.5 * 4.0 / (ORC_PI * ORC_PI) * exp(-gamma) / log(log((double)n)));
+}
+
+/* Semantic-mode register: the first register is not
+ * generated; the second (m qubits, value a) holds the uniform superposition
+ * over {a : x^a = v (mod N)}. */
+void orc_shor_semantic_state(cplx *psi, int m, uint64_t x, uint64_t N, uint64_t v)
+{
+    const uint64_t M = (uint64_t)1 << m;
+    uint64_t c = 0;
+    uint64_t p = 1 % N;
+    for (uint64_t a = 0; a < M; ++a) {
+        psi[a] = (p == v) ? 1.0 : 0.0;
+        c += p == v;
+        p = (uint64_t)(((unsigned __int128)p * x) % N);
+    }
+    const double s = 1.0 / sqrt((double)c);
+    for (uint64_t a = 0; a < M; ++a) psi[a] *= s;
+}
+
+/* Continued-fraction convergents k/r of y / 2^m (step 4):
+ * every convergent with 0 < r < N and |y/2^m - k/r| <= 1/2^(m+1), in order
+ * of increasing r.  Returns the count (<= cap). */
+int orc_shor_candidates(uint64_t y, int m, uint64_t N, uint64_t *r_out, int cap)
+{
+    const uint64_t M = (uint64_t)1 << m;
+    if (y == 0) return 0;
+    /* expansion of y / M with exact integers */
+    uint64_t num = y, den = M;
+    uint64_t p0 = 0, q0 = 1, p1 = 1, q1 = 0;   /* convergents h_{-2}/k_{-2}, h_{-1}/k_{-1} */
+    int cnt = 0;
+    while (den != 0) {
+        const uint64_t a = num / den;
+        const uint64_t t = num - a * den;
+        num = den;
+        den = t;
+        const uint64_t p2 = a * p1 + p0, q2 = a * q1 + q0;
+        p0 = p1; q0 = q1; p1 = p2; q1 = q2;
+        if (q1 >= N) break;
+        if (q1 == 0) continue;
+        /* |y/M - p/q| <= 1/(2M)  <=>  |2 (y q - p M)| <= q */
+        const __int128 diff = (__int128)y * q1 - (__int128)p1 * M;
+        const __int128 ad = diff < 0 ? -diff : diff;
+        if (2 * ad <= (__int128)q1 && p1 > 0 && cnt < cap) r_out[cnt++] = q1;
+    }
+    return cnt;
+}
+
+/* Steps 4-5 for one candidate r.  gcd_check = 1 is the
+ * "GCD Check" improvement: d+- are tried even when
+ * x^r != 1.  Returns a nontrivial factor of N or 0. */
+uint64_t orc_shor_try(uint64_t N, uint64_t x, uint64_t r, int gcd_check)
+{
+    if (r == 0 || (r & 1)) return 0;
+    const uint64_t xr = orc_powmod(x, r, N);
+    if (xr != 1 % N && !gcd_check) return 0;
+    const uint64_t z = orc_powmod(x, r / 2, N);
+    if (!gcd_check && (z == 1 % N || z == N - 1)) return 0;
+    const uint64_t d1 = orc_gcd(N, (z + N - 1) % N), d2 = orc_gcd(N, (z + 1) % N);
+    if (d1 > 1 && d1 < N) return d1;
+    if (d2 > 1 && d2 < N) return d2;
+    return 0;
+}
+
+static uint64_t lcm64(uint64_t a, uint64_t b) { return a / orc_gcd(a, b) * b; }
+
+/* One factoring run (PAPER.md:827-859 repeated until a factor is found):
+ * iteration t draws (a, b) = draw(seed, TAG_SHOR, run, t-1): x = 1 + uint(a, N-1),
+ * step 2 gcd; else the semantic order-finding register (2l = m qubits), the
+ * QFT, measurement with r = u01(b),
+ * then post-processing; improved = 1 adds the four checks of
+ * PAPER.md:969-998 (neighbour y+-1, y+-2; GCD check; multiples 2r..8r;
+ * lcm of remembered candidates).  Returns the iteration count (0: none
+ * within max_iter); *factor receives the factor. */
+int orc_shor_run(uint64_t N, int m, uint64_t seed, uint64_t run, int improved, int max_iter, uint64_t *factor)
+{
+    const uint64_t M = (uint64_t)1 << m;
+    cplx *psi = (cplx *)malloc(sizeof(cplx) * M);
+    uint64_t mem[64];
+    int nmem = 0;
+    *factor = 0;
+    for (int t = 1; t <= max_iter; ++t) {
+        uint64_t d[2];
+        orc_draw(seed, TAG_SHOR, run, (uint32_t)(t - 1), d);
+        const uint64_t x = 1 + orc_uint(d[0], N - 1);
+        const uint64_t g = orc_gcd(x, N);
+        if (g > 1 && g < N) { *factor = g; free(psi); return t; }
+        /* semantic register: v = x^a* for a uniform a* is the first-register outcome */
+        const uint64_t astar = orc_uint(d[1], M);
+        const uint64_t v = orc_powmod(x, astar, N);
+        orc_shor_semantic_state(psi, m, x, N, v);
+        orc_noise_t nz = { 0, 0.0, 0 };
+        orc_qft(psi, m, 0, m, 0, &nz);
+        uint64_t dm[2];
+        orc_draw(seed, TAG_MEASURE, run, (uint32_t)(t - 1), dm);
+        const uint64_t y = orc_measure(psi, m, orc_u01(dm[0]));
+        /* post-processing */
+        uint64_t f = 0;
+        const int nys = improved ? 5 : 1;
+        const int64_t dy[5] = { 0, 1, -1, 2, -2 };
+        for (int iy = 0; iy < nys && !f; ++iy) {
+            const int64_t yy = (int64_t)y + dy[iy];
+            if (yy <= 0 || (uint64_t)yy >= M) continue;
+            uint64_t rs[64];
+            const int nr = orc_shor_candidates((uint64_t)yy, m, N, rs, 64);
+            for (int i = 0; i < nr && !f; ++i) {
+                const uint64_t r = rs[i];
+                f = orc_shor_try(N, x, r, 0);
+                if (!f && improved) f = orc_shor_try(N, x, r, 1);
+                if (!f && improved && orc_powmod(x, r, N) != 1 % N)
+                    for (uint64_t k = 2; k <= 8 && !f; ++k) f = orc_shor_try(N, x, k * r, 1);
+                if (!f && improved) {
+                    for (int j = 0; j < nmem && !f; ++j) f = orc_shor_try(N, x, lcm64(mem[j], r), 1);
+                    if (nmem < 64) mem[nmem++] = r;
+                }
+            }
+        }
+        if (f) { *factor = f; free(psi); return t; }
+    }
+    free(psi);
+    return 0;
 }

@@ -35,3 +35,19 @@ def order(a, N):
         x = (x * a) % N
         r += 1
     return r
+
+
+def fejer_branch(M, r, c, y):
+    """P(y) after the QFT of the uniform superposition over a0, a0+r, ...,
+    a0+(c-1)r (one branch of the sum above, PAPER.md:896-903 semantic mode):
+    |sum_j e^{2 pi i (a0 + j r) y / M}|^2 / (c M) = F_c(T/M) / (c M),
+    T = r y mod M, with the same exact integer reduction.  y: int array."""
+    y = np.asarray(y, dtype=object)
+    T = np.array([(r * int(v)) % M for v in y.ravel()], dtype=np.int64)
+    X = np.array([(c * int(t)) % M for t in T], dtype=np.int64)
+    X = np.minimum(X, M - X)
+    Tf = np.minimum(T, M - T)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        F = np.sin(np.pi * X / M) ** 2 / np.sin(np.pi * Tf / M) ** 2
+    F[T == 0] = c * c
+    return (F / (c * M)).reshape(np.shape(y))
