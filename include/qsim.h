@@ -67,7 +67,7 @@ enum { QSIM_GATE_RP = 0, QSIM_GATE_P1 = 1, QSIM_GATE_HAAR = 2 };
 enum {
     QSIM_TAG_GATE = 1, QSIM_TAG_HAAR = 2, QSIM_TAG_PAIR = 3, QSIM_TAG_OPNOISE = 4,
     QSIM_TAG_MARK = 5, QSIM_TAG_BASE = 6, QSIM_TAG_GAUSS = 7, QSIM_TAG_PAULI = 8,
-    QSIM_TAG_MEASURE = 9
+    QSIM_TAG_MEASURE = 9, QSIM_TAG_SHOR = 10
 };
 
 /* ---------------------------------------------------------------- lifecycle */
@@ -280,6 +280,50 @@ int qsim_prob_index(qsim_t *h, uint64_t idx, double *out);
  * then a scan of one block); if rounding leaves r >= the total, the largest i
  * with alpha_i != 0 (R22). */
 int qsim_measure(qsim_t *h, double r, uint64_t *idx);
+
+/* ---------------------------------------------------------------- Shor, semantic mode */
+/* Shor's factoring algorithm in the paper's semantic mode
+ * (modular exponentiation classical, first register not
+ * generated, QFT by the fast transform).  The exponent register is the whole
+ * handle: m = n = 2l qubits for an l-bit modulus, value a = basis index. */
+
+/* Prepare the post-measurement exponent register of step 3: the uniform
+ * superposition over {a < 2^n : x^a = v (mod N)}, amplitude 1/sqrt(count)
+ * (the predicate and the count are evaluated on the device).  Resets the
+ * layout to canonical and discards queued gates.  QSIM_ERANGE unless
+ * 3 <= N < 2^32; QSIM_EINVAL if x >= N or v >= N, or if no exponent matches
+ * (state then undefined). */
+int qsim_shor_semantic_state(qsim_t *h, uint64_t x, uint64_t N, uint64_t v);
+
+/* One factoring run: repeat the algorithm until a nontrivial factor of N is
+ * found or max_iter iterations have run.  Iteration t (1-based) draws
+ * (a, b) = draw(seed, QSIM_TAG_SHOR, run, t-1): x = 1 + uint(a, N-1); if
+ * 1 < gcd(x, N) < N step 2 succeeds; otherwise v = x^(uint(b, 2^n)) mod N
+ * (the outcome of measuring f(a) = x^a mod N), qsim_shor_semantic_state,
+ * qsim_qft(0, n), and y = qsim_measure(u01(draw(seed, QSIM_TAG_MEASURE, run,
+ * t-1).a)); then steps 4-5 on y.  improved = 1 adds the four checks of
+ * PAPER.md:969-998 (R27).  *iters = t of the success, 0 if none
+ * (then *factor = 0).  Overwrites the state.  QSIM_ERANGE unless
+ * 3 <= N < 2^32 and N^2 <= 2^n (the precision of PAPER.md:841-843). */
+int qsim_shor_run(qsim_t *h, uint64_t N, uint64_t seed, uint64_t run, int improved, int max_iter,
+                  uint64_t *factor, int *iters);
+
+/* Step 4's classical part: every convergent k/r of the
+ * continued fraction of y / 2^m with 0 < k, 0 < r < N and
+ * |y/2^m - k/r| <= 1/2^(m+1), in order of increasing r.  Writes up to cap
+ * denominators to r_out (host); returns their number, or QSIM_EINVAL. */
+int qsim_shor_candidates(uint64_t y, int m, uint64_t N, uint64_t *r_out, int cap);
+
+/* Step 5 for one candidate r: 0 (failure) if r is odd,
+ * x^r != 1 or x^(r/2) = -1 (mod N) ... else the nontrivial one of
+ * d+- = gcd(N, x^(r/2) +- 1).  gcd_check = 1 is the "GCD Check" of
+ * d+- are tried for every even r. */
+uint64_t qsim_shor_try(uint64_t N, uint64_t x, uint64_t r, int gcd_check);
+
+/* Prob_succ(N) of PAPER.md:907-920 for phi = phi(N), natural logarithms;
+ * 1 / Prob_succ is Table 5's "Theoretical" column.
+ * NaN unless 3 <= N and 0 < phi < N. */
+double qsim_shor_prob_succ(uint64_t N, uint64_t phi);
 
 /* ---------------------------------------------------------------- counter RNG */
 

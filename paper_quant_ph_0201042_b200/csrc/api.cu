@@ -345,6 +345,15 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse)
     std::vector<int> gsize(G, m / G);
     for (int g = 0; g < m % G; ++g) gsize[g]++;
     const bool block_moves = qft && h0->world == 1;
+    if (block_moves && G > 1 && gsize[0] < amax) {
+        // the first block lands on the lowest positions; with >= 7 wires its
+        // last register window stays clear of the 3 lowest, so the store keeps
+        // 128-byte thread runs and the pass fits the specialised kernel
+        // (k_qft_tma) -- put the full amax there, spread the rest evenly
+        gsize[0] = amax;
+        const int rest = m - amax, G1 = G - 1;
+        for (int g = 1; g < G; ++g) gsize[g] = rest / G1 + (g - 1 < rest % G1 ? 1 : 0);
+    }
     if (block_moves) {
         if (int rc = dist_canonicalize(R)) return rc;
     } else {
@@ -1435,6 +1444,116 @@ int qsim_measure(qsim_t *h, double r, uint64_t *idx)
     double v = 0.0;
     if (int rc = dist_sum_host(R, res, &v, 1)) return lift(h, R, rc);
     *idx = (uint64_t)v;
+    return QSIM_OK;
+}
+
+// ----------------------------------------------------------------- Shor, semantic mode
+static uint64_t host_powmod_u(uint64_t x, uint64_t e, uint64_t N)
+{
+    unsigned __int128 r = 1 % N, b = x % N;
+    for (; e; e >>= 1) {
+        if (e & 1) r = r * b % N;
+        b = b * b % N;
+    }
+    return (uint64_t)r;
+}
+
+int qsim_shor_semantic_state(qsim_t *h, uint64_t x, uint64_t N, uint64_t v)
+{
+    QS_CHECK_HANDLE(h);
+    if (N < 3 || (N >> 32)) return fail(h, QSIM_ERANGE, "modulus must be in [3, 2^32)");
+    if (x >= N || v >= N) return fail(h, QSIM_EINVAL, "x and v must be < N");
+    const Ranks R = ranks_of(h);
+    std::vector<std::vector<double>> parts(R.size(), std::vector<double>(1, 0.0));
+    for (size_t i = 0; i < R.size(); ++i) {
+        Handle *m = R[i];
+        m->queue.clear();   // the state is overwritten
+        for (int q = 0; q < m->n; ++q) m->pos[q] = m->n - 1 - q;
+        ensure_red(m, 1);
+        unsigned long long *d_cnt = reinterpret_cast<unsigned long long *>(m->d_red);
+        int rc = check_cuda(m, cudaMemsetAsync(d_cnt, 0, sizeof *d_cnt, m->stream), "shor count");
+        if (!rc) {
+            launch_shor_count(m, x, N, v, d_cnt);
+            rc = after_launch(m, "shor count");
+        }
+        unsigned long long c = 0;
+        if (!rc) rc = check_cuda(m, cudaMemcpyAsync(&c, d_cnt, sizeof c, cudaMemcpyDeviceToHost, m->stream), "shor count");
+        if (!rc) rc = check_cuda(m, cudaStreamSynchronize(m->stream), "shor count");
+        if (rc) return lift(h, R, rc);
+        parts[i][0] = (double)c;   // < 2^53: exact
+    }
+    double total = 0.0;
+    if (int rc = dist_sum_host(R, parts, &total, 1)) return lift(h, R, rc);
+    if (total == 0.0) return fail(h, QSIM_EINVAL, "no exponent a < 2^n with x^a = v (mod N)");
+    for (Handle *m : R) {
+        launch_shor_write(m, x, N, v, 1.0 / std::sqrt(total));
+        if (int rc = after_launch(m, "shor state")) return lift(h, R, rc);
+    }
+    return QSIM_OK;
+}
+
+// Steps 4-5 with the optional improvements for
+// the measured y; mem keeps the candidates of earlier iterations (LCM Check).
+// Order of the checks: DESIGN.md R27.
+static uint64_t shor_postprocess(uint64_t N, uint64_t x, uint64_t y, int nbits, bool improved,
+                                 std::vector<uint64_t> &mem)
+{
+    const uint64_t M = 1ull << nbits;
+    const int64_t shifts[5] = {0, 1, -1, 2, -2};   // Neighbor y Check
+    for (int s = 0; s < (improved ? 5 : 1); ++s) {
+        const int64_t yy = (int64_t)y + shifts[s];
+        if (yy <= 0 || (uint64_t)yy >= M) continue;
+        uint64_t cand[64];
+        const int nc = qsim_shor_candidates((uint64_t)yy, nbits, N, cand, 64);
+        for (int c = 0; c < nc; ++c) {
+            const uint64_t r = cand[c];
+            if (uint64_t f = qsim_shor_try(N, x, r, 0)) return f;
+            if (!improved) continue;
+            if (uint64_t f = qsim_shor_try(N, x, r, 1)) return f;           // GCD Check
+            if (host_powmod_u(x, r, N) != 1)
+                for (uint64_t k = 2; k <= 8; ++k)                              // Small Factor Check
+                    if (uint64_t f = qsim_shor_try(N, x, k * r, 1)) return f;
+            for (const uint64_t r1 : mem)                                      // LCM Check
+                if (uint64_t f = qsim_shor_try(N, x, r1 / gcd64(r1, r) * r, 1)) return f;
+            if (mem.size() < 64) mem.push_back(r);
+        }
+    }
+    return 0;
+}
+
+int qsim_shor_run(qsim_t *h, uint64_t N, uint64_t seed, uint64_t run, int improved, int max_iter,
+                  uint64_t *factor, int *iters)
+{
+    QS_CHECK_HANDLE(h);
+    if (!factor || !iters || max_iter < 0) return QSIM_EINVAL;
+    *factor = 0;
+    *iters = 0;
+    if (N < 3 || (N >> 32)) return fail(h, QSIM_ERANGE, "modulus must be in [3, 2^32)");
+    const int n = h->n;
+    if (n > 62 || (unsigned __int128)N * N > ((unsigned __int128)1 << n))
+        return fail(h, QSIM_ERANGE, "exponent register needs 2^n >= N^2 (PAPER.md:841-843)");
+    std::vector<uint64_t> mem;
+    for (int t = 1; t <= max_iter; ++t) {
+        const u64x2 d = draw(seed, QSIM_TAG_SHOR, run, (uint32_t)(t - 1));
+        const uint64_t x = 1 + uint_below(d.a, N - 1);
+        const uint64_t g = gcd64(x, N);
+        if (g > 1 && g < N) {   // step 2
+            *factor = g;
+            *iters = t;
+            return QSIM_OK;
+        }
+        const uint64_t v = host_powmod_u(x, uint_below(d.b, 1ull << n), N);
+        if (int rc = qsim_shor_semantic_state(h, x, N, v)) return rc;
+        if (int rc = qsim_qft(h, 0, n, 0)) return rc;
+        const u64x2 dm = draw(seed, QSIM_TAG_MEASURE, run, (uint32_t)(t - 1));
+        uint64_t y = 0;
+        if (int rc = qsim_measure(h, u01(dm.a), &y)) return rc;
+        if (const uint64_t f = shor_postprocess(N, x, y, n, improved != 0, mem)) {
+            *factor = f;
+            *iters = t;
+            return QSIM_OK;
+        }
+    }
     return QSIM_OK;
 }
 

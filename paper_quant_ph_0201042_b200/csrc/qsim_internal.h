@@ -67,6 +67,9 @@ struct PermDesc {
 void launch_perm(Handle *h, const PermDesc &d);
 // Grover: iters fused iterations; d_trace receives |a_mark|^2 per iteration.
 void launch_grover(Handle *h, uint64_t mark_local, int mark_rank, int iters, double *d_trace);
+// Shor semantic-mode register (k_shor.cu): count / write {a : x^a = v mod N}
+void launch_shor_count(Handle *h, uint64_t x, uint64_t N, uint64_t v, unsigned long long *d_count);
+void launch_shor_write(Handle *h, uint64_t x, uint64_t N, uint64_t v, double amp);
 
 // Fused tile passes (k_tile.cu).  A pass reads every amplitude once and
 // writes it once: the shard is cut into tiles of 2^tbits amplitudes that

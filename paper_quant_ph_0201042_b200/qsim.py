@@ -105,6 +105,11 @@ _sig("qsim_probs", _i32, _H, _i32, _i32, _p)
 _sig("qsim_prob_index", _i32, _H, _u64, C.POINTER(_f64))
 _sig("qsim_measure", _i32, _H, _f64, C.POINTER(_u64))
 _sig("qsim_philox_draw", None, _u64, _u32, _u64, _u32, _p)
+_sig("qsim_shor_semantic_state", _i32, _H, _u64, _u64, _u64)
+_sig("qsim_shor_run", _i32, _H, _u64, _u64, _u64, _i32, _i32, C.POINTER(_u64), C.POINTER(_i32))
+_sig("qsim_shor_candidates", _i32, _u64, _i32, _u64, _p, _i32)
+_sig("qsim_shor_try", _u64, _u64, _u64, _u64, _i32)
+_sig("qsim_shor_prob_succ", _f64, _u64, _u64)
 _sig("qsim_get_stream", _p, _H)
 _sig("qsim_set_fusion", _i32, _H, _i32)
 _sig("qsim_profile", _i32, _H, _i32)
@@ -311,6 +316,33 @@ def qsim_measure(h, r: float) -> int:
 
 
 # ------------------------------------------------------------------ RNG + planners
+def qsim_shor_semantic_state(h, x: int, N: int, v: int) -> None:
+    _chk(h, lib.qsim_shor_semantic_state(h, x, N, v))
+
+
+def qsim_shor_run(h, N: int, seed: int, run: int, improved: bool = False, max_iter: int = 1000):
+    """One factoring run; returns (iterations, factor), (0, 0) if none."""
+    f, t = _u64(0), _i32(0)
+    _chk(h, lib.qsim_shor_run(h, N, seed, run, int(bool(improved)), max_iter, C.byref(f), C.byref(t)))
+    return t.value, f.value
+
+
+def qsim_shor_candidates(y: int, m: int, N: int, cap: int = 64):
+    out = np.zeros(cap, np.uint64)
+    k = lib.qsim_shor_candidates(y, m, N, out.ctypes.data, cap)
+    if k < 0:
+        raise QsimError(k, "qsim_shor_candidates: invalid argument")
+    return [int(v) for v in out[:k]]
+
+
+def qsim_shor_try(N: int, x: int, r: int, gcd_check: bool = False) -> int:
+    return int(lib.qsim_shor_try(N, x, r, int(bool(gcd_check))))
+
+
+def qsim_shor_prob_succ(N: int, phi: int) -> float:
+    return float(lib.qsim_shor_prob_succ(N, phi))
+
+
 def qsim_philox_draw(seed: int, tag: int, i: int, j: int):
     out = np.zeros(2, np.uint64)
     lib.qsim_philox_draw(seed, tag, i, j, out.ctypes.data)

@@ -1,0 +1,66 @@
+#!/usr/bin/env python3
+"""Reproduce Table 5 of the paper on one GPU.
+
+For every RSA-type n of the table: `runs` factoring runs (PAPER.md:928-933:
+"The experiment is executed 100 times and we use the average of these
+recorded iterations"), Original and Improved post-processing, in the
+semantic mode with a 2l = 30-qubit exponent register.
+Prints one JSON line per (n, mode) with the mean number of iterations, the
+paper's Theoretical / Original / Improved values, and the device time per
+quantum iteration (semantic register + QFT + measurement).
+
+Usage: python tools/shor_table5.py [runs] [seed]
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_quant_ph_0201042_b200 import qsim as Q  # noqa: E402
+
+# PAPER.md:956-962 (Table 5): n, p, q, Theoretical, Original, Improved
+TABLE5 = [(21311, 211, 101, 15.79, 6.690, 1.760), (21733, 211, 103, 15.85, 8.990, 2.356),
+          (22999, 211, 109, 16.00, 6.360, 1.730), (22523, 223, 101, 15.88, 5.480, 1.770),
+          (22927, 227, 101, 15.91, 3.790, 1.470), (22969, 223, 103, 15.94, 8.050, 2.070),
+          (23129, 229, 101, 15.92, 7.133, 1.636)]
+
+
+def main():
+    runs = int(sys.argv[1]) if len(sys.argv) > 1 else 100
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 2002
+    m = 30
+    h = Q.qsim_create(m)
+    Q.qsim_shor_run(h, 21311, 1, 0, False, 3)   # warm-up (allocations, tensor maps)
+    for n, p, q, th, orig, imp in TABLE5:
+        for improved in (False, True):
+            Q.qsim_profile(h, True)
+            t0 = time.perf_counter()
+            its = []
+            for run in range(runs):
+                t, f = Q.qsim_shor_run(h, n, seed, run, improved, 1000)
+                assert t >= 1 and f in (p, q), (n, run, t, f)
+                its.append(t)
+            wall = time.perf_counter() - t0
+            prof = Q.qsim_profile_json(h)
+            prof.pop("_launches", None)
+            Q.qsim_profile(h, False)
+            qiters = prof.get("k_shor_semantic_write", {}).get("launches", 0)
+            dev_ms = sum(v["ms"] for v in prof.values())
+            print(json.dumps({
+                "n": n, "mode": "improved" if improved else "original", "runs": runs, "seed": seed,
+                "mean_iterations": float(np.mean(its)), "std_error": float(np.std(its, ddof=1) / np.sqrt(runs)),
+                "paper": {"theoretical": th, "original": orig, "improved": imp},
+                "theoretical_exact": 1.0 / Q.qsim_shor_prob_succ(n, (p - 1) * (q - 1)),
+                "quantum_iterations": qiters, "wall_s": round(wall, 2),
+                "device_ms_per_quantum_iteration": round(dev_ms / max(qiters, 1), 3),
+                "kernels_ms": {k: round(v["ms"], 2) for k, v in prof.items()}}), flush=True)
+    Q.qsim_destroy(h)
+
+
+if __name__ == "__main__":
+    main()
