@@ -96,7 +96,7 @@ _sig("orc_shor_prob_succ", _f64, _u64, _u64)
 _sig("orc_shor_semantic_state", None, _p, _i32, _u64, _u64, _u64)
 _sig("orc_shor_candidates", _i32, _u64, _i32, _u64, _p, _i32)
 _sig("orc_shor_try", _u64, _u64, _u64, _u64, _i32)
-_sig("orc_shor_run", _i32, _u64, _i32, _u64, _u64, _i32, _i32, C.POINTER(_u64))
+_sig("orc_shor_run", _i32, _u64, _i32, _u64, _u64, _i32, _i32, C.POINTER(_u64), _p)
 
 
 def _ptr(a: np.ndarray) -> int:
@@ -347,8 +347,15 @@ def shor_try(N, x, r, gcd_check=False) -> int:
     return _lib.orc_shor_try(N, x, r, int(bool(gcd_check)))
 
 
-def shor_run(N, m, seed, run, improved=False, max_iter=200):
-    """One factoring run; returns (iterations, factor)."""
+SHOR_STATS = ("step2", "quantum", "basic_s", "basic_f", "neighbor_s", "neighbor_f", "gcd_s", "gcd_f",
+              "sf_s", "sf_f", "lcm_s", "lcm_f")
+
+
+def shor_run(N, m, seed, run, improved=False, max_iter=200, stats=None):
+    """One factoring run; returns (iterations, factor).  stats: optional
+    int64 array of len(SHOR_STATS), accumulated (Table 6 tallies)."""
     f = C.c_uint64(0)
-    t = _lib.orc_shor_run(N, m, seed, run, int(bool(improved)), max_iter, C.byref(f))
+    st = stats if stats is not None else np.zeros(len(SHOR_STATS), np.int64)
+    assert st.dtype == np.int64 and st.size == len(SHOR_STATS)
+    t = _lib.orc_shor_run(N, m, seed, run, int(bool(improved)), max_iter, C.byref(f), _ptr(st))
     return t, f.value

@@ -783,57 +783,101 @@ uint64_t orc_shor_try(uint64_t N, uint64_t x, uint64_t r, int gcd_check)
 
 static uint64_t lcm64(uint64_t a, uint64_t b) { return a / orc_gcd(a, b) * b; }
 
-/* One factoring run (PAPER.md:827-859 repeated until a factor is found):
- * iteration t draws (a, b) = draw(seed, TAG_SHOR, run, t-1): x = 1 + uint(a, N-1),
- * step 2 gcd; else the semantic order-finding register (2l = m qubits), the
- * QFT, measurement with r = u01(b),
- * then post-processing; improved = 1 adds the four checks of
- * PAPER.md:969-998 (neighbour y+-1, y+-2; GCD check; multiples 2r..8r;
- * lcm of remembered candidates).  Returns the iteration count (0: none
- * within max_iter); *factor receives the factor. */
-int orc_shor_run(uint64_t N, int m, uint64_t seed, uint64_t run, int improved, int max_iter, uint64_t *factor)
+/* Tallies of one or more runs (Table 6: "s/f where s
+ * means the number of success iterations and f ... failure iterations"). */
+enum { ST_STEP2 = 0, ST_QUANTUM, ST_BASIC_S, ST_BASIC_F, ST_NEIGH_S, ST_NEIGH_F, ST_GCD_S, ST_GCD_F,
+       ST_SF_S, ST_SF_F, ST_LCM_S, ST_LCM_F, ST_COUNT };
+
+/* The post-processing of one measured y (R27):
+ *   candidate r from the continued fraction of y/2^m (step 4); none and
+ *   improved: Neighbor y Check -- y+1, y-1, y+2, y-2, first with a candidate
+ *   (success = a candidate found);
+ *   basic test of step 5 on r;
+ *   improved, r even: GCD Check -- d+- even if x^r != 1;
+ *   improved, x^r != 1: Small Factor Check -- k r for k = 2..8 with the
+ *   basic test and the GCD check;
+ *   improved, earlier candidates r1: LCM Check -- lcm(r1, r) likewise;
+ *   r is remembered for later LCM checks. */
+static uint64_t shor_post(uint64_t N, int m, uint64_t x, uint64_t y, int improved,
+                          uint64_t *mem, int *nmem, int64_t *st)
+{
+    const uint64_t M = (uint64_t)1 << m;
+    uint64_t rs[64];
+    int nr = y ? orc_shor_candidates(y, m, N, rs, 64) : 0;
+    if (nr == 0) {
+        if (!improved) return 0;
+        const int64_t dy[4] = { 1, -1, 2, -2 };
+        for (int i = 0; i < 4 && nr == 0; ++i) {
+            const int64_t yy = (int64_t)y + dy[i];
+            if (yy > 0 && (uint64_t)yy < M) nr = orc_shor_candidates((uint64_t)yy, m, N, rs, 64);
+        }
+        st[nr ? ST_NEIGH_S : ST_NEIGH_F]++;
+        if (nr == 0) return 0;
+    }
+    const uint64_t r = rs[nr - 1];
+    uint64_t f = orc_shor_try(N, x, r, 0);
+    st[f ? ST_BASIC_S : ST_BASIC_F]++;
+    if (f || !improved) return f;
+    if (r % 2 == 0) {
+        f = orc_shor_try(N, x, r, 1);
+        st[f ? ST_GCD_S : ST_GCD_F]++;
+        if (f) return f;
+    }
+    if (orc_powmod(x, r, N) != 1 % N) {
+        for (uint64_t k = 2; k <= 8 && !f; ++k) {
+            f = orc_shor_try(N, x, k * r, 0);
+            if (!f) f = orc_shor_try(N, x, k * r, 1);
+        }
+        st[f ? ST_SF_S : ST_SF_F]++;
+        if (f) return f;
+    }
+    if (*nmem > 0) {
+        for (int j = 0; j < *nmem && !f; ++j) {
+            const uint64_t l = lcm64(mem[j], r);
+            f = orc_shor_try(N, x, l, 0);
+            if (!f) f = orc_shor_try(N, x, l, 1);
+        }
+        st[f ? ST_LCM_S : ST_LCM_F]++;
+        if (f) return f;
+    }
+    if (*nmem < 64) mem[(*nmem)++] = r;
+    return 0;
+}
+
+/* One factoring run (PAPER.md:827-859 repeated until a factor is found,
+ * PAPER.md:928-930): iteration t draws (a, b) = draw(seed, TAG_SHOR, run,
+ * t-1): x = 1 + uint(a, N-1) (step 1); step 2: 1 < gcd(x, N) < N ends the
+ * run; else the semantic order-finding register for the
+ * first-register outcome v = x^uint(b, 2^m) mod N, the QFT,
+ * measurement y with r = u01(draw(seed, TAG_MEASURE, run, t-1).a)
+ * (PAPER.md:397-404), then shor_post.  Returns the iteration count (0: none
+ * within max_iter); *factor receives the factor; st (ST_COUNT int64, may be
+ * NULL) accumulates the tallies. */
+int orc_shor_run(uint64_t N, int m, uint64_t seed, uint64_t run, int improved, int max_iter, uint64_t *factor,
+                 int64_t *stats)
 {
     const uint64_t M = (uint64_t)1 << m;
     cplx *psi = (cplx *)malloc(sizeof(cplx) * M);
     uint64_t mem[64];
     int nmem = 0;
+    int64_t local[ST_COUNT] = { 0 };
+    int64_t *st = stats ? stats : local;
     *factor = 0;
     for (int t = 1; t <= max_iter; ++t) {
         uint64_t d[2];
         orc_draw(seed, TAG_SHOR, run, (uint32_t)(t - 1), d);
         const uint64_t x = 1 + orc_uint(d[0], N - 1);
         const uint64_t g = orc_gcd(x, N);
-        if (g > 1 && g < N) { *factor = g; free(psi); return t; }
-        /* semantic register: v = x^a* for a uniform a* is the first-register outcome */
-        const uint64_t astar = orc_uint(d[1], M);
-        const uint64_t v = orc_powmod(x, astar, N);
+        if (g > 1 && g < N) { st[ST_STEP2]++; *factor = g; free(psi); return t; }
+        st[ST_QUANTUM]++;
+        const uint64_t v = orc_powmod(x, orc_uint(d[1], M), N);
         orc_shor_semantic_state(psi, m, x, N, v);
         orc_noise_t nz = { 0, 0.0, 0 };
         orc_qft(psi, m, 0, m, 0, &nz);
         uint64_t dm[2];
         orc_draw(seed, TAG_MEASURE, run, (uint32_t)(t - 1), dm);
         const uint64_t y = orc_measure(psi, m, orc_u01(dm[0]));
-        /* post-processing */
-        uint64_t f = 0;
-        const int nys = improved ? 5 : 1;
-        const int64_t dy[5] = { 0, 1, -1, 2, -2 };
-        for (int iy = 0; iy < nys && !f; ++iy) {
-            const int64_t yy = (int64_t)y + dy[iy];
-            if (yy <= 0 || (uint64_t)yy >= M) continue;
-            uint64_t rs[64];
-            const int nr = orc_shor_candidates((uint64_t)yy, m, N, rs, 64);
-            for (int i = 0; i < nr && !f; ++i) {
-                const uint64_t r = rs[i];
-                f = orc_shor_try(N, x, r, 0);
-                if (!f && improved) f = orc_shor_try(N, x, r, 1);
-                if (!f && improved && orc_powmod(x, r, N) != 1 % N)
-                    for (uint64_t k = 2; k <= 8 && !f; ++k) f = orc_shor_try(N, x, k * r, 1);
-                if (!f && improved) {
-                    for (int j = 0; j < nmem && !f; ++j) f = orc_shor_try(N, x, lcm64(mem[j], r), 1);
-                    if (nmem < 64) mem[nmem++] = r;
-                }
-            }
-        }
+        const uint64_t f = shor_post(N, m, x, y, improved, mem, &nmem, st);
         if (f) { *factor = f; free(psi); return t; }
     }
     free(psi);

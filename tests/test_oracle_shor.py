@@ -165,3 +165,29 @@ def test_run_iterations_statistics():
     assert all(t >= 1 for t in orig + imp)
     assert all(b <= a for a, b in zip(orig, imp))
     assert np.mean(orig) < 1 / O.shor_prob_succ(N, 120)
+
+
+@pytest.mark.parametrize("improved", [False, True])
+def test_run_tallies_are_consistent(improved):
+    """Table 6 bookkeeping: every run ends with exactly
+    one success; an iteration runs a check only after the earlier ones
+    failed; the iteration count is the number of quantum iterations plus
+    the step-2 ending."""
+    N, m, runs = 437, 18, 40
+    st = np.zeros(len(O.SHOR_STATS), np.int64)
+    total = 0
+    for r in range(runs):
+        t, f = O.shor_run(N, m, 5, r, improved, 200, st)
+        assert t >= 1 and N % f == 0
+        total += t
+    S = dict(zip(O.SHOR_STATS, st.tolist()))
+    assert S["quantum"] + S["step2"] == total
+    assert S["step2"] + S["basic_s"] + S["gcd_s"] + S["sf_s"] + S["lcm_s"] == runs
+    if improved:
+        assert S["quantum"] == S["basic_s"] + S["basic_f"] + S["neighbor_f"]
+        assert S["gcd_s"] + S["gcd_f"] <= S["basic_f"]
+        assert S["sf_s"] + S["sf_f"] <= S["basic_f"] - S["gcd_s"]
+        assert S["lcm_s"] + S["lcm_f"] <= S["basic_f"] - S["gcd_s"] - S["sf_s"]
+    else:
+        assert S["neighbor_s"] == S["neighbor_f"] == S["gcd_s"] == S["sf_s"] == S["lcm_s"] == 0
+        assert S["basic_s"] + S["basic_f"] <= S["quantum"]
