@@ -295,18 +295,33 @@ int qsim_measure(qsim_t *h, double r, uint64_t *idx);
  * (state then undefined). */
 int qsim_shor_semantic_state(qsim_t *h, uint64_t x, uint64_t N, uint64_t v);
 
+/* Tallies of qsim_shor_run (Table 6: s/f = iterations in
+ * which a check was performed and succeeded / failed). */
+enum {
+    QSIM_SHOR_STEP2 = 0,      /* runs ended by step 2 (1 < gcd(x, N) < N) */
+    QSIM_SHOR_QUANTUM = 1,    /* iterations that ran the order-finding register */
+    QSIM_SHOR_BASIC_S = 2, QSIM_SHOR_BASIC_F = 3,        /* step 5 on the candidate */
+    QSIM_SHOR_NEIGHBOR_S = 4, QSIM_SHOR_NEIGHBOR_F = 5,  /* 1 (Neighbor): a candidate found */
+    QSIM_SHOR_GCD_S = 6, QSIM_SHOR_GCD_F = 7,            /* 2 (GCD): a factor found */
+    QSIM_SHOR_SF_S = 8, QSIM_SHOR_SF_F = 9,              /* 3 (Small Factor) */
+    QSIM_SHOR_LCM_S = 10, QSIM_SHOR_LCM_F = 11,          /* 4 (LCM) */
+    QSIM_SHOR_NSTATS = 12
+};
+
 /* One factoring run: repeat the algorithm until a nontrivial factor of N is
- * found or max_iter iterations have run.  Iteration t (1-based) draws
- * (a, b) = draw(seed, QSIM_TAG_SHOR, run, t-1): x = 1 + uint(a, N-1); if
- * 1 < gcd(x, N) < N step 2 succeeds; otherwise v = x^(uint(b, 2^n)) mod N
- * (the outcome of measuring f(a) = x^a mod N), qsim_shor_semantic_state,
- * qsim_qft(0, n), and y = qsim_measure(u01(draw(seed, QSIM_TAG_MEASURE, run,
- * t-1).a)); then steps 4-5 on y.  improved = 1 adds the four checks of
- * PAPER.md:969-998 (R27).  *iters = t of the success, 0 if none
- * (then *factor = 0).  Overwrites the state.  QSIM_ERANGE unless
- * 3 <= N < 2^32 and N^2 <= 2^n (the precision of PAPER.md:841-843). */
+ * found or max_iter iterations have run.  Iteration t
+ * (1-based) draws (a, b) = draw(seed, QSIM_TAG_SHOR, run, t-1):
+ * x = 1 + uint(a, N-1); if 1 < gcd(x, N) < N step 2 succeeds; otherwise
+ * v = x^(uint(b, 2^n)) mod N (the outcome of measuring f(a) = x^a mod N),
+ * qsim_shor_semantic_state, qsim_qft(0, n), and y = qsim_measure(u01(
+ * draw(seed, QSIM_TAG_MEASURE, run, t-1).a)); then steps 4-5 on y.
+ * improved = 1 adds the four checks of PAPER.md:969-998 in the paper's order
+ * (R27).  *iters = t of the success, 0 if none (then *factor = 0).
+ * stats: NULL or a host array of QSIM_SHOR_NSTATS counters, incremented
+ * (not reset).  Overwrites the state.  QSIM_ERANGE unless 3 <= N < 2^32 and
+ * N^2 <= 2^n (the precision of PAPER.md:841-843). */
 int qsim_shor_run(qsim_t *h, uint64_t N, uint64_t seed, uint64_t run, int improved, int max_iter,
-                  uint64_t *factor, int *iters);
+                  uint64_t *factor, int *iters, int64_t *stats);
 
 /* Step 4's classical part: every convergent k/r of the
  * continued fraction of y / 2^m with 0 < k, 0 < r < N and

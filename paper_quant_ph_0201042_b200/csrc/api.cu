@@ -1492,38 +1492,59 @@ int qsim_shor_semantic_state(qsim_t *h, uint64_t x, uint64_t N, uint64_t v)
     return QSIM_OK;
 }
 
-// Steps 4-5 with the optional improvements for
-// the measured y; mem keeps the candidates of earlier iterations (LCM Check).
-// Order of the checks: DESIGN.md R27.
+// Post-processing of one measured y (PAPER.md:851-859 steps 4-5; with
+// `improved` the four checks of PAPER.md:969-998 in the paper's order, each
+// run only when the earlier ones did not finish the iteration -- DESIGN.md
+// R27).  mem keeps the candidates of earlier iterations for the LCM Check;
+// st accumulates the Table 6 tallies (QSIM_SHOR_*).
 static uint64_t shor_postprocess(uint64_t N, uint64_t x, uint64_t y, int nbits, bool improved,
-                                 std::vector<uint64_t> &mem)
+                                 std::vector<uint64_t> &mem, int64_t *st)
 {
     const uint64_t M = 1ull << nbits;
-    const int64_t shifts[5] = {0, 1, -1, 2, -2};   // Neighbor y Check
-    for (int s = 0; s < (improved ? 5 : 1); ++s) {
-        const int64_t yy = (int64_t)y + shifts[s];
-        if (yy <= 0 || (uint64_t)yy >= M) continue;
-        uint64_t cand[64];
-        const int nc = qsim_shor_candidates((uint64_t)yy, nbits, N, cand, 64);
-        for (int c = 0; c < nc; ++c) {
-            const uint64_t r = cand[c];
-            if (uint64_t f = qsim_shor_try(N, x, r, 0)) return f;
-            if (!improved) continue;
-            if (uint64_t f = qsim_shor_try(N, x, r, 1)) return f;           // GCD Check
-            if (host_powmod_u(x, r, N) != 1)
-                for (uint64_t k = 2; k <= 8; ++k)                              // Small Factor Check
-                    if (uint64_t f = qsim_shor_try(N, x, k * r, 1)) return f;
-            for (const uint64_t r1 : mem)                                      // LCM Check
-                if (uint64_t f = qsim_shor_try(N, x, r1 / gcd64(r1, r) * r, 1)) return f;
-            if (mem.size() < 64) mem.push_back(r);
+    uint64_t cand[64];
+    int nc = y ? qsim_shor_candidates(y, nbits, N, cand, 64) : 0;
+    if (nc == 0) {
+        if (!improved) return 0;
+        const int64_t shifts[4] = {1, -1, 2, -2};     // Neighbor y Check
+        for (int s = 0; s < 4 && nc == 0; ++s) {
+            const int64_t yy = (int64_t)y + shifts[s];
+            if (yy > 0 && (uint64_t)yy < M) nc = qsim_shor_candidates((uint64_t)yy, nbits, N, cand, 64);
         }
+        st[nc ? QSIM_SHOR_NEIGHBOR_S : QSIM_SHOR_NEIGHBOR_F]++;
+        if (nc == 0) return 0;
     }
+    const uint64_t r = cand[nc - 1];
+    uint64_t f = qsim_shor_try(N, x, r, 0);
+    st[f ? QSIM_SHOR_BASIC_S : QSIM_SHOR_BASIC_F]++;
+    if (f || !improved) return f;
+    auto both = [&](uint64_t rr) {
+        uint64_t d = qsim_shor_try(N, x, rr, 0);
+        return d ? d : qsim_shor_try(N, x, rr, 1);
+    };
+    if ((r & 1) == 0) {                                // GCD Check
+        f = qsim_shor_try(N, x, r, 1);
+        st[f ? QSIM_SHOR_GCD_S : QSIM_SHOR_GCD_F]++;
+        if (f) return f;
+    }
+    if (host_powmod_u(x, r, N) != 1) {                 // Small Factor Check
+        for (uint64_t k = 2; k <= 8 && !f; ++k) f = both(k * r);
+        st[f ? QSIM_SHOR_SF_S : QSIM_SHOR_SF_F]++;
+        if (f) return f;
+    }
+    if (!mem.empty()) {                                // LCM Check
+        for (size_t i = 0; i < mem.size() && !f; ++i) f = both(mem[i] / gcd64(mem[i], r) * r);
+        st[f ? QSIM_SHOR_LCM_S : QSIM_SHOR_LCM_F]++;
+        if (f) return f;
+    }
+    if (mem.size() < 64) mem.push_back(r);
     return 0;
 }
 
 int qsim_shor_run(qsim_t *h, uint64_t N, uint64_t seed, uint64_t run, int improved, int max_iter,
-                  uint64_t *factor, int *iters)
+                  uint64_t *factor, int *iters, int64_t *stats)
 {
+    int64_t local[QSIM_SHOR_NSTATS] = {0};
+    int64_t *st = stats ? stats : local;
     QS_CHECK_HANDLE(h);
     if (!factor || !iters || max_iter < 0) return QSIM_EINVAL;
     *factor = 0;
@@ -1538,17 +1559,19 @@ int qsim_shor_run(qsim_t *h, uint64_t N, uint64_t seed, uint64_t run, int improv
         const uint64_t x = 1 + uint_below(d.a, N - 1);
         const uint64_t g = gcd64(x, N);
         if (g > 1 && g < N) {   // step 2
+            st[QSIM_SHOR_STEP2]++;
             *factor = g;
             *iters = t;
             return QSIM_OK;
         }
+        st[QSIM_SHOR_QUANTUM]++;
         const uint64_t v = host_powmod_u(x, uint_below(d.b, 1ull << n), N);
         if (int rc = qsim_shor_semantic_state(h, x, N, v)) return rc;
         if (int rc = qsim_qft(h, 0, n, 0)) return rc;
         const u64x2 dm = draw(seed, QSIM_TAG_MEASURE, run, (uint32_t)(t - 1));
         uint64_t y = 0;
         if (int rc = qsim_measure(h, u01(dm.a), &y)) return rc;
-        if (const uint64_t f = shor_postprocess(N, x, y, n, improved != 0, mem)) {
+        if (const uint64_t f = shor_postprocess(N, x, y, n, improved != 0, mem, st)) {
             *factor = f;
             *iters = t;
             return QSIM_OK;

@@ -29,7 +29,7 @@ QSIM_ECUDA, QSIM_ENOTBIJ, QSIM_ESTATE, QSIM_ENCCL, QSIM_ENODEV = -4, -5, -6, -7,
 QSIM_GATE_RP, QSIM_GATE_P1, QSIM_GATE_HAAR = 0, 1, 2
 QSIM_PERM_TABLE, QSIM_PERM_MODMUL, QSIM_PERM_MODEXP = 0, 1, 2
 QSIM_TAG_GATE, QSIM_TAG_HAAR, QSIM_TAG_PAIR, QSIM_TAG_OPNOISE = 1, 2, 3, 4
-QSIM_TAG_MARK, QSIM_TAG_BASE, QSIM_TAG_GAUSS, QSIM_TAG_PAULI, QSIM_TAG_MEASURE = 5, 6, 7, 8, 9
+QSIM_TAG_MARK, QSIM_TAG_BASE, QSIM_TAG_GAUSS, QSIM_TAG_PAULI, QSIM_TAG_MEASURE, QSIM_TAG_SHOR = 5, 6, 7, 8, 9, 10
 
 _ERRNAMES = {
     -1: "QSIM_EINVAL", -2: "QSIM_ERANGE", -3: "QSIM_ENOMEM", -4: "QSIM_ECUDA",
@@ -106,7 +106,7 @@ _sig("qsim_prob_index", _i32, _H, _u64, C.POINTER(_f64))
 _sig("qsim_measure", _i32, _H, _f64, C.POINTER(_u64))
 _sig("qsim_philox_draw", None, _u64, _u32, _u64, _u32, _p)
 _sig("qsim_shor_semantic_state", _i32, _H, _u64, _u64, _u64)
-_sig("qsim_shor_run", _i32, _H, _u64, _u64, _u64, _i32, _i32, C.POINTER(_u64), C.POINTER(_i32))
+_sig("qsim_shor_run", _i32, _H, _u64, _u64, _u64, _i32, _i32, C.POINTER(_u64), C.POINTER(_i32), _p)
 _sig("qsim_shor_candidates", _i32, _u64, _i32, _u64, _p, _i32)
 _sig("qsim_shor_try", _u64, _u64, _u64, _u64, _i32)
 _sig("qsim_shor_prob_succ", _f64, _u64, _u64)
@@ -320,10 +320,19 @@ def qsim_shor_semantic_state(h, x: int, N: int, v: int) -> None:
     _chk(h, lib.qsim_shor_semantic_state(h, x, N, v))
 
 
-def qsim_shor_run(h, N: int, seed: int, run: int, improved: bool = False, max_iter: int = 1000):
-    """One factoring run; returns (iterations, factor), (0, 0) if none."""
+SHOR_STATS = ("step2", "quantum", "basic_s", "basic_f", "neighbor_s", "neighbor_f", "gcd_s", "gcd_f",
+              "sf_s", "sf_f", "lcm_s", "lcm_f")   # QSIM_SHOR_* order
+
+
+def qsim_shor_run(h, N: int, seed: int, run: int, improved: bool = False, max_iter: int = 1000, stats=None):
+    """One factoring run; returns (iterations, factor), (0, 0) if none.
+    stats: optional int64 numpy array of len(SHOR_STATS), accumulated."""
     f, t = _u64(0), _i32(0)
-    _chk(h, lib.qsim_shor_run(h, N, seed, run, int(bool(improved)), max_iter, C.byref(f), C.byref(t)))
+    ptr = None
+    if stats is not None:
+        assert stats.dtype == np.int64 and stats.size == len(SHOR_STATS) and stats.flags.c_contiguous
+        ptr = stats.ctypes.data
+    _chk(h, lib.qsim_shor_run(h, N, seed, run, int(bool(improved)), max_iter, C.byref(f), C.byref(t), ptr))
     return t.value, f.value
 
 

@@ -80,12 +80,16 @@ def test_run_parity(reg, N, m, improved):
     """Same draws, same register, same measurement: iterations and factors
     agree with the oracle run for run."""
     h = reg(m)
+    sg = np.zeros(len(Q.SHOR_STATS), np.int64)
+    so = np.zeros(len(O.SHOR_STATS), np.int64)
     for run in range(8):
-        got = Q.qsim_shor_run(h, N, 11, run, improved, 200)
-        ref = O.shor_run(N, m, 11, run, improved, 200)
+        got = Q.qsim_shor_run(h, N, 11, run, improved, 200, sg)
+        ref = O.shor_run(N, m, 11, run, improved, 200, so)
         assert got == ref, (run, got, ref)
         t, f = got
         assert t >= 1 and 1 < f < N and N % f == 0
+    assert Q.SHOR_STATS == O.SHOR_STATS
+    assert np.array_equal(sg, so)
 
 
 def test_full_size_register_sampled(reg):

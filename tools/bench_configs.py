@@ -32,6 +32,7 @@ def timed(h, fn, reps=1):
     out = None
     for _ in range(reps):
         out = fn()
+    Q.qsim_sync(h)   # flush queued (fused) gates inside the timed region
     e1.record(stream)
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) / reps

@@ -6,8 +6,9 @@ For every RSA-type n of the table: `runs` factoring runs (PAPER.md:928-933:
 recorded iterations"), Original and Improved post-processing, in the
 semantic mode with a 2l = 30-qubit exponent register.
 Prints one JSON line per (n, mode) with the mean number of iterations, the
-paper's Theoretical / Original / Improved values, and the device time per
-quantum iteration (semantic register + QFT + measurement).
+paper's Theoretical / Original / Improved values, the per-check tallies of
+Table 6 and the device time per quantum iteration
+(semantic register + QFT + measurement).
 
 Usage: python tools/shor_table5.py [runs] [seed]
 """
@@ -41,8 +42,9 @@ def main():
             Q.qsim_profile(h, True)
             t0 = time.perf_counter()
             its = []
+            st = np.zeros(len(Q.SHOR_STATS), np.int64)
             for run in range(runs):
-                t, f = Q.qsim_shor_run(h, n, seed, run, improved, 1000)
+                t, f = Q.qsim_shor_run(h, n, seed, run, improved, 1000, st)
                 assert t >= 1 and f in (p, q), (n, run, t, f)
                 its.append(t)
             wall = time.perf_counter() - t0
@@ -57,6 +59,7 @@ def main():
                 "paper": {"theoretical": th, "original": orig, "improved": imp},
                 "theoretical_exact": 1.0 / Q.qsim_shor_prob_succ(n, (p - 1) * (q - 1)),
                 "quantum_iterations": qiters, "wall_s": round(wall, 2),
+                "tallies": dict(zip(Q.SHOR_STATS, st.tolist())),
                 "device_ms_per_quantum_iteration": round(dev_ms / max(qiters, 1), 3),
                 "kernels_ms": {k: round(v["ms"], 2) for k, v in prof.items()}}), flush=True)
     Q.qsim_destroy(h)
