@@ -442,187 +442,6 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse)
 
 }  // namespace
 
-// ---------------------------------------------------------------- gate queue
-// Pack the queued gates into fused passes (k_ops.cu) and run them.
-//
-// Greedy, order-preserving up to commutation of gates on disjoint qubits:
-// a pass collects, in queue order, every gate whose non-diagonal target is
-// (or can still become) one of its <= amax "active" positions; a gate that
-// cannot join blocks all of its positions for the rest of the scan, so no
-// later gate on those positions overtakes it.  The tile = active positions +
-// the lowest other positions (passive, for contiguous runs), <= 12 bits.
-int qs::flush_queue(Handle *h)
-{
-    if (h->queue.empty()) return QSIM_OK;
-    std::vector<QOp> rem;
-    rem.swap(h->queue);
-    const int nl = h->nl;
-    const int tbits = std::min(kTileMaxBits, nl);
-    const int amax = nl <= kTileMaxBits ? nl : kTileMaxBits - 3;
-    std::vector<GOp> hops;
-    while (!rem.empty()) {
-        std::vector<int> act;                 // active positions (tile bits 0..)
-        std::vector<char> is_act(nl, 0), blocked(nl, 0);
-        std::vector<QOp> take, left;
-        for (const QOp &op : rem) {
-            uint64_t touch = op.cmask;
-            if (op.tpos >= 0) touch |= 1ull << op.tpos;
-            bool blk = false;
-            for (int p = 0; p < nl; ++p)
-                if (((touch >> p) & 1) && blocked[p]) blk = true;
-            bool ok = !blk;
-            if (ok && !op.diag && !is_act[op.tpos]) {
-                if ((int)act.size() < amax) { act.push_back(op.tpos); is_act[op.tpos] = 1; }
-                else ok = false;
-            }
-            if (ok) take.push_back(op);
-            else {
-                left.push_back(op);
-                for (int p = 0; p < nl; ++p)
-                    if ((touch >> p) & 1) blocked[p] = 1;
-            }
-        }
-        rem.swap(left);
-        // tile: active + passive lowest positions
-        std::vector<int> tile(act);
-        std::vector<int> tbit_of(nl, -1);
-        for (size_t b = 0; b < act.size(); ++b) tbit_of[act[b]] = (int)b;
-        for (int p = 0; p < nl && (int)tile.size() < tbits; ++p)
-            if (tbit_of[p] < 0) { tbit_of[p] = (int)tile.size(); tile.push_back(p); }
-        OpsPass P;
-        std::memset(&P, 0, sizeof P);
-        P.tbits = tbits;
-        for (int b = 0; b < tbits; ++b) P.in_pos[b] = tile[b];
-        std::vector<int> fix_of(nl, -1);
-        for (int p = 0; p < nl; ++p)
-            if (tbit_of[p] < 0) { fix_of[p] = P.nfix; P.fin_pos[P.nfix++] = p; }
-        // segments: a register window of 4 tile bits covering the next dense targets
-        std::vector<std::vector<int>> wins;
-        std::vector<int> seg_of(take.size());
-        {
-            std::vector<int> cur;
-            for (size_t i = 0; i < take.size(); ++i) {
-                if (!take[i].diag) {
-                    const int t = tbit_of[take[i].tpos];
-                    if (std::find(cur.begin(), cur.end(), t) == cur.end()) {
-                        if (!wins.empty() || !cur.empty()) {}
-                        // new window: this target + the next distinct dense targets
-                        cur.clear();
-                        cur.push_back(t);
-                        for (size_t j = i + 1; j < take.size() && (int)cur.size() < kRegBits; ++j) {
-                            if (take[j].diag) continue;
-                            const int t2 = tbit_of[take[j].tpos];
-                            if (std::find(cur.begin(), cur.end(), t2) == cur.end()) cur.push_back(t2);
-                        }
-                        for (int b = 0; b < tbits && (int)cur.size() < kRegBits; ++b)
-                            if (std::find(cur.begin(), cur.end(), b) == cur.end() && tile[b] >= kRegBits) cur.push_back(b);
-                        for (int b = 0; b < tbits && (int)cur.size() < kRegBits; ++b)
-                            if (std::find(cur.begin(), cur.end(), b) == cur.end()) cur.push_back(b);
-                        std::sort(cur.begin(), cur.end());
-                        wins.push_back(cur);
-                    }
-                }
-                if (wins.empty()) {
-                    std::vector<int> w;
-                    for (int b = tbits - kRegBits; b < tbits; ++b) w.push_back(b);
-                    wins.push_back(w);
-                }
-                seg_of[i] = (int)wins.size() - 1;
-            }
-            if (wins.empty()) {
-                std::vector<int> w;
-                for (int b = tbits - kRegBits; b < tbits; ++b) w.push_back(b);
-                wins.push_back(w);
-            }
-        }
-        // split into chunks of <= kMaxSegs segments (each chunk = one launch)
-        size_t op0 = 0;
-        for (size_t s0 = 0; s0 < wins.size(); s0 += kMaxSegs) {
-            const size_t s1 = std::min(wins.size(), s0 + kMaxSegs);
-            P.nseg = (int)(s1 - s0);
-            hops.clear();
-            size_t i = op0;
-            for (size_t s = s0; s < s1; ++s) {
-                OpsSeg &sg = P.seg[s - s0];
-                for (int b = 0; b < kRegBits; ++b) sg.map.win[b] = wins[s][b];
-                // thread order: ascending tile bits, first/last segment by position
-                std::vector<int> rest;
-                for (int b = 0; b < tbits; ++b)
-                    if (std::find(wins[s].begin(), wins[s].end(), b) == wins[s].end()) rest.push_back(b);
-                if (s == s0 || s + 1 == s1)
-                    std::stable_sort(rest.begin(), rest.end(), [&](int x, int y) { return tile[x] < tile[y]; });
-                for (size_t t = 0; t < rest.size(); ++t) sg.map.order[t] = rest[t];
-                sg.op_begin = (int)hops.size();
-                for (; i < take.size() && seg_of[i] == (int)s; ++i) {
-                    const QOp &q = take[i];
-                    GOp g;
-                    std::memset(&g, 0, sizeof g);
-                    for (int k = 0; k < 4; ++k) g.u[k] = q.u[k];
-                    auto win_idx = [&](int t) {
-                        for (int b = 0; b < kRegBits; ++b)
-                            if (wins[s][b] == t) return b;
-                        return -1;
-                    };
-                    if (!q.diag) {
-                        g.kind = GOP_DENSE;
-                        g.rb = (uint8_t)win_idx(tbit_of[q.tpos]);
-                    } else if (q.tpos < 0) {
-                        g.kind = GOP_PHASE;
-                    } else if (tbit_of[q.tpos] >= 0) {
-                        const int w = win_idx(tbit_of[q.tpos]);
-                        if (w >= 0) { g.kind = GOP_DIAGW; g.rb = (uint8_t)w; }
-                        else { g.kind = GOP_DIAGT; g.tb = 1u << tbit_of[q.tpos]; }
-                    } else {
-                        g.kind = GOP_DIAGF;
-                        g.fbit = (uint32_t)fix_of[q.tpos];
-                    }
-                    for (int p = 0; p < nl; ++p) {
-                        if (!((q.cmask >> p) & 1)) continue;
-                        const uint64_t want = (q.cval >> p) & 1;
-                        if (tbit_of[p] >= 0) {
-                            const int w = win_idx(tbit_of[p]);
-                            if (w >= 0) {
-                                g.wm |= (uint8_t)(1u << w);
-                                g.wv |= (uint8_t)(want << w);
-                            } else {
-                                g.tm |= 1u << tbit_of[p];
-                                g.tv |= (uint32_t)want << tbit_of[p];
-                            }
-                        } else {
-                            g.fm |= 1ull << fix_of[p];
-                            g.fv |= want << fix_of[p];
-                        }
-                    }
-                    hops.push_back(g);
-                }
-                sg.op_end = (int)hops.size();
-            }
-            op0 = i;
-            P.nops = (int)hops.size();
-            if (hops.size() > h->d_ops_cap) {
-                if (h->d_ops) {
-                    cudaStreamSynchronize(h->stream);
-                    cudaFree(h->d_ops);
-                }
-                h->d_ops_cap = std::max<size_t>(hops.size(), 4096);
-                if (cudaMalloc(&h->d_ops, h->d_ops_cap * sizeof(GOp)) != cudaSuccess) {
-                    cudaGetLastError();
-                    h->d_ops = nullptr;
-                    h->d_ops_cap = 0;
-                    h->poisoned = 1;
-                    return fail(h, QSIM_ENOMEM, "gate-list buffer");
-                }
-            }
-            // the op list is copied on the stream; the host vector lives until
-            // the copy has been enqueued and is synchronous for pageable memory
-            cudaMemcpyAsync(h->d_ops, hops.data(), hops.size() * sizeof(GOp), cudaMemcpyHostToDevice, h->stream);
-            launch_ops_pass(h, P, h->d_ops);
-            if (int rc = after_launch(h, "fused gate pass")) return rc;
-        }
-    }
-    return QSIM_OK;
-}
-
 // Local bit permutation pass: new position of old local position p is perm[p].
 void qs::permute_local(Handle *h, const std::vector<int> &perm)
 {
@@ -843,7 +662,6 @@ void qsim_destroy(qsim_t *h)
     if (h->scratch) cudaFree(h->scratch);
     if (h->d_red) cudaFree(h->d_red);
     if (h->h_red) cudaFreeHost(h->h_red);
-    if (h->d_ops) cudaFree(h->d_ops);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;

@@ -21,16 +21,13 @@ namespace {
 
 using namespace tile;
 
-__global__ void __launch_bounds__(256, 1) k_ops_pass(const __grid_constant__ OpsPass P, const GOp *__restrict__ ops,
-                                                     const double2 *in, double2 *out, uint64_t ntiles)
+__global__ void __launch_bounds__(256, 1) k_ops_pass(const __grid_constant__ OpsLaunch L, const double2 *in,
+                                                     double2 *out, uint64_t ntiles)
 {
     extern __shared__ double2 tile_buf[];
+    const OpsPass &P = L.P;
     const uint32_t tid = threadIdx.x;
     const int tb = P.tbits - kRegBits;
-    __shared__ GOp sops[kOpsSmem];
-    const int nsm = P.nops < kOpsSmem ? P.nops : kOpsSmem;
-    for (int i = tid; i < nsm; i += blockDim.x) sops[i] = ops[i];
-    __syncthreads();
 
     const TileMap &m0 = P.seg[0].map;
     const TileMap &mL = P.seg[P.nseg - 1].map;
@@ -92,7 +89,7 @@ __global__ void __launch_bounds__(256, 1) k_ops_pass(const __grid_constant__ Ops
 #pragma unroll
                 for (int k = 0; k < NS; ++k) v[k] = tile_buf[o[k]];
             }
-            run_ops(v, P.nops <= kOpsSmem ? sops : ops, sg.op_begin, sg.op_end, T, tpart);
+            run_ops(v, L.ops, sg.op_begin, sg.op_end, T, tpart);
             prev_tpart = tpart;
             prev_stp = stp;
 #pragma unroll
@@ -118,9 +115,10 @@ __global__ void __launch_bounds__(256, 1) k_ops_pass(const __grid_constant__ Ops
 
 }  // namespace
 
-void launch_ops_pass(Handle *h, const OpsPass &P, const GOp *d_ops)
+void launch_ops_pass(Handle *h, const OpsLaunch &L)
 {
-    if (launch_ops_pass_tma(h, P, d_ops)) return;
+    if (launch_ops_pass_tma(h, L)) return;
+    const OpsPass &P = L.P;
     const size_t smem = (sizeof(double2) << P.tbits);
     static bool attr = false;
     if (!attr) {
@@ -136,7 +134,7 @@ void launch_ops_pass(Handle *h, const OpsPass &P, const GOp *d_ops)
     const uint64_t cap = (uint64_t)h->num_sms * per_sm;
     const unsigned grid = (unsigned)(ntiles < cap ? ntiles : cap);
     prof_begin(h);
-    k_ops_pass<<<grid, threads, smem, h->stream>>>(P, d_ops, h->psi, h->psi, ntiles);
+    k_ops_pass<<<grid, threads, smem, h->stream>>>(L, h->psi, h->psi, ntiles);
     prof_end(h, "k_ops_pass", (1ull << (P.tbits + P.nfix)) * 32);
 }
 

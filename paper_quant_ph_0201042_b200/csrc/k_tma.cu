@@ -417,19 +417,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 // smem transposes) is k_ops.cu's; only the data movement differs.
 __global__ void __launch_bounds__(kThreads, 1)
     k_ops_tma(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
-              const __grid_constant__ OpsPass P, const __grid_constant__ TmaArgs ta, const GOp *__restrict__ ops,
-              uint64_t ntiles, int ops_in_smem)
+              const __grid_constant__ OpsLaunch L, const __grid_constant__ TmaArgs ta, uint64_t ntiles)
 {
     static_assert(kTmaTileBits == 12, "tile");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     double2 *bufs = reinterpret_cast<double2 *>(smem_raw);
     uint64_t *full = reinterpret_cast<uint64_t *>(bufs + kStages * (1u << kTmaTileBits));
-    GOp *sops = reinterpret_cast<GOp *>(full + 8);          // the whole op list, if it fits
+    const OpsPass &P = L.P;
     const uint32_t tid = threadIdx.x;
-    const bool in_smem = ops_in_smem;
-    if (in_smem)
-        for (int i = tid; i < P.nops; i += blockDim.x) sops[i] = ops[i];
-    const GOp *opl = in_smem ? sops : ops;
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -507,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int k = 0; k < NS; ++k) v[k] = buf[o[k]];
             }
-            run_ops(v, opl, sg.op_begin, sg.op_end, T, tpart);
+            run_ops(v, L.ops, sg.op_begin, sg.op_end, T, tpart);
             prev_stp = stp;
 #pragma unroll
             for (int b = 0; b < kRegBits; ++b) prev_wsw[b] = wsw[b];
@@ -712,8 +707,9 @@ bool launch_tile_pass_tma(Handle *h, const TilePass &tp_in, const double2 *in, d
     return true;
 }
 
-bool launch_ops_pass_tma(Handle *h, const OpsPass &P, const GOp *d_ops)
+bool launch_ops_pass_tma(Handle *h, const OpsLaunch &L)
 {
+    const OpsPass &P = L.P;
     if (P.tbits != kTmaTileBits || getenv("QSIM_NO_TMA")) return false;
     std::vector<int> fid(h->nl, -1);
     for (int f = 0; f < P.nfix; ++f) fid[P.fin_pos[f]] = f;
@@ -726,20 +722,16 @@ bool launch_ops_pass_tma(Handle *h, const OpsPass &P, const GOp *d_ops)
     std::memcpy(ta.out_first, ta.in_first, sizeof ta.in_first);
     std::memcpy(ta.out_len, ta.in_len, sizeof ta.in_len);
     std::memcpy(ta.out_rank, ta.in_rank, sizeof ta.in_rank);
-    const size_t base = (size_t)kStages * kTileBytes + 8 * sizeof(uint64_t);
-    const size_t with_ops = base + (size_t)P.nops * sizeof(GOp);
-    const size_t limit = 227 * 1024;
-    const int in_smem = with_ops <= limit;
-    const size_t smem = in_smem ? with_ops : base;
+    const size_t smem = (size_t)kStages * kTileBytes + 8 * sizeof(uint64_t);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_ops_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit);
+        cudaFuncSetAttribute(k_ops_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
     const uint64_t ntiles = 1ull << P.nfix;
     const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)h->num_sms);
     prof_begin(h);
-    k_ops_tma<<<grid, kThreads, smem, h->stream>>>(im, om, P, ta, d_ops, ntiles, in_smem);
+    k_ops_tma<<<grid, kThreads, smem, h->stream>>>(im, om, L, ta, ntiles);
     prof_end(h, "k_ops_tma", (1ull << (P.tbits + P.nfix)) * 32);
     return true;
 }

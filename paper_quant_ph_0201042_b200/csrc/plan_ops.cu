@@ -1,0 +1,489 @@
+// plan_ops.cu -- the gate queue's planner: queued gates -> fused tile passes
+// (k_ops.cu / k_tma.cu k_ops_tma).
+//
+// Each pass reads and writes every amplitude once (one HBM sweep, the cost
+// the paper pays per gate) and applies a whole run of
+// gates in between.  Three steps per flush:
+//
+//  1. Pass selection (greedy, order-preserving up to commutation): a pass
+//     collects, in queue order, every gate whose non-diagonal target is (or
+//     can still become) one of its <= amax "active" positions; a gate that
+//     cannot join blocks all of its positions for the rest of the scan.
+//  2. Segment scheduling inside a pass.  A thread holds 16 amplitudes = a
+//     4-bit register "window" of the tile; changing the window costs a
+//     shared-memory transpose of the whole tile (as much time as ~2 dense
+//     gates), so the planner orders the pass's gates -- any topological
+//     order of their commutation DAG is the same operator -- to apply as
+//     many gates per window as possible: for each candidate window (4-subsets
+//     of the next dense targets) it simulates the closure of gates that
+//     become applicable and keeps the best.
+//  3. Merging: gates on one target that are adjacent in that order (up to
+//     commutation) and are uncontrolled or controlled by the same window
+//     qubit are multiplied into one 2x2 (or a pair of 2x2 selected by the
+//     control, DENSE2): e.g. a Haar gate followed by a noisy CNOT on the same
+//     target costs one register update instead of two.
+//
+// Two gates commute when every position they share is acted on diagonally
+// by both (controls are diagonal projectors): exact, no numerical test.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <queue>
+#include <string>
+#include <vector>
+
+#include "qsim_internal.h"
+
+namespace qs {
+
+namespace {
+
+// A gate of one pass in pass-local form.
+struct POp {
+    int dense;              // non-diagonal on tpos
+    int tpos;               // target local position; -1: constant phase u[3]
+    uint64_t cmask, cval;   // controls (local positions)
+    int cs;                 // choice form: position selecting m1 (m0 where it is 0); -1: none
+    double2 m0[4], m1[4];   // m1 == m0 when cs < 0
+    uint64_t nmask, dmask;  // positions acted on non-diagonally / diagonally
+    bool dead;
+};
+
+inline bool conflict(const POp &a, const POp &b)
+{
+    return (a.nmask & (b.nmask | b.dmask)) || (b.nmask & (a.nmask | a.dmask));
+}
+
+inline bool eq(double2 a, double re, double im) { return a.x == re && a.y == im; }
+inline bool is_ident(const double2 m[4]) { return eq(m[0], 1, 0) && eq(m[1], 0, 0) && eq(m[2], 0, 0) && eq(m[3], 1, 0); }
+inline bool is_diagm(const double2 m[4]) { return eq(m[1], 0, 0) && eq(m[2], 0, 0); }
+
+// C = A B (row-major 2x2 complex)
+void mul2(const double2 A[4], const double2 B[4], double2 C[4])
+{
+    double2 r[4];
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j) {
+            const double2 a0 = A[2 * i], a1 = A[2 * i + 1], b0 = B[j], b1 = B[2 + j];
+            r[2 * i + j] = make_double2(a0.x * b0.x - a0.y * b0.y + a1.x * b1.x - a1.y * b1.y,
+                                        a0.x * b0.y + a0.y * b0.x + a1.x * b1.y + a1.y * b1.x);
+        }
+    std::memcpy(C, r, sizeof r);
+}
+
+void set_masks(POp &p)
+{
+    p.nmask = p.dense ? 1ull << p.tpos : 0;
+    p.dmask = p.cmask | (p.cs >= 0 ? 1ull << p.cs : 0) | (!p.dense && p.tpos >= 0 ? 1ull << p.tpos : 0);
+}
+
+POp from_queue(const QOp &q)
+{
+    POp p;
+    std::memset(&p, 0, sizeof p);
+    p.dense = !q.diag;
+    p.tpos = q.tpos;
+    p.cmask = q.cmask;
+    p.cval = q.cval;
+    p.cs = -1;
+    for (int k = 0; k < 4; ++k) p.m0[k] = p.m1[k] = q.u[k];
+    set_masks(p);
+    return p;
+}
+
+struct Segment {
+    int win[kRegBits];      // tile bits held in registers
+    std::vector<int> ops;   // op indices in application order
+};
+
+// Choice form (cs, m0, m1) of an op whose only control (if any) is one
+// window position; false if the op has other controls.
+bool choice_form(const POp &p, const std::vector<char> &in_win, int &cs, double2 m0[4], double2 m1[4])
+{
+    static const double2 I[4] = {{1, 0}, {0, 0}, {0, 0}, {1, 0}};
+    if (p.cs >= 0) {
+        if (p.cmask) return false;
+        cs = p.cs;
+        std::memcpy(m0, p.m0, 4 * sizeof(double2));
+        std::memcpy(m1, p.m1, 4 * sizeof(double2));
+        return true;
+    }
+    if (!p.cmask) {
+        cs = -1;
+        std::memcpy(m0, p.m0, 4 * sizeof(double2));
+        std::memcpy(m1, p.m0, 4 * sizeof(double2));
+        return true;
+    }
+    if (__builtin_popcountll(p.cmask) != 1) return false;
+    const int c = __builtin_ctzll(p.cmask);
+    if (!in_win[c]) return false;
+    cs = c;
+    const bool v = (p.cval >> c) & 1;
+    std::memcpy(v ? m1 : m0, p.m0, 4 * sizeof(double2));
+    std::memcpy(v ? m0 : m1, I, 4 * sizeof(double2));
+    return true;
+}
+
+// Merge B (applied after A, commuting with everything in between) into A.
+bool try_merge(POp &A, const POp &B, const std::vector<char> &in_win)
+{
+    if (A.tpos < 0 || A.tpos != B.tpos || !in_win[A.tpos]) return false;
+    int ca, cb;
+    double2 a0[4], a1[4], b0[4], b1[4];
+    if (!choice_form(A, in_win, ca, a0, a1) || !choice_form(B, in_win, cb, b0, b1)) return false;
+    if (ca >= 0 && cb >= 0 && ca != cb) return false;
+    if (!A.dense && !B.dense && (ca >= 0 || cb >= 0)) return false;   // keep cheap controlled phases
+    const int cs = ca >= 0 ? ca : cb;
+    double2 r0[4], r1[4];
+    mul2(b0, a0, r0);
+    mul2(b1, a1, r1);
+    A.cmask = A.cval = 0;
+    A.cs = cs;
+    std::memcpy(A.m0, r0, sizeof r0);
+    std::memcpy(A.m1, r1, sizeof r1);
+    A.dense = !(is_diagm(r0) && is_diagm(r1));
+    if (cs < 0 && !A.dense) A.cs = -1;
+    set_masks(A);
+    return true;
+}
+
+// Order the ops of one pass into register-window segments (see header).
+std::vector<Segment> schedule(const std::vector<POp> &ops, int nl, const std::vector<int> &tbit_of,
+                              const std::vector<int> &tile)
+{
+    const int n = (int)ops.size();
+    const int tbits = (int)tile.size();
+    std::vector<std::vector<int>> succ(n);
+    std::vector<int> npred(n, 0);
+    {
+        std::vector<int> lastN(nl, -1);
+        std::vector<std::vector<int>> sinceD(nl);
+        std::vector<int> pr;
+        for (int j = 0; j < n; ++j) {
+            pr.clear();
+            const uint64_t dn = ops[j].dmask & ~ops[j].nmask;
+            for (int p = 0; p < nl; ++p) {
+                if ((ops[j].nmask >> p) & 1) {
+                    if (lastN[p] >= 0) pr.push_back(lastN[p]);
+                    pr.insert(pr.end(), sinceD[p].begin(), sinceD[p].end());
+                } else if ((dn >> p) & 1) {
+                    if (lastN[p] >= 0) pr.push_back(lastN[p]);
+                }
+            }
+            std::sort(pr.begin(), pr.end());
+            pr.erase(std::unique(pr.begin(), pr.end()), pr.end());
+            for (int i : pr) {
+                succ[i].push_back(j);
+                ++npred[j];
+            }
+            for (int p = 0; p < nl; ++p) {
+                if ((ops[j].nmask >> p) & 1) {
+                    lastN[p] = j;
+                    sinceD[p].clear();
+                } else if ((dn >> p) & 1) {
+                    sinceD[p].push_back(j);
+                }
+            }
+        }
+    }
+    std::vector<int> cnt = npred;
+    std::vector<char> done(n, 0);
+    int ndone = 0;
+    std::vector<Segment> segs;
+    std::vector<int> prev;
+    for (int b = tbits - kRegBits; b < tbits; ++b) prev.push_back(b);
+
+    // closure of window W from the current state; commit = apply it
+    std::vector<int> c2;
+    std::vector<int> taken;
+    auto closure = [&](const std::vector<int> &W, bool commit) -> int {
+        uint32_t wmask = 0;
+        for (int b : W) wmask |= 1u << b;
+        c2 = cnt;
+        taken.clear();
+        std::priority_queue<int, std::vector<int>, std::greater<int>> pq;
+        for (int j = 0; j < n; ++j)
+            if (!done[j] && c2[j] == 0) pq.push(j);
+        int score = 0;
+        std::vector<int> skipped;
+        while (!pq.empty()) {
+            const int j = pq.top();
+            pq.pop();
+            const POp &o = ops[j];
+            if (o.dense && !((wmask >> tbit_of[o.tpos]) & 1)) continue;   // stays for a later window
+            taken.push_back(j);
+            if (o.dense) {
+                score += 4;
+                bool cw = true;
+                for (int p = 0; p < nl; ++p)
+                    if (((o.cmask >> p) & 1) && tbit_of[p] >= 0 && !((wmask >> tbit_of[p]) & 1)) cw = false;
+                score += cw;
+            }
+            for (int s : succ[j])
+                if (--c2[s] == 0) pq.push(s);
+        }
+        if (commit) {
+            for (int j : taken) {
+                done[j] = 1;
+                ++ndone;
+            }
+            cnt = c2;
+        }
+        return score;
+    };
+
+    while (ndone < n) {
+        std::vector<int> cand;
+        for (int j = 0; j < n && (int)cand.size() < 8; ++j) {
+            if (done[j] || !ops[j].dense) continue;
+            const int t = tbit_of[ops[j].tpos];
+            if (std::find(cand.begin(), cand.end(), t) == cand.end()) cand.push_back(t);
+        }
+        std::vector<int> best;
+        if ((int)cand.size() <= kRegBits) {
+            best = cand;
+            for (int b : prev)
+                if ((int)best.size() < kRegBits && std::find(best.begin(), best.end(), b) == best.end()) best.push_back(b);
+            // filler: highest tile positions first (low positions stay lane bits)
+            std::vector<int> byp(tbits);
+            for (int b = 0; b < tbits; ++b) byp[b] = b;
+            std::sort(byp.begin(), byp.end(), [&](int x, int y) { return tile[x] > tile[y]; });
+            for (int b : byp)
+                if ((int)best.size() < kRegBits && std::find(best.begin(), best.end(), b) == best.end()) best.push_back(b);
+        } else {
+            int bscore = -1;
+            const int m = (int)cand.size();
+            for (int a = 0; a < m; ++a)
+                for (int b = a + 1; b < m; ++b)
+                    for (int c = b + 1; c < m; ++c)
+                        for (int d = c + 1; d < m; ++d) {
+                            std::vector<int> W = {cand[a], cand[b], cand[c], cand[d]};
+                            const int s = closure(W, false);
+                            if (s > bscore) {
+                                bscore = s;
+                                best = W;
+                            }
+                        }
+        }
+        std::sort(best.begin(), best.end());
+        closure(best, true);
+        Segment sg;
+        for (int b = 0; b < kRegBits; ++b) sg.win[b] = best[b];
+        sg.ops = taken;
+        segs.push_back(sg);
+        prev = best;
+    }
+    return segs;
+}
+
+int launch_check(Handle *h, const char *what)
+{
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return check_cuda(h, e, what);
+    if (h->poisoned) return fail(h, QSIM_ECUDA, h->err);
+    return QSIM_OK;
+}
+
+}  // namespace
+
+int flush_queue(Handle *h)
+{
+    if (h->queue.empty()) return QSIM_OK;
+    std::vector<QOp> rem;
+    rem.swap(h->queue);
+    const int nl = h->nl;
+    const int tbits = std::min(kTileMaxBits, nl);
+    const int amax = nl <= kTileMaxBits ? nl : kTileMaxBits - 3;
+    constexpr size_t kPassCap = 512;   // bounds the planner's work per pass
+    static thread_local OpsLaunch L;   // 28 KiB, copied into the launch parameters
+    while (!rem.empty()) {
+        // ---- 1. pass selection
+        std::vector<int> act;
+        std::vector<char> is_act(nl, 0), blocked(nl, 0);
+        std::vector<QOp> take, left;
+        for (const QOp &op : rem) {
+            uint64_t touch = op.cmask;
+            if (op.tpos >= 0) touch |= 1ull << op.tpos;
+            bool ok = take.size() < kPassCap;
+            for (int p = 0; p < nl && ok; ++p)
+                if (((touch >> p) & 1) && blocked[p]) ok = false;
+            if (ok && !op.diag && !is_act[op.tpos]) {
+                if ((int)act.size() < amax) {
+                    act.push_back(op.tpos);
+                    is_act[op.tpos] = 1;
+                } else {
+                    ok = false;
+                }
+            }
+            if (ok) {
+                take.push_back(op);
+            } else {
+                left.push_back(op);
+                for (int p = 0; p < nl; ++p)
+                    if ((touch >> p) & 1) blocked[p] = 1;
+            }
+        }
+        rem.swap(left);
+        // tile: active + passive lowest positions
+        std::vector<int> tile(act);
+        std::vector<int> tbit_of(nl, -1);
+        for (size_t b = 0; b < act.size(); ++b) tbit_of[act[b]] = (int)b;
+        for (int p = 0; p < nl && (int)tile.size() < tbits; ++p)
+            if (tbit_of[p] < 0) {
+                tbit_of[p] = (int)tile.size();
+                tile.push_back(p);
+            }
+        OpsPass &P = L.P;
+        std::memset(&P, 0, sizeof P);
+        P.tbits = tbits;
+        for (int b = 0; b < tbits; ++b) P.in_pos[b] = tile[b];
+        std::vector<int> fix_of(nl, -1);
+        for (int p = 0; p < nl; ++p)
+            if (tbit_of[p] < 0) {
+                fix_of[p] = P.nfix;
+                P.fin_pos[P.nfix++] = p;
+            }
+
+        // ---- 2. segments, 3. merging
+        std::vector<POp> ops;
+        ops.reserve(take.size());
+        for (const QOp &q : take) ops.push_back(from_queue(q));
+        std::vector<Segment> segs = schedule(ops, nl, tbit_of, tile);
+        std::vector<std::vector<GOp>> enc(segs.size());
+        for (size_t s = 0; s < segs.size(); ++s) {
+            const Segment &sg = segs[s];
+            std::vector<char> in_win(nl, 0);
+            for (int b = 0; b < kRegBits; ++b) in_win[tile[sg.win[b]]] = 1;
+            const std::vector<int> &Ls = sg.ops;
+            for (size_t jj = 0; jj < Ls.size(); ++jj) {
+                POp &B = ops[Ls[jj]];
+                for (size_t ii = jj; ii-- > 0;) {
+                    POp &A = ops[Ls[ii]];
+                    if (A.dead) continue;
+                    if (A.tpos == B.tpos && try_merge(A, B, in_win)) {
+                        B.dead = true;
+                        break;
+                    }
+                    if (conflict(A, B)) break;
+                }
+            }
+            auto win_idx = [&](int pos) {
+                const int t = tbit_of[pos];
+                for (int b = 0; b < kRegBits; ++b)
+                    if (sg.win[b] == t) return b;
+                return -1;
+            };
+            for (int j : Ls) {
+                const POp &q = ops[j];
+                if (q.dead) continue;
+                GOp g;
+                std::memset(&g, 0, sizeof g);
+                for (int k = 0; k < 4; ++k) {
+                    g.u[k] = q.m0[k];
+                    g.u[4 + k] = q.m1[k];
+                }
+                if (q.cs >= 0) {
+                    // choice form (merged run): one 2x2 per value of the window bit cs
+                    g.rb = (uint8_t)win_idx(q.tpos);
+                    g.cs = (uint8_t)win_idx(q.cs);
+                    if (is_ident(q.m0)) {
+                        g.kind = GOP_CDENSE;
+                        g.cv = 1;
+                        for (int k = 0; k < 4; ++k) g.u[k] = q.m1[k];
+                    } else if (is_ident(q.m1)) {
+                        g.kind = GOP_CDENSE;
+                        g.cv = 0;
+                    } else {
+                        g.kind = GOP_DENSE2;
+                    }
+                    enc[s].push_back(g);
+                    continue;
+                }
+                if (q.dense) {
+                    g.kind = GOP_DENSE;
+                    g.rb = (uint8_t)win_idx(q.tpos);
+                } else if (q.tpos < 0) {
+                    g.kind = GOP_PHASE;
+                } else if (tbit_of[q.tpos] >= 0 && win_idx(q.tpos) >= 0) {
+                    g.kind = GOP_DIAGW;
+                    g.rb = (uint8_t)win_idx(q.tpos);
+                } else if (tbit_of[q.tpos] >= 0) {
+                    g.kind = GOP_DIAGT;
+                    g.tb = 1u << tbit_of[q.tpos];
+                } else {
+                    g.kind = GOP_DIAGF;
+                    g.fbit = (uint32_t)fix_of[q.tpos];
+                }
+                for (int p = 0; p < nl; ++p) {
+                    if (!((q.cmask >> p) & 1)) continue;
+                    const uint64_t want = (q.cval >> p) & 1;
+                    if (tbit_of[p] >= 0) {
+                        const int w = win_idx(p);
+                        if (w >= 0) {
+                            g.wm |= (uint8_t)(1u << w);
+                            g.wv |= (uint8_t)(want << w);
+                        } else {
+                            g.tm |= 1u << tbit_of[p];
+                            g.tv |= (uint32_t)want << tbit_of[p];
+                        }
+                    } else {
+                        g.fm |= 1ull << fix_of[p];
+                        g.fv |= want << fix_of[p];
+                    }
+                }
+                // a dense gate with exactly one control, on a window bit: static slot selection
+                if (g.kind == GOP_DENSE && g.tm == 0 && g.fm == 0 && __builtin_popcount(g.wm) == 1) {
+                    g.kind = GOP_CDENSE;
+                    g.cs = (uint8_t)__builtin_ctz(g.wm);
+                    g.cv = g.wv ? 1 : 0;
+                    g.wm = g.wv = 0;
+                }
+                enc[s].push_back(g);
+            }
+        }
+        // ---- launches: consecutive segments, <= kMaxSegs segments and <= kOpsParam ops each
+        struct Piece { int seg; size_t b, e; };
+        std::vector<Piece> pieces;
+        for (size_t s = 0; s < segs.size(); ++s) {
+            const size_t m = enc[s].size();
+            for (size_t b = 0; b < m || (b == 0 && m == 0); b += kOpsParam) {
+                pieces.push_back({(int)s, b, std::min(m, b + (size_t)kOpsParam)});
+                if (m == 0) break;
+            }
+        }
+        size_t pi = 0;
+        while (pi < pieces.size()) {
+            size_t pe = pi;
+            size_t nops = 0;
+            while (pe < pieces.size() && (int)(pe - pi) < kMaxSegs &&
+                   nops + (pieces[pe].e - pieces[pe].b) <= (size_t)kOpsParam) {
+                nops += pieces[pe].e - pieces[pe].b;
+                ++pe;
+            }
+            P.nseg = (int)(pe - pi);
+            P.nops = 0;
+            for (size_t k = pi; k < pe; ++k) {
+                const Segment &sg = segs[pieces[k].seg];
+                OpsSeg &os = P.seg[k - pi];
+                for (int b = 0; b < kRegBits; ++b) os.map.win[b] = sg.win[b];
+                std::vector<int> rest;
+                for (int b = 0; b < tbits; ++b)
+                    if (std::find(sg.win, sg.win + kRegBits, b) == sg.win + kRegBits) rest.push_back(b);
+                // first/last segment of a launch: thread bits by position (coalesced gather/scatter)
+                if (k == pi || k + 1 == pe)
+                    std::stable_sort(rest.begin(), rest.end(), [&](int x, int y) { return tile[x] < tile[y]; });
+                for (size_t t = 0; t < rest.size(); ++t) os.map.order[t] = rest[t];
+                os.op_begin = P.nops;
+                for (size_t i = pieces[k].b; i < pieces[k].e; ++i) L.ops[P.nops++] = enc[pieces[k].seg][i];
+                os.op_end = P.nops;
+            }
+            launch_ops_pass(h, L);
+            if (int rc = launch_check(h, "fused gate pass")) return rc;
+            pi = pe;
+        }
+    }
+    return QSIM_OK;
+}
+
+}  // namespace qs

@@ -127,18 +127,22 @@ bool launch_tile_pass_tma(Handle *h, const TilePass &tp, const double2 *in, doub
 //   DENSE   2x2 on window bit rb          DIAGW  diag(d0, d1) on window bit rb
 //   DIAGT   diag on a thread-part bit     DIAGF  diag on a fixed (tile-id) bit
 //   PHASE   constant phase u[3]
+//   CDENSE  2x2 on window bit rb where window bit cs == cv (one control)
+//   DENSE2  2x2 on window bit rb: u[0..3] where window bit cs = 0, u[4..7]
+//           where it is 1 (a run of gates on one target, each uncontrolled or
+//           controlled by the same qubit, multiplied together on the host)
 // Controls: wm/wv on the 4 window bits (slot index), tm/tv on the other tile
 // bits (thread part), fm/fv on fixed bits (tile id).
-enum { GOP_DENSE = 0, GOP_DIAGW = 1, GOP_DIAGT = 2, GOP_DIAGF = 3, GOP_PHASE = 4 };
+enum { GOP_DENSE = 0, GOP_DIAGW = 1, GOP_DIAGT = 2, GOP_DIAGF = 3, GOP_PHASE = 4, GOP_CDENSE = 5, GOP_DENSE2 = 6 };
 struct GOp {
     uint8_t kind, rb, wm, wv;
+    uint8_t cs, cv, pad_[2];
     uint32_t tm, tv;   // controls on non-window tile bits
     uint32_t tb;       // DIAGT: mask of the target tile bit
     uint32_t fbit;     // DIAGF: tile-id bit of the target
     uint64_t fm, fv;   // controls on fixed bits (tile-id mask / values)
-    double2 u[4];      // dense U (u11 u12 u21 u22) or diag(u[0], u[3])
+    double2 u[8];      // dense U (u11 u12 u21 u22) or diag(u[0], u[3]); DENSE2: two matrices
 };
-constexpr int kOpsSmem = 64;   // ops cached in static shared memory by k_ops_pass
 constexpr int kMaxSegs = 48;
 struct OpsSeg {
     TileMap map;       // register window + thread order
@@ -152,8 +156,17 @@ struct OpsPass {
     int nops, nseg;
     OpsSeg seg[kMaxSegs];
 };
-void launch_ops_pass(Handle *h, const OpsPass &P, const GOp *d_ops);
-bool launch_ops_pass_tma(Handle *h, const OpsPass &P, const GOp *d_ops);   // k_tma.cu
+// One launch: the pass geometry and its op list travel as one __grid_constant__
+// kernel parameter (<= 32 KiB), so every op read is a uniform constant-bank load
+// (no shared-memory traffic, no per-handle device buffer).
+constexpr int kOpsParam = 140;
+struct OpsLaunch {
+    OpsPass P;
+    GOp ops[kOpsParam];
+};
+static_assert(sizeof(OpsLaunch) <= 32000, "kernel parameter space");
+void launch_ops_pass(Handle *h, const OpsLaunch &L);
+bool launch_ops_pass_tma(Handle *h, const OpsLaunch &L);   // k_tma.cu
 
 // A queued gate in physical local positions (api.cu gate queue).
 struct QOp {
@@ -202,8 +215,6 @@ struct Handle {
     // gate queue (fused into k_ops passes at the next flush)
     std::vector<QOp> queue;
     int fuse = 1;
-    GOp *d_ops = nullptr;
-    size_t d_ops_cap = 0;
     // in-process rank group (qsim_create_group): the group handle owns the
     // member handles (one shard each); members point back at the group
     std::vector<Handle *> members;

@@ -259,23 +259,85 @@ __device__ __forceinline__ void diag_any(double2 (&v)[NS], const GOp &op)
     }
 }
 
+// dense 2x2 on register bit RB where register bit CB == CV (one window control)
+template <int RB, int CB, int CV>
+__device__ __forceinline__ void cdense_rb(double2 (&v)[NS], const GOp &op)
+{
+    const double2 u0 = op.u[0], u1 = op.u[1], u2 = op.u[2], u3 = op.u[3];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        if (k & (1 << RB)) continue;
+        if (((k >> CB) & 1) != CV) continue;
+        const double2 x = v[k], y = v[k | (1 << RB)];
+        v[k] = cfma2(u0, x, u1, y);
+        v[k | (1 << RB)] = cfma2(u2, x, u3, y);
+    }
+}
+
+// two 2x2 on register bit RB, selected by register bit CS (u[0..3] / u[4..7])
+template <int RB, int CS>
+__device__ __forceinline__ void dense2_rb(double2 (&v)[NS], const GOp &op)
+{
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        if (k & (1 << RB)) continue;
+        const int o = ((k >> CS) & 1) * 4;
+        const double2 x = v[k], y = v[k | (1 << RB)];
+        v[k] = cfma2(op.u[o], x, op.u[o + 1], y);
+        v[k | (1 << RB)] = cfma2(op.u[o + 2], x, op.u[o + 3], y);
+    }
+}
+
+#define QS_CD(RB, CB)                                                  \
+    case (RB) * 8 + (CB) * 2 + 0: cdense_rb<RB, CB, 0>(v, op); break; \
+    case (RB) * 8 + (CB) * 2 + 1: cdense_rb<RB, CB, 1>(v, op); break;
+#define QS_D2(RB, CS) \
+    case (RB) * 4 + (CS): dense2_rb<RB, CS>(v, op); break;
+
 // Apply ops [i0, i1) of a gate-list pass to the 16 register slots of a thread
-// (thread part tpart of the tile index, tile id T).
+// (thread part tpart of the tile index, tile id T).  The op list lives in the
+// kernel parameters: every field read is warp-uniform.
 __device__ __forceinline__ void run_ops(double2 (&v)[NS], const GOp *ops, int i0, int i1, uint64_t T, uint32_t tpart)
 {
     for (int i = i0; i < i1; ++i) {
         const GOp &op = ops[i];
         if ((T & op.fm) != op.fv) continue;           // fixed-bit controls (uniform)
         if ((tpart & op.tm) != op.tv) continue;       // thread-part controls
-        switch (op.kind * 4 + op.rb) {
-        case 0: dense_any<0>(v, op); break;
-        case 1: dense_any<1>(v, op); break;
-        case 2: dense_any<2>(v, op); break;
-        case 3: dense_any<3>(v, op); break;
-        case 4: diag_any<0>(v, op); break;
-        case 5: diag_any<1>(v, op); break;
-        case 6: diag_any<2>(v, op); break;
-        case 7: diag_any<3>(v, op); break;
+        switch (op.kind) {
+        case GOP_DENSE:
+            switch (op.rb) {
+            case 0: dense_any<0>(v, op); break;
+            case 1: dense_any<1>(v, op); break;
+            case 2: dense_any<2>(v, op); break;
+            default: dense_any<3>(v, op); break;
+            }
+            break;
+        case GOP_CDENSE:
+            switch (op.rb * 8 + op.cs * 2 + op.cv) {
+                QS_CD(0, 1) QS_CD(0, 2) QS_CD(0, 3)
+                QS_CD(1, 0) QS_CD(1, 2) QS_CD(1, 3)
+                QS_CD(2, 0) QS_CD(2, 1) QS_CD(2, 3)
+                QS_CD(3, 0) QS_CD(3, 1) QS_CD(3, 2)
+            default: break;
+            }
+            break;
+        case GOP_DENSE2:
+            switch (op.rb * 4 + op.cs) {
+                QS_D2(0, 1) QS_D2(0, 2) QS_D2(0, 3)
+                QS_D2(1, 0) QS_D2(1, 2) QS_D2(1, 3)
+                QS_D2(2, 0) QS_D2(2, 1) QS_D2(2, 3)
+                QS_D2(3, 0) QS_D2(3, 1) QS_D2(3, 2)
+            default: break;
+            }
+            break;
+        case GOP_DIAGW:
+            switch (op.rb) {
+            case 0: diag_any<0>(v, op); break;
+            case 1: diag_any<1>(v, op); break;
+            case 2: diag_any<2>(v, op); break;
+            default: diag_any<3>(v, op); break;
+            }
+            break;
         default: {
             double2 d;
             if (op.kind == GOP_DIAGT) d = (tpart & op.tb) ? op.u[3] : op.u[0];
@@ -289,6 +351,8 @@ __device__ __forceinline__ void run_ops(double2 (&v)[NS], const GOp *ops, int i0
         }
     }
 }
+#undef QS_CD
+#undef QS_D2
 
 }  // namespace tile
 }  // namespace qs

@@ -417,6 +417,36 @@ def test_fused_gate_passes_match_oracle(reg, n, ngates):
     assert maxdiff(get(hu, n), ref) < TOL
 
 
+@pytest.mark.parametrize("n,nq,ngates", [(14, 5, 400), (18, 7, 500), (22, 14, 600)])
+def test_fused_merge_runs_match_oracle(reg, n, nq, ngates):
+    """Runs the planner's merging hard: gates on a few qubits, each
+    uncontrolled, singly controlled (either value) or a controlled phase, so
+    consecutive gates on one target collapse into single / choice (DENSE2) /
+    controlled (CDENSE) register updates and commute past each other."""
+    rng = np.random.default_rng(77 + n)
+    psi = rand_state(n, 90 + n)
+    h = reg(n, psi)
+    ref = psi.copy()
+    qs = [int(x) for x in rng.choice(n, size=nq, replace=False)]
+    for _ in range(ngates):
+        q = qs[int(rng.integers(nq))]
+        kind = int(rng.integers(5))
+        if kind == 4:
+            U = np.diag([1, np.exp(1j * rng.uniform(0, 6.3))])
+        else:
+            U = O.mat_angles(O.HAAR, O.haar_angles(9, int(rng.integers(1 << 20))))
+        c = qs[int(rng.integers(nq))]
+        if c != q and rng.integers(3):
+            v = int(rng.integers(2))
+            Q.qsim_apply_ctrl(h, 1 << c, v << c, q, U)
+            O.apply_ctrl(ref, 1 << c, v << c, q, U)
+        else:
+            Q.qsim_apply_1q(h, q, U)
+            O.apply_1q(ref, q, U)
+    assert maxdiff(get(h, n), ref) < TOL
+    assert abs(Q.qsim_norm(h) - 1) < 1e-12
+
+
 def test_fusion_is_a_single_pass_for_small_registers(reg):
     """configs[0]: all 200 gates of the n = 10 circuit fuse into one launch."""
     h = reg(10)
