@@ -411,132 +411,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-// Gate-list pass on the same TMA pipeline (in place): tiles stream in by
-// TMA while the previous tile's op list runs in registers, results stream
-// back by TMA store.  The op interpretation (segments, register windows,
-// smem transposes) is k_ops.cu's; only the data movement differs.
-__global__ void __launch_bounds__(kThreads, 1)
-    k_ops_tma(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
-              const __grid_constant__ OpsLaunch L, const __grid_constant__ TmaArgs ta, uint64_t ntiles)
-{
-    static_assert(kTmaTileBits == 12, "tile");
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    double2 *bufs = reinterpret_cast<double2 *>(smem_raw);
-    uint64_t *full = reinterpret_cast<uint64_t *>(bufs + kStages * (1u << kTmaTileBits));
-    const OpsPass &P = L.P;
-    const uint32_t tid = threadIdx.x;
-    if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (tid == 0) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&in_map) : "memory");
-        for (uint64_t q = 0; q < kStages - 1; ++q) {
-            const uint64_t T = blockIdx.x + q * gridDim.x;
-            if (T >= ntiles) break;
-            int c[5];
-            coords(ta.in_first, ta.in_len, T, c);
-            mbar_expect_tx(&full[q], kTileBytes);
-            tma_load(bufs + (size_t)q * (1u << kTmaTileBits), &in_map, c, &full[q]);
-        }
-    }
-    constexpr int tb = kTmaTileBits - kRegBits;
-    const TileMap &m0 = P.seg[0].map;
-    const TileMap &mL = P.seg[P.nseg - 1].map;
-    uint32_t lin = 0, lout = 0;
-    for (int t = 0; t < tb; ++t) {
-        lin |= ((tid >> t) & 1u) << ta.in_rank[m0.order[t]];
-        lout |= ((tid >> t) & 1u) << ta.out_rank[mL.order[t]];
-    }
-    uint32_t pin[kRegBits], pout[kRegBits];
-#pragma unroll
-    for (int b = 0; b < kRegBits; ++b) {
-        pin[b] = 1u << ta.in_rank[m0.win[b]];
-        pout[b] = 1u << ta.out_rank[mL.win[b]];
-    }
-    uint64_t j = 0;
-    for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x, ++j) {
-        const int st = (int)(j % kStages);
-        double2 *buf = bufs + (size_t)st * (1u << kTmaTileBits);
-        mbar_wait(&full[st], (uint32_t)((j / kStages) & 1));
-        double2 v[NS];
-        {
-            uint32_t o[NS];
-            o[0] = lin;
-#pragma unroll
-            for (int b = 0; b < kRegBits; ++b)
-#pragma unroll
-                for (int q = 0; q < (1 << b); ++q) o[q | (1 << b)] = o[q] | pin[b];
-#pragma unroll
-            for (int k = 0; k < NS; ++k) v[k] = buf[o[k]];
-        }
-        uint32_t prev_stp = 0;
-        uint32_t prev_wsw[kRegBits] = {0, 0, 0, 0};
-        for (int s = 0; s < P.nseg; ++s) {
-            const OpsSeg &sg = P.seg[s];
-            const uint32_t tpart = thread_part(sg.map, tb, tid);
-            const uint32_t stp = swz(tpart);
-            uint32_t wb[kRegBits], wsw[kRegBits];
-#pragma unroll
-            for (int b = 0; b < kRegBits; ++b) {
-                wb[b] = 1u << sg.map.win[b];
-                wsw[b] = swz(wb[b]);
-            }
-            if (s > 0) {
-                uint32_t o[NS];
-                o[0] = prev_stp;
-#pragma unroll
-                for (int b = 0; b < kRegBits; ++b)
-#pragma unroll
-                    for (int q = 0; q < (1 << b); ++q) o[q | (1 << b)] = o[q] ^ prev_wsw[b];
-                __syncthreads();
-#pragma unroll
-                for (int k = 0; k < NS; ++k) buf[o[k]] = v[k];
-                o[0] = stp;
-#pragma unroll
-                for (int b = 0; b < kRegBits; ++b)
-#pragma unroll
-                    for (int q = 0; q < (1 << b); ++q) o[q | (1 << b)] = o[q] ^ wsw[b];
-                __syncthreads();
-#pragma unroll
-                for (int k = 0; k < NS; ++k) v[k] = buf[o[k]];
-            }
-            run_ops(v, L.ops, sg.op_begin, sg.op_end, T, tpart);
-            prev_stp = stp;
-#pragma unroll
-            for (int b = 0; b < kRegBits; ++b) prev_wsw[b] = wsw[b];
-        }
-        {
-            uint32_t o[NS];
-            o[0] = lout;
-#pragma unroll
-            for (int b = 0; b < kRegBits; ++b)
-#pragma unroll
-                for (int q = 0; q < (1 << b); ++q) o[q | (1 << b)] = o[q] | pout[b];
-            __syncthreads();
-#pragma unroll
-            for (int k = 0; k < NS; ++k) buf[o[k]] = v[k];
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        if (tid == 0) {
-            int c[5];
-            coords(ta.out_first, ta.out_len, T, c);
-            tma_store(&out_map, c, buf);
-            bulk_wait_read<1>();
-            const uint64_t Tn = T + (uint64_t)(kStages - 1) * gridDim.x;
-            if (Tn < ntiles) {
-                const int sn = (int)((j + kStages - 1) % kStages);
-                coords(ta.in_first, ta.in_len, Tn, c);
-                mbar_expect_tx(&full[sn], kTileBytes);
-                tma_load(bufs + (size_t)sn * (1u << kTmaTileBits), &in_map, c, &full[sn]);
-            }
-        }
-    }
-    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-
 // ------------------------------------------------------------------ host
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
@@ -704,35 +578,6 @@ bool launch_tile_pass_tma(Handle *h, const TilePass &tp_in, const double2 *in, d
     case 5: launch_tma_nm<5>(h, im, om, tp, ta); break;
     default: launch_tma_nm<6>(h, im, om, tp, ta); break;
     }
-    return true;
-}
-
-bool launch_ops_pass_tma(Handle *h, const OpsLaunch &L)
-{
-    const OpsPass &P = L.P;
-    if (P.tbits != kTmaTileBits || getenv("QSIM_NO_TMA")) return false;
-    std::vector<int> fid(h->nl, -1);
-    for (int f = 0; f < P.nfix; ++f) fid[P.fin_pos[f]] = f;
-    std::vector<int> tp(P.in_pos, P.in_pos + P.tbits);
-    CUtensorMap im, om;
-    TmaArgs ta;
-    std::memset(&ta, 0, sizeof ta);
-    if (!build_side(h->psi, h->nl, tp, fid, im, ta.in_first, ta.in_len, ta.in_rank)) return false;
-    om = im;
-    std::memcpy(ta.out_first, ta.in_first, sizeof ta.in_first);
-    std::memcpy(ta.out_len, ta.in_len, sizeof ta.in_len);
-    std::memcpy(ta.out_rank, ta.in_rank, sizeof ta.in_rank);
-    const size_t smem = (size_t)kStages * kTileBytes + 8 * sizeof(uint64_t);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_ops_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
-    const uint64_t ntiles = 1ull << P.nfix;
-    const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)h->num_sms);
-    prof_begin(h);
-    k_ops_tma<<<grid, kThreads, smem, h->stream>>>(im, om, L, ta, ntiles);
-    prof_end(h, "k_ops_tma", (1ull << (P.tbits + P.nfix)) * 32);
     return true;
 }
 

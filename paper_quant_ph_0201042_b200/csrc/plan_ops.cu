@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <queue>
 #include <string>
@@ -93,12 +95,12 @@ POp from_queue(const QOp &q)
 }
 
 struct Segment {
-    int win[kRegBits];      // tile bits held in registers
+    int win[kOpsRegBits];      // tile bits held in registers
     std::vector<int> ops;   // op indices in application order
 };
 
-// Choice form (cs, m0, m1) of an op whose only control (if any) is one
-// window position; false if the op has other controls.
+// Choice form (cs, m0, m1) of an op with at most one control (any local
+// position: window, thread part or tile id); false if it has more.
 bool choice_form(const POp &p, const std::vector<char> &in_win, int &cs, double2 m0[4], double2 m1[4])
 {
     static const double2 I[4] = {{1, 0}, {0, 0}, {0, 0}, {1, 0}};
@@ -117,7 +119,6 @@ bool choice_form(const POp &p, const std::vector<char> &in_win, int &cs, double2
     }
     if (__builtin_popcountll(p.cmask) != 1) return false;
     const int c = __builtin_ctzll(p.cmask);
-    if (!in_win[c]) return false;
     cs = c;
     const bool v = (p.cval >> c) & 1;
     std::memcpy(v ? m1 : m0, p.m0, 4 * sizeof(double2));
@@ -192,7 +193,7 @@ std::vector<Segment> schedule(const std::vector<POp> &ops, int nl, const std::ve
     int ndone = 0;
     std::vector<Segment> segs;
     std::vector<int> prev;
-    for (int b = tbits - kRegBits; b < tbits; ++b) prev.push_back(b);
+    for (int b = tbits - kOpsRegBits; b < tbits; ++b) prev.push_back(b);
 
     // closure of window W from the current state; commit = apply it
     std::vector<int> c2;
@@ -235,46 +236,58 @@ std::vector<Segment> schedule(const std::vector<POp> &ops, int nl, const std::ve
 
     while (ndone < n) {
         std::vector<int> cand;
-        for (int j = 0; j < n && (int)cand.size() < 8; ++j) {
+        for (int j = 0; j < n && (int)cand.size() < 2 * kOpsRegBits; ++j) {
             if (done[j] || !ops[j].dense) continue;
             const int t = tbit_of[ops[j].tpos];
             if (std::find(cand.begin(), cand.end(), t) == cand.end()) cand.push_back(t);
         }
         std::vector<int> best;
-        if ((int)cand.size() <= kRegBits) {
+        if ((int)cand.size() <= kOpsRegBits) {
             best = cand;
             for (int b : prev)
-                if ((int)best.size() < kRegBits && std::find(best.begin(), best.end(), b) == best.end()) best.push_back(b);
+                if ((int)best.size() < kOpsRegBits && std::find(best.begin(), best.end(), b) == best.end()) best.push_back(b);
             // filler: highest tile positions first (low positions stay lane bits)
             std::vector<int> byp(tbits);
             for (int b = 0; b < tbits; ++b) byp[b] = b;
             std::sort(byp.begin(), byp.end(), [&](int x, int y) { return tile[x] > tile[y]; });
             for (int b : byp)
-                if ((int)best.size() < kRegBits && std::find(best.begin(), best.end(), b) == best.end()) best.push_back(b);
+                if ((int)best.size() < kOpsRegBits && std::find(best.begin(), best.end(), b) == best.end()) best.push_back(b);
         } else {
+            // every kOpsRegBits-subset of the candidates (<= C(10, 5) = 252)
             int bscore = -1;
             const int m = (int)cand.size();
-            for (int a = 0; a < m; ++a)
-                for (int b = a + 1; b < m; ++b)
-                    for (int c = b + 1; c < m; ++c)
-                        for (int d = c + 1; d < m; ++d) {
-                            std::vector<int> W = {cand[a], cand[b], cand[c], cand[d]};
-                            const int s = closure(W, false);
-                            if (s > bscore) {
-                                bscore = s;
-                                best = W;
-                            }
-                        }
+            std::vector<int> idx(kOpsRegBits);
+            for (int k = 0; k < kOpsRegBits; ++k) idx[k] = k;
+            while (true) {
+                std::vector<int> W(kOpsRegBits);
+                for (int k = 0; k < kOpsRegBits; ++k) W[k] = cand[idx[k]];
+                const int sc = closure(W, false);
+                if (sc > bscore) {
+                    bscore = sc;
+                    best = W;
+                }
+                int k = kOpsRegBits - 1;
+                while (k >= 0 && idx[k] == m - kOpsRegBits + k) --k;
+                if (k < 0) break;
+                ++idx[k];
+                for (int l = k + 1; l < kOpsRegBits; ++l) idx[l] = idx[l - 1] + 1;
+            }
         }
         std::sort(best.begin(), best.end());
         closure(best, true);
         Segment sg;
-        for (int b = 0; b < kRegBits; ++b) sg.win[b] = best[b];
+        for (int b = 0; b < kOpsRegBits; ++b) sg.win[b] = best[b];
         sg.ops = taken;
         segs.push_back(sg);
         prev = best;
     }
     return segs;
+}
+
+bool plan_log()
+{
+    static const bool on = std::getenv("QSIM_PLAN_LOG") != nullptr;
+    return on;
 }
 
 int launch_check(Handle *h, const char *what)
@@ -354,7 +367,7 @@ int flush_queue(Handle *h)
         for (size_t s = 0; s < segs.size(); ++s) {
             const Segment &sg = segs[s];
             std::vector<char> in_win(nl, 0);
-            for (int b = 0; b < kRegBits; ++b) in_win[tile[sg.win[b]]] = 1;
+            for (int b = 0; b < kOpsRegBits; ++b) in_win[tile[sg.win[b]]] = 1;
             const std::vector<int> &Ls = sg.ops;
             for (size_t jj = 0; jj < Ls.size(); ++jj) {
                 POp &B = ops[Ls[jj]];
@@ -370,7 +383,7 @@ int flush_queue(Handle *h)
             }
             auto win_idx = [&](int pos) {
                 const int t = tbit_of[pos];
-                for (int b = 0; b < kRegBits; ++b)
+                for (int b = 0; b < kOpsRegBits; ++b)
                     if (sg.win[b] == t) return b;
                 return -1;
             };
@@ -383,8 +396,9 @@ int flush_queue(Handle *h)
                     g.u[k] = q.m0[k];
                     g.u[4 + k] = q.m1[k];
                 }
-                if (q.cs >= 0) {
-                    // choice form (merged run): one 2x2 per value of the window bit cs
+                g.fsel = 0xff;
+                if (q.cs >= 0 && win_idx(q.cs) >= 0) {
+                    // choice form (merged run) selected by a window bit: static slot selection
                     g.rb = (uint8_t)win_idx(q.tpos);
                     g.cs = (uint8_t)win_idx(q.cs);
                     if (is_ident(q.m0)) {
@@ -396,6 +410,25 @@ int flush_queue(Handle *h)
                         g.cv = 0;
                     } else {
                         g.kind = GOP_DENSE2;
+                    }
+                    enc[s].push_back(g);
+                    continue;
+                }
+                if (q.cs >= 0) {
+                    // choice by a thread-part bit (one matrix per thread) or a
+                    // tile-id bit (one matrix per tile; a tile whose matrix is I skips)
+                    g.kind = GOP_DENSE;
+                    g.rb = (uint8_t)win_idx(q.tpos);
+                    const int tb = tbit_of[q.cs];
+                    if (tb >= 0) {
+                        g.tsel = 1u << tb;
+                    } else if (is_ident(q.m0) || is_ident(q.m1)) {
+                        const bool one = is_ident(q.m0);
+                        g.fm = 1ull << fix_of[q.cs];
+                        g.fv = one ? g.fm : 0;
+                        for (int k = 0; k < 4; ++k) g.u[k] = g.u[4 + k] = one ? q.m1[k] : q.m0[k];
+                    } else {
+                        g.fsel = (uint8_t)fix_of[q.cs];
                     }
                     enc[s].push_back(g);
                     continue;
@@ -466,17 +499,30 @@ int flush_queue(Handle *h)
             for (size_t k = pi; k < pe; ++k) {
                 const Segment &sg = segs[pieces[k].seg];
                 OpsSeg &os = P.seg[k - pi];
-                for (int b = 0; b < kRegBits; ++b) os.map.win[b] = sg.win[b];
+                for (int b = 0; b < kOpsRegBits; ++b) os.win[b] = sg.win[b];
                 std::vector<int> rest;
                 for (int b = 0; b < tbits; ++b)
-                    if (std::find(sg.win, sg.win + kRegBits, b) == sg.win + kRegBits) rest.push_back(b);
+                    if (std::find(sg.win, sg.win + kOpsRegBits, b) == sg.win + kOpsRegBits) rest.push_back(b);
                 // first/last segment of a launch: thread bits by position (coalesced gather/scatter)
                 if (k == pi || k + 1 == pe)
                     std::stable_sort(rest.begin(), rest.end(), [&](int x, int y) { return tile[x] < tile[y]; });
-                for (size_t t = 0; t < rest.size(); ++t) os.map.order[t] = rest[t];
+                for (size_t t = 0; t < rest.size(); ++t) os.order[t] = rest[t];
                 os.op_begin = P.nops;
                 for (size_t i = pieces[k].b; i < pieces[k].e; ++i) L.ops[P.nops++] = enc[pieces[k].seg][i];
                 os.op_end = P.nops;
+            }
+            if (plan_log()) {
+                int cnt[8] = {0};
+                int thr = 0;
+                for (int i = 0; i < P.nops; ++i) {
+                    ++cnt[L.ops[i].kind & 7];
+                    thr += L.ops[i].tm != 0;
+                }
+                std::fprintf(stderr,
+                             "[qsim plan] nl=%d tile=%d nseg=%d nops=%d dense=%d cdense=%d dense2=%d diagw=%d "
+                             "diagt=%d diagf=%d phase=%d thread-ctrl=%d\n",
+                             nl, tbits, P.nseg, P.nops, cnt[GOP_DENSE], cnt[GOP_CDENSE], cnt[GOP_DENSE2],
+                             cnt[GOP_DIAGW], cnt[GOP_DIAGT], cnt[GOP_DIAGF], cnt[GOP_PHASE], thr);
             }
             launch_ops_pass(h, L);
             if (int rc = launch_check(h, "fused gate pass")) return rc;

@@ -130,22 +130,30 @@ bool launch_tile_pass_tma(Handle *h, const TilePass &tp, const double2 *in, doub
 //   CDENSE  2x2 on window bit rb where window bit cs == cv (one control)
 //   DENSE2  2x2 on window bit rb: u[0..3] where window bit cs = 0, u[4..7]
 //           where it is 1 (a run of gates on one target, each uncontrolled or
-//           controlled by the same qubit, multiplied together on the host)
+//           controlled by the same qubit, multiplied together on the host);
+//           DENSE with tsel / fsel is the same choice by a thread-part or a
+//           tile-id bit (one matrix per thread / per tile: no divergence)
 // Controls: wm/wv on the 4 window bits (slot index), tm/tv on the other tile
 // bits (thread part), fm/fv on fixed bits (tile id).
 enum { GOP_DENSE = 0, GOP_DIAGW = 1, GOP_DIAGT = 2, GOP_DIAGF = 3, GOP_PHASE = 4, GOP_CDENSE = 5, GOP_DENSE2 = 6 };
 struct GOp {
     uint8_t kind, rb, wm, wv;
-    uint8_t cs, cv, pad_[2];
+    uint8_t cs, cv;
+    uint8_t fsel;      // DENSE: tile-id bit selecting u[4..7] (0xff: none)
+    uint8_t pad_;
     uint32_t tm, tv;   // controls on non-window tile bits
     uint32_t tb;       // DIAGT: mask of the target tile bit
     uint32_t fbit;     // DIAGF: tile-id bit of the target
+    uint32_t tsel;     // DENSE: thread-part bit selecting u[4..7] (0: none)
+    uint32_t pad2_;
     uint64_t fm, fv;   // controls on fixed bits (tile-id mask / values)
     double2 u[8];      // dense U (u11 u12 u21 u22) or diag(u[0], u[3]); DENSE2: two matrices
 };
 constexpr int kMaxSegs = 48;
+constexpr int kOpsRegBits = 5;   // gate-list passes: 32 amplitudes per thread
 struct OpsSeg {
-    TileMap map;       // register window + thread order
+    int win[kOpsRegBits];       // tile bits held in registers (slot bit b <-> tile bit win[b])
+    int order[kTileMaxBits];    // thread bit t <-> tile bit order[t]
     int op_begin, op_end;
 };
 struct OpsPass {
@@ -166,7 +174,6 @@ struct OpsLaunch {
 };
 static_assert(sizeof(OpsLaunch) <= 32000, "kernel parameter space");
 void launch_ops_pass(Handle *h, const OpsLaunch &L);
-bool launch_ops_pass_tma(Handle *h, const OpsLaunch &L);   // k_tma.cu
 
 // A queued gate in physical local positions (api.cu gate queue).
 struct QOp {

@@ -187,172 +187,5 @@ __device__ __forceinline__ void tile_body(double2 (&v)[NS], const TilePass &tp, 
     }
 }
 
-__device__ __forceinline__ double2 cfma2(double2 u, double2 x, double2 v, double2 y)
-{
-    double re = fma(u.x, x.x, -u.y * x.y);
-    double im = fma(u.x, x.y, u.y * x.x);
-    re = fma(v.x, y.x, re);
-    re = fma(-v.y, y.y, re);
-    im = fma(v.x, y.y, im);
-    im = fma(v.y, y.x, im);
-    return make_double2(re, im);
-}
-
-// dense 2x2 on register bit RB for every slot pair whose window controls match
-template <int RB, bool WC>
-__device__ __forceinline__ void dense_rb(double2 (&v)[NS], const GOp &op)
-{
-    const double2 u0 = op.u[0], u1 = op.u[1], u2 = op.u[2], u3 = op.u[3];
-    const uint32_t wm = op.wm, wv = op.wv;
-#pragma unroll
-    for (int k = 0; k < NS; ++k) {
-        if (k & (1 << RB)) continue;
-        if (WC && ((k & wm) != wv)) continue;
-        const double2 x = v[k], y = v[k | (1 << RB)];
-        v[k] = cfma2(u0, x, u1, y);
-        v[k | (1 << RB)] = cfma2(u2, x, u3, y);
-    }
-}
-
-// diag(d0, d1) on window bit RB (D0ONE: d0 == 1, only the b = 1 half moves)
-template <int RB, bool WC, bool D0ONE>
-__device__ __forceinline__ void diag_rb(double2 (&v)[NS], const GOp &op)
-{
-    const double2 d0 = op.u[0], d1 = op.u[3];
-    const uint32_t wm = op.wm, wv = op.wv;
-#pragma unroll
-    for (int k = 0; k < NS; ++k) {
-        if (WC && ((k & wm) != wv)) continue;
-        if (k & (1 << RB)) v[k] = cmul(v[k], d1);
-        else if (!D0ONE) v[k] = cmul(v[k], d0);
-    }
-}
-
-// multiply every slot whose window controls match by d
-template <bool WC>
-__device__ __forceinline__ void phase_all(double2 (&v)[NS], double2 d, uint32_t wm, uint32_t wv)
-{
-#pragma unroll
-    for (int k = 0; k < NS; ++k) {
-        if (WC && ((k & wm) != wv)) continue;
-        v[k] = cmul(v[k], d);
-    }
-}
-
-template <int RB>
-__device__ __forceinline__ void dense_any(double2 (&v)[NS], const GOp &op)
-{
-    if (op.wm) dense_rb<RB, true>(v, op);
-    else dense_rb<RB, false>(v, op);
-}
-
-template <int RB>
-__device__ __forceinline__ void diag_any(double2 (&v)[NS], const GOp &op)
-{
-    const bool one = op.u[0].x == 1.0 && op.u[0].y == 0.0;
-    if (op.wm) {
-        if (one) diag_rb<RB, true, true>(v, op);
-        else diag_rb<RB, true, false>(v, op);
-    } else {
-        if (one) diag_rb<RB, false, true>(v, op);
-        else diag_rb<RB, false, false>(v, op);
-    }
-}
-
-// dense 2x2 on register bit RB where register bit CB == CV (one window control)
-template <int RB, int CB, int CV>
-__device__ __forceinline__ void cdense_rb(double2 (&v)[NS], const GOp &op)
-{
-    const double2 u0 = op.u[0], u1 = op.u[1], u2 = op.u[2], u3 = op.u[3];
-#pragma unroll
-    for (int k = 0; k < NS; ++k) {
-        if (k & (1 << RB)) continue;
-        if (((k >> CB) & 1) != CV) continue;
-        const double2 x = v[k], y = v[k | (1 << RB)];
-        v[k] = cfma2(u0, x, u1, y);
-        v[k | (1 << RB)] = cfma2(u2, x, u3, y);
-    }
-}
-
-// two 2x2 on register bit RB, selected by register bit CS (u[0..3] / u[4..7])
-template <int RB, int CS>
-__device__ __forceinline__ void dense2_rb(double2 (&v)[NS], const GOp &op)
-{
-#pragma unroll
-    for (int k = 0; k < NS; ++k) {
-        if (k & (1 << RB)) continue;
-        const int o = ((k >> CS) & 1) * 4;
-        const double2 x = v[k], y = v[k | (1 << RB)];
-        v[k] = cfma2(op.u[o], x, op.u[o + 1], y);
-        v[k | (1 << RB)] = cfma2(op.u[o + 2], x, op.u[o + 3], y);
-    }
-}
-
-#define QS_CD(RB, CB)                                                  \
-    case (RB) * 8 + (CB) * 2 + 0: cdense_rb<RB, CB, 0>(v, op); break; \
-    case (RB) * 8 + (CB) * 2 + 1: cdense_rb<RB, CB, 1>(v, op); break;
-#define QS_D2(RB, CS) \
-    case (RB) * 4 + (CS): dense2_rb<RB, CS>(v, op); break;
-
-// Apply ops [i0, i1) of a gate-list pass to the 16 register slots of a thread
-// (thread part tpart of the tile index, tile id T).  The op list lives in the
-// kernel parameters: every field read is warp-uniform.
-__device__ __forceinline__ void run_ops(double2 (&v)[NS], const GOp *ops, int i0, int i1, uint64_t T, uint32_t tpart)
-{
-    for (int i = i0; i < i1; ++i) {
-        const GOp &op = ops[i];
-        if ((T & op.fm) != op.fv) continue;           // fixed-bit controls (uniform)
-        if ((tpart & op.tm) != op.tv) continue;       // thread-part controls
-        switch (op.kind) {
-        case GOP_DENSE:
-            switch (op.rb) {
-            case 0: dense_any<0>(v, op); break;
-            case 1: dense_any<1>(v, op); break;
-            case 2: dense_any<2>(v, op); break;
-            default: dense_any<3>(v, op); break;
-            }
-            break;
-        case GOP_CDENSE:
-            switch (op.rb * 8 + op.cs * 2 + op.cv) {
-                QS_CD(0, 1) QS_CD(0, 2) QS_CD(0, 3)
-                QS_CD(1, 0) QS_CD(1, 2) QS_CD(1, 3)
-                QS_CD(2, 0) QS_CD(2, 1) QS_CD(2, 3)
-                QS_CD(3, 0) QS_CD(3, 1) QS_CD(3, 2)
-            default: break;
-            }
-            break;
-        case GOP_DENSE2:
-            switch (op.rb * 4 + op.cs) {
-                QS_D2(0, 1) QS_D2(0, 2) QS_D2(0, 3)
-                QS_D2(1, 0) QS_D2(1, 2) QS_D2(1, 3)
-                QS_D2(2, 0) QS_D2(2, 1) QS_D2(2, 3)
-                QS_D2(3, 0) QS_D2(3, 1) QS_D2(3, 2)
-            default: break;
-            }
-            break;
-        case GOP_DIAGW:
-            switch (op.rb) {
-            case 0: diag_any<0>(v, op); break;
-            case 1: diag_any<1>(v, op); break;
-            case 2: diag_any<2>(v, op); break;
-            default: diag_any<3>(v, op); break;
-            }
-            break;
-        default: {
-            double2 d;
-            if (op.kind == GOP_DIAGT) d = (tpart & op.tb) ? op.u[3] : op.u[0];
-            else if (op.kind == GOP_DIAGF) d = ((T >> op.fbit) & 1u) ? op.u[3] : op.u[0];
-            else d = op.u[3];
-            if (!(d.x == 1.0 && d.y == 0.0)) {
-                if (op.wm) phase_all<true>(v, d, op.wm, op.wv);
-                else phase_all<false>(v, d, op.wm, op.wv);
-            }
-        }
-        }
-    }
-}
-#undef QS_CD
-#undef QS_D2
-
 }  // namespace tile
 }  // namespace qs
