@@ -214,6 +214,14 @@ bool is_diag(const double2 U[4]) { return U[1].x == 0 && U[1].y == 0 && U[2].x =
 // Immediate (unfused) application of a queued op.
 void run_op_now(Handle *h, const QOp &op)
 {
+    qs::run_gate_unfused(h, op);
+}
+
+}  // namespace
+
+// The paper's one-sweep-per-gate kernels (k_gates.cu) for one queued op.
+void qs::run_gate_unfused(Handle *h, const QOp &op)
+{
     if (op.diag) {
         if (op.tpos >= 0) launch_apply_diag(h, op.tpos, op.cmask, op.cval, op.u[0], op.u[3]);
         else if (!(op.u[3].x == 1.0 && op.u[3].y == 0.0)) launch_phase_mask(h, op.cmask, op.cval, op.u[3]);
@@ -221,6 +229,8 @@ void run_op_now(Handle *h, const QOp &op)
         launch_apply_2x2(h, op.tpos, op.cmask, op.cval, op.u);
     }
 }
+
+namespace {
 
 // A member's failure is reported on the handle the caller holds.
 int lift(Handle *top, const Ranks &R, int rc)

@@ -58,15 +58,15 @@ __global__ void __launch_bounds__(kThreads) k_apply_2x2(double2 *__restrict__ ps
             const uint64_t j = base + (uint64_t)k * stride;
             i0[k] = insert_zero(j, p);
             ok[k] = j < npairs && (i0[k] & cm) == cv;
-            if (ok[k]) { a[k] = psi[i0[k]]; b[k] = psi[i0[k] + s]; }
+            if (ok[k]) { a[k] = __ldcs(psi + i0[k]); b[k] = __ldcs(psi + i0[k] + s); }
         }
 #pragma unroll
         for (int k = 0; k < kUnroll; ++k) {
             if (!ok[k]) continue;
             const double2 x = cfma2(U.u[0], a[k], U.u[1], b[k]);
             const double2 y = cfma2(U.u[2], a[k], U.u[3], b[k]);
-            psi[i0[k]] = x;
-            psi[i0[k] + s] = y;
+            __stcs(psi + i0[k], x);
+            __stcs(psi + i0[k] + s, y);
         }
     }
 }
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kThreads) k_phase_mask(double2 *__restrict__ p
         uint64_t i = j;
         for (int k = 0; k < mb.nb; ++k) i = insert_zero(i, mb.bit[k]);
         i |= val;
-        psi[i] = cmul(psi[i], ph);
+        __stcs(psi + i, cmul(__ldcs(psi + i), ph));
     }
 }
 

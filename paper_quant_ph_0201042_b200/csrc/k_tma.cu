@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "qsim_internal.h"
+#include "ops_common.cuh"
 #include "tile_common.cuh"
 
 namespace qs {
@@ -411,6 +412,94 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Gate-list pass on the TMA pipeline (in place), for passes whose FP64 work
+// hides under the transfer: tiles stream in by TMA while the previous tile's
+// segments run in registers (ops_common.cuh, transposes in the stage buffer),
+// results stream back by TMA store.  One CTA of 128 threads per SM.
+__global__ void __launch_bounds__(ops::kOpsThreads, 1)
+    k_ops_tma(const __grid_constant__ CUtensorMap map, const __grid_constant__ OpsLaunch L,
+              const __grid_constant__ TmaArgs ta, uint64_t ntiles)
+{
+    using namespace ops;
+    static_assert(kTmaTileBits == kTileMaxBits, "tile");
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    double2 *bufs = reinterpret_cast<double2 *>(smem_raw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(bufs + kStages * (1u << kTmaTileBits));
+    const OpsPass &P = L.P;
+    const uint32_t tid = threadIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map) : "memory");
+        for (uint64_t q = 0; q < kStages - 1; ++q) {
+            const uint64_t T = blockIdx.x + q * gridDim.x;
+            if (T >= ntiles) break;
+            int c[5];
+            coords(ta.in_first, ta.in_len, T, c);
+            mbar_expect_tx(&full[q], kTileBytes);
+            tma_load(bufs + (size_t)q * (1u << kTmaTileBits), &map, c, &full[q]);
+        }
+    }
+    const int tb = kTmaTileBits - RB5;
+    const OpsSeg &s0 = P.seg[0];
+    const OpsSeg &sL = P.seg[P.nseg - 1];
+    uint32_t lin = 0, lout = 0;
+    for (int t = 0; t < tb; ++t) {
+        lin |= ((tid >> t) & 1u) << ta.in_rank[s0.order[t]];
+        lout |= ((tid >> t) & 1u) << ta.in_rank[sL.order[t]];
+    }
+    uint32_t pin[RB5], pout[RB5];
+#pragma unroll
+    for (int b = 0; b < RB5; ++b) {
+        pin[b] = 1u << ta.in_rank[s0.win[b]];
+        pout[b] = 1u << ta.in_rank[sL.win[b]];
+    }
+    uint64_t j = 0;
+    for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x, ++j) {
+        const int st = (int)(j % kStages);
+        double2 *buf = bufs + (size_t)st * (1u << kTmaTileBits);
+        mbar_wait(&full[st], (uint32_t)((j / kStages) & 1));
+        double2 v[NS5];
+#pragma unroll
+        for (int k = 0; k < NS5; ++k) {
+            uint32_t o = lin;
+#pragma unroll
+            for (int b = 0; b < RB5; ++b)
+                if (k & (1 << b)) o |= pin[b];
+            v[k] = buf[o];
+        }
+        run_segments(v, L, T, tid, tb, buf);
+        __syncthreads();   // every reader of the stage buffer is done
+#pragma unroll
+        for (int k = 0; k < NS5; ++k) {
+            uint32_t o = lout;
+#pragma unroll
+            for (int b = 0; b < RB5; ++b)
+                if (k & (1 << b)) o |= pout[b];
+            buf[o] = v[k];
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            int c[5];
+            coords(ta.in_first, ta.in_len, T, c);
+            tma_store(&map, c, buf);
+            bulk_wait_read<1>();
+            const uint64_t Tn = T + (uint64_t)(kStages - 1) * gridDim.x;
+            if (Tn < ntiles) {
+                const int sn = (int)((j + kStages - 1) % kStages);
+                coords(ta.in_first, ta.in_len, Tn, c);
+                mbar_expect_tx(&full[sn], kTileBytes);
+                tma_load(bufs + (size_t)sn * (1u << kTmaTileBits), &map, c, &full[sn]);
+            }
+        }
+    }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ host
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
@@ -578,6 +667,31 @@ bool launch_tile_pass_tma(Handle *h, const TilePass &tp_in, const double2 *in, d
     case 5: launch_tma_nm<5>(h, im, om, tp, ta); break;
     default: launch_tma_nm<6>(h, im, om, tp, ta); break;
     }
+    return true;
+}
+
+bool launch_ops_pass_tma(Handle *h, const OpsLaunch &L)
+{
+    const OpsPass &P = L.P;
+    if (P.tbits != kTmaTileBits || getenv("QSIM_NO_TMA")) return false;
+    std::vector<int> fid(h->nl, -1);
+    for (int f = 0; f < P.nfix; ++f) fid[P.fin_pos[f]] = f;
+    std::vector<int> tp(P.in_pos, P.in_pos + P.tbits);
+    CUtensorMap im;
+    TmaArgs ta;
+    std::memset(&ta, 0, sizeof ta);
+    if (!build_side(h->psi, h->nl, tp, fid, im, ta.in_first, ta.in_len, ta.in_rank)) return false;
+    const size_t smem = (size_t)kStages * kTileBytes + 8 * sizeof(uint64_t);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_ops_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    const uint64_t ntiles = 1ull << P.nfix;
+    const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)h->num_sms);
+    prof_begin(h);
+    k_ops_tma<<<grid, ops::kOpsThreads, smem, h->stream>>>(im, L, ta, ntiles);
+    prof_end(h, "k_ops_tma", (1ull << (P.tbits + P.nfix)) * 32);
     return true;
 }
 

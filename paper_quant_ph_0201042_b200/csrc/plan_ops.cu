@@ -338,6 +338,22 @@ int flush_queue(Handle *h)
             }
         }
         rem.swap(left);
+        // A pass of one sparse gate (controlled, or a phase on half the
+        // amplitudes) reads and writes every amplitude; the unfused kernel
+        // touches only the amplitudes the gate changes -- worth it when the
+        // masked positions are >= 3 (runs of >= 128 B, so DRAM skips whole
+        // sectors).
+        if (take.size() == 1) {
+            const QOp &q = take[0];
+            uint64_t m = q.cmask;
+            if (q.diag && q.tpos >= 0 && q.u[0].x == 1.0 && q.u[0].y == 0.0) m |= 1ull << q.tpos;
+            if (q.diag && q.tpos < 0) m = q.cmask;
+            if (m && (m & 7ull) == 0) {
+                run_gate_unfused(h, q);
+                if (int rc = launch_check(h, "gate")) return rc;
+                continue;
+            }
+        }
         // tile: active + passive lowest positions
         std::vector<int> tile(act);
         std::vector<int> tbit_of(nl, -1);

@@ -174,6 +174,7 @@ struct OpsLaunch {
 };
 static_assert(sizeof(OpsLaunch) <= 32000, "kernel parameter space");
 void launch_ops_pass(Handle *h, const OpsLaunch &L);
+bool launch_ops_pass_tma(Handle *h, const OpsLaunch &L);   // k_tma.cu; false: geometry unsupported
 
 // A queued gate in physical local positions (api.cu gate queue).
 struct QOp {
@@ -259,6 +260,8 @@ int dist_canonicalize(const Ranks &R);                               // pos[q] =
 // per-rank host partials -> the sum over all ranks of the world, in rank order
 // (parts[i] belongs to R[i]); out may alias parts[0]
 int dist_sum_host(const Ranks &R, const std::vector<std::vector<double>> &parts, double *out, size_t count);
+// one queued gate with the unfused streaming kernels (k_gates.cu)
+void run_gate_unfused(Handle *h, const QOp &op);
 // run every queued gate (fused passes); called before anything that reads or moves data
 int flush_queue(Handle *h);
 int flush_all(const Ranks &R);
