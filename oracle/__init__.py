@@ -81,6 +81,9 @@ _sig("orc_gcd", _u64, _u64, _u64)
 _sig("orc_apply_angles", None, _p, _i32, C.POINTER(_Noise), _i32, _p, _u64, _u64, _i32)
 _sig("orc_qft", None, _p, _i32, _i32, _i32, _i32, C.POINTER(_Noise))
 _sig("orc_hadamard_range", None, _p, _i32, _i32, _i32)
+_sig("orc_aqft", None, _p, _i32, _i32, _i32, _i32, _i32, C.POINTER(_Noise))
+_sig("orc_measure_range", _u64, _p, _i32, _i32, _i32, _f64, _i32)
+_sig("orc_inner", None, _p, _p, _i32, _p)
 _sig("orc_dft_samples", None, _p, _i32, _i32, _p, _i32, _p)
 _sig("orc_cfg0", None, _p, _i32, _u64, _i32, _p, _p)
 _sig("orc_grover_mark", _u64, _u64, _i32)
@@ -245,6 +248,25 @@ def apply_angles(psi, noise: Noise, kind, ang, ctrl_mask, ctrl_vals, q):
 def qft(psi, lo, m, inverse=False, noise: Noise | None = None):
     noise = noise or Noise()
     _lib.orc_qft(_state(psi), _nq(psi), lo, m, int(bool(inverse)), C.byref(noise._c))
+
+
+def aqft(psi, lo, m, b, inverse=False, noise: Noise | None = None):
+    """Approximate QFT: R_d with d > b omitted (R30)."""
+    noise = noise or Noise()
+    _lib.orc_aqft(_state(psi), _nq(psi), lo, m, b, int(bool(inverse)), C.byref(noise._c))
+
+
+def measure_range(psi, lo, m, r: float, collapse=True) -> int:
+    """Measure qubits [lo, lo+m) with random number r (R31); collapses psi."""
+    return _lib.orc_measure_range(_state(psi), _nq(psi), lo, m, r, int(bool(collapse)))
+
+
+def inner(a, b) -> complex:
+    """<a|b> (pairwise sum); the paper's fidelity is abs(inner) (R32)."""
+    assert a.shape == b.shape
+    out = np.zeros(1, np.complex128)
+    _lib.orc_inner(_state(a), _state(b), _nq(a), _ptr(out))
+    return complex(out[0])
 
 
 def hadamard_range(psi, lo, m):

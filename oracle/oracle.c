@@ -343,6 +343,61 @@ uint64_t orc_measure(const cplx *psi, int n, double r)
     return last_nz;
 }
 
+/* Measurement of the sub-register of qubits [lo, lo+m) (PAPER.md:391-404
+ * applied to the marginal distribution; reading R31): y = the smallest value
+ * with sum_{y'<=y} P(y') > r, scanning P in order (P from orc_probs); if
+ * rounding leaves r >= the total, the largest y with P(y) > 0.  With collapse
+ * != 0 the state is projected onto that value and renormalised:
+ * alpha_j <- alpha_j / sqrt(P(y)) where the sub-register of j equals y, 0
+ * elsewhere. */
+uint64_t orc_measure_range(cplx *psi, int n, int lo, int m, double r, int collapse)
+{
+    const uint64_t ny = (uint64_t)1 << m;
+    double *P = (double *)malloc(sizeof(double) * ny);
+    orc_probs(psi, n, lo, m, P);
+    double acc = 0.0;
+    uint64_t y = ny, last_nz = 0;
+    for (uint64_t v = 0; v < ny; ++v) {
+        if (P[v] > 0.0) last_nz = v;
+        acc += P[v];
+        if (r < acc) { y = v; break; }
+    }
+    if (y == ny) y = last_nz;
+    if (collapse) {
+        const double s = 1.0 / sqrt(P[y]);
+        const uint64_t dim = (uint64_t)1 << n;
+        const int shift = n - lo - m;
+        #pragma omp parallel for schedule(static)
+        for (int64_t jj = 0; jj < (int64_t)dim; ++jj) {
+            uint64_t j = (uint64_t)jj;
+            if (((j >> shift) & (ny - 1)) == y) psi[j] *= s;
+            else psi[j] = 0.0;
+        }
+    }
+    free(P);
+    return y;
+}
+
+/* Pairwise sum of conj(a_j) b_j over [lo, lo+len) (R23). */
+static cplx pairwise_inner(const cplx *a, const cplx *b, uint64_t lo, uint64_t len)
+{
+    if (len <= 8) {
+        cplx s = 0.0;
+        for (uint64_t j = lo; j < lo + len; ++j) s += conj(a[j]) * b[j];
+        return s;
+    }
+    uint64_t h = len / 2;
+    return pairwise_inner(a, b, lo, h) + pairwise_inner(a, b, lo + h, len - h);
+}
+
+/* Inner product <a|b> = sum_j conj(a_j) b_j; the paper's fidelity is its
+ * modulus, "the inner product of the correct state and the simulated state"
+ * (reading C26/R32). */
+void orc_inner(const cplx *a, const cplx *b, int n, cplx *out)
+{
+    *out = pairwise_inner(a, b, 0, (uint64_t)1 << n);
+}
+
 /* ------------------------------------------------------------------------ */
 /* Basis permutations: modular multiplication / exponentiation               */
 /* (§2.3.3; applied semantically as a permutation, R9/R10) */
@@ -437,6 +492,40 @@ void orc_qft(cplx *psi, int n, int lo, int m, int inverse, orc_noise_t *nz)
             nz->g += 1;
         }
         for (int k = j + 1; k < m; ++k) {
+            double phi = sgn * ORC_PI / ldexp(1.0, k - j);
+            uint64_t cm = (uint64_t)1 << (lo + k);
+            if (nz->sigma > 0.0) {
+                orc_apply_angles(psi, n, nz, ORC_P1, &phi, cm, cm, lo + j);
+            } else {
+                cplx R[4] = { 1.0, 0.0, 0.0, cos(phi) + I * sin(phi) };
+                orc_apply_ctrl(psi, n, cm, cm, lo + j, R);
+                nz->g += 1;
+            }
+        }
+    }
+    for (int j = 0; j < m / 2; ++j) orc_swap(psi, n, lo + j, lo + m - 1 - j);
+}
+
+/* Approximate QFT (§2.3.2: "the controlled phase shift
+ * gates acting on distantly separated qubits contribute only exponentially
+ * small phases"; Barenco et al.): the circuit of orc_qft with every R_d of
+ * distance d = k - j > b left out (reading R30).  b >= m-1 is the exact QFT.
+ * The gate counter g advances only for gates that are applied. */
+void orc_aqft(cplx *psi, int n, int lo, int m, int b, int inverse, orc_noise_t *nz)
+{
+    const double sgn = inverse ? -1.0 : 1.0;
+    const double r = 0.70710678118654752440; /* M_SQRT1_2 */
+    cplx H[4] = { r, r, r, -r };
+    for (int j = 0; j < m; ++j) {
+        if (nz->sigma > 0.0) {
+            double ang[2] = { ORC_PI / 4.0, ORC_PI };
+            orc_apply_angles(psi, n, nz, ORC_RP, ang, 0, 0, lo + j);
+        } else {
+            orc_apply_1q(psi, n, lo + j, H);
+            nz->g += 1;
+        }
+        for (int k = j + 1; k < m; ++k) {
+            if (k - j > b) continue;
             double phi = sgn * ORC_PI / ldexp(1.0, k - j);
             uint64_t cm = (uint64_t)1 << (lo + k);
             if (nz->sigma > 0.0) {
