@@ -202,6 +202,23 @@ int qsim_hadamard(qsim_t *h, int lo, int m);
  * m + m(m-1)/2 in total either way).  QSIM_ERANGE if the range leaves [0, n). */
 int qsim_qft(qsim_t *h, int lo, int m, int inverse);
 
+/* FFT of the sub-register [lo, lo+m) ("If we regard the
+ * QFT transform as a black box operator ... we can use fast Fourier
+ * transform (FFT) in the simulator instead of the QFT circuit"; SURVEY §8(f)
+ * row f1): the exact transform beta_x = 2^(-m/2) sum_y e^(+-2 pi i x y/2^m)
+ * alpha_y of qsim_qft, never subject to gate noise and not counted by the
+ * gate counter (it is not a circuit).  Radix-2^(<=10) Cooley-Tukey passes over
+ * HBM (the same tile kernels as the noiseless QFT).  QSIM_ERANGE if the range
+ * leaves [0, n). */
+int qsim_fft(qsim_t *h, int lo, int m, int inverse);
+
+/* Approximate QFT (§2.3.2; Barenco et al.; R30):
+ * the qsim_qft circuit with every R_d of distance d = k - j > b left out.
+ * b >= m-1 is qsim_qft.  Gate noise applies as in qsim_qft; the gate counter
+ * advances only for the gates that are applied.  QSIM_ERANGE if the range
+ * leaves [0, n) or b < 0. */
+int qsim_aqft(qsim_t *h, int lo, int m, int b, int inverse);
+
 /* Sign-changing operator V_f for f = delta_{x, idx}, as
  * the phase flip alpha_idx <- -alpha_idx (R17).  QSIM_ERANGE if
  * idx >= 2^n. */
@@ -280,6 +297,21 @@ int qsim_prob_index(qsim_t *h, uint64_t idx, double *out);
  * then a scan of one block); if rounding leaves r >= the total, the largest i
  * with alpha_i != 0 (R22). */
 int qsim_measure(qsim_t *h, double r, uint64_t *idx);
+
+/* Measurement of the sub-register [lo, lo+m) (PAPER.md:391-404 applied to
+ * its marginal distribution; R31): y = the smallest value with
+ * sum_{y'<=y} P(y') > r (P as qsim_probs, summed in order on the host); if
+ * rounding leaves r >= the total, the largest y with P(y) > 0.  With
+ * collapse != 0 the state is projected onto y and renormalised by
+ * 1/sqrt(P(y)) on the device.  m <= 26.  Synchronising. */
+int qsim_measure_range(qsim_t *h, int lo, int m, double r, int collapse, uint64_t *y);
+
+/* Inner product <a|b> = sum_i conj(a_i) b_i of two registers of the same size
+ * on the same devices (the paper's fidelity is its modulus, "the inner product
+ * of the correct state and the simulated state"; DESIGN.md
+ * R32).  Fixed-order tree sums on the device, ranks combined in rank order.
+ * QSIM_EINVAL if the handles differ in n, world or devices.  Synchronising. */
+int qsim_inner(qsim_t *a, qsim_t *b, qsim_c128 *out);
 
 /* ---------------------------------------------------------------- Shor, semantic mode */
 /* Shor's factoring algorithm in the paper's semantic mode

@@ -671,6 +671,7 @@ void qsim_destroy(qsim_t *h)
     if (h->psi) cudaFree(h->psi);
     if (h->scratch) cudaFree(h->scratch);
     if (h->d_red) cudaFree(h->d_red);
+    if (h->d_probs) cudaFree(h->d_probs);
     if (h->h_red) cudaFreeHost(h->h_red);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -925,42 +926,38 @@ int qsim_hadamard(qsim_t *h, int lo, int m)
     return QSIM_OK;
 }
 
-int qsim_qft(qsim_t *h, int lo, int m, int inverse)
+// The QFT circuit of PAPER.md:442-469 gate by gate through the gate queue
+// (fused into tile passes at the next flush): H(lo+j), R_{k-j} controlled by
+// lo+k on lo+j for k - j <= band, closing swaps as relabels.  With gate noise
+// every H / R_d is an angle-form gate (R14/R15); count = advance the gate
+// counter per applied gate.
+static int qft_gates(qsim_t *h, const Ranks &R, int lo, int m, int band, int inverse, bool count)
 {
-    QS_CHECK_HANDLE(h);
-    if (lo < 0 || m < 0 || lo + m > h->n) return fail(h, QSIM_ERANGE, "range outside [0, n)");
-    if (m == 0) return QSIM_OK;
-    const Ranks R = ranks_of(h);
     const double sgn = inverse ? -1.0 : 1.0;
-    if (h->sigma == 0.0 && h->nl >= 9 && m <= h->nl) {
-        // noiseless: fused passes (constant gates, DESIGN.md R25)
-        h->gcount += (uint64_t)m + (uint64_t)m * (m - 1) / 2;
-        return lift(h, R, fused_range(R, lo, m, 1, inverse));
-    }
-    // gate by gate (angle forms with operational noise, R14/R15): the gate
-    // queue fuses them into tile passes
     const double r = M_SQRT1_2;
     const double2 H[4] = {make_double2(r, 0), make_double2(r, 0), make_double2(r, 0), make_double2(-r, 0)};
+    const bool noisy = count && h->sigma > 0.0;
     for (int j = 0; j < m; ++j) {
         int rc;
-        if (h->sigma > 0.0) {
+        if (noisy) {
             const double ang[2] = {M_PI / 4.0, M_PI};
             rc = qsim_apply_angles(h, QSIM_GATE_RP, ang, 0, 0, lo + j);
         } else {
             rc = lift(h, R, apply_gate(R, 0, 0, lo + j, H));
-            h->gcount++;
+            if (count) h->gcount++;
         }
         if (rc) return rc;
         for (int k = j + 1; k < m; ++k) {
+            if (k - j > band) continue;
             const double phi = sgn * M_PI / std::ldexp(1.0, k - j);
             const uint64_t cm = 1ull << (lo + k);
-            if (h->sigma > 0.0) {
+            if (noisy) {
                 rc = qsim_apply_angles(h, QSIM_GATE_P1, &phi, cm, cm, lo + j);
             } else {
                 double2 Rd[4] = {make_double2(1, 0), make_double2(0, 0), make_double2(0, 0),
                                  make_double2(std::cos(phi), std::sin(phi))};
                 rc = lift(h, R, apply_gate(R, cm, cm, lo + j, Rd));
-                h->gcount++;
+                if (count) h->gcount++;
             }
             if (rc) return rc;
         }
@@ -968,6 +965,40 @@ int qsim_qft(qsim_t *h, int lo, int m, int inverse)
     for (Handle *mm : R)
         for (int j = 0; j < m / 2; ++j) std::swap(mm->pos[lo + j], mm->pos[lo + m - 1 - j]);
     return QSIM_OK;
+}
+
+int qsim_qft(qsim_t *h, int lo, int m, int inverse)
+{
+    QS_CHECK_HANDLE(h);
+    if (lo < 0 || m < 0 || lo + m > h->n) return fail(h, QSIM_ERANGE, "range outside [0, n)");
+    if (m == 0) return QSIM_OK;
+    const Ranks R = ranks_of(h);
+    if (h->sigma == 0.0 && h->fuse && h->nl >= 9 && m <= h->nl) {
+        // noiseless: fused passes (constant gates, DESIGN.md R25)
+        h->gcount += (uint64_t)m + (uint64_t)m * (m - 1) / 2;
+        return lift(h, R, fused_range(R, lo, m, 1, inverse));
+    }
+    // noisy, or fusion off (the paper's one sweep per gate)
+    return qft_gates(h, R, lo, m, m, inverse, true);
+}
+
+int qsim_fft(qsim_t *h, int lo, int m, int inverse)
+{
+    QS_CHECK_HANDLE(h);
+    if (lo < 0 || m < 0 || lo + m > h->n) return fail(h, QSIM_ERANGE, "range outside [0, n)");
+    if (m == 0) return QSIM_OK;
+    const Ranks R = ranks_of(h);
+    if (h->nl >= 9 && m <= h->nl) return lift(h, R, fused_range(R, lo, m, 1, inverse));
+    return qft_gates(h, R, lo, m, m, inverse, false);   // tiny registers: constant gates, not counted
+}
+
+int qsim_aqft(qsim_t *h, int lo, int m, int b, int inverse)
+{
+    QS_CHECK_HANDLE(h);
+    if (lo < 0 || m < 0 || lo + m > h->n || b < 0) return fail(h, QSIM_ERANGE, "range outside [0, n) or b < 0");
+    if (m == 0) return QSIM_OK;
+    if (b >= m - 1) return qsim_qft(h, lo, m, inverse);
+    return qft_gates(h, ranks_of(h), lo, m, b, inverse, true);
 }
 
 int qsim_phase_flip(qsim_t *h, uint64_t idx)
@@ -1156,18 +1187,28 @@ int qsim_probs(qsim_t *h, int lo, int m, double *out)
     std::vector<std::vector<double>> parts(R.size(), std::vector<double>(ny, 0.0));
     for (size_t i = 0; i < R.size(); ++i) {
         Handle *hm = R[i];
-        double *d_res = nullptr;
-        if (cudaMalloc(&d_res, nyl * sizeof(double)) != cudaSuccess) {
-            cudaGetLastError();
-            return fail(h, QSIM_ENOMEM, "probs buffer");
+        if (hm->probs_cap < nyl) {
+            if (hm->d_probs) {
+                cudaStreamSynchronize(hm->stream);
+                cudaFree(hm->d_probs);
+            }
+            hm->d_probs = nullptr;
+            hm->probs_cap = 0;
+            if (cudaMalloc(&hm->d_probs, nyl * sizeof(double)) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(h, QSIM_ENOMEM, "probs buffer");
+            }
+            hm->probs_cap = nyl;
         }
+        double *d_res = hm->d_probs;
         if (mloc > 0) launch_probs_contig(hm, pl, mloc, d_res);
         else launch_norm(hm, d_res);
         int rc = after_launch(hm, "probs");
-        std::vector<double> part(nyl);
-        if (!rc) rc = check_cuda(hm, cudaMemcpyAsync(part.data(), d_res, nyl * sizeof(double), cudaMemcpyDeviceToHost, hm->stream), "probs");
+        ensure_hred(hm, nyl);   // pinned staging: a pageable D2H of 2^m doubles is several times slower
+        if (!rc && !hm->h_red) rc = fail(hm, QSIM_ENOMEM, "pinned probs buffer");
+        if (!rc) rc = check_cuda(hm, cudaMemcpyAsync(hm->h_red, d_res, nyl * sizeof(double), cudaMemcpyDeviceToHost, hm->stream), "probs");
         if (!rc) rc = check_cuda(hm, cudaStreamSynchronize(hm->stream), "probs");
-        cudaFree(d_res);
+        const double *part = hm->h_red;
         if (rc) return lift(h, R, rc);
         // y = (rank bits inside the range) << mloc | y_loc
         uint64_t yhi = 0;
@@ -1179,6 +1220,92 @@ int qsim_probs(qsim_t *h, int lo, int m, double *out)
         for (uint64_t y = 0; y < nyl; ++y) parts[i][(yhi << mloc) | y] = part[y];
     }
     return lift(h, R, dist_sum_host(R, parts, out, ny));
+}
+
+int qsim_measure_range(qsim_t *h, int lo, int m, double r, int collapse, uint64_t *y)
+{
+    QS_CHECK_HANDLE(h);
+    if (!y) return QSIM_EINVAL;
+    if (lo < 0 || m < 1 || m > 26 || lo + m > h->n) return fail(h, QSIM_ERANGE, "range outside [0, n) or m > 26");
+    const uint64_t ny = 1ull << m;
+    std::vector<double> P(ny);
+    if (int rc = qsim_probs(h, lo, m, P.data())) return rc;   // canonical layout from here on
+    // R31: the sequential scan of PAPER.md:400-401 over the marginal
+    double acc = 0.0;
+    uint64_t v = ny, last_nz = 0;
+    for (uint64_t k = 0; k < ny; ++k) {
+        if (P[k] > 0.0) last_nz = k;
+        acc += P[k];
+        if (r < acc) {
+            v = k;
+            break;
+        }
+    }
+    if (v == ny) v = last_nz;
+    *y = v;
+    if (!collapse) return QSIM_OK;
+    if (!(P[v] > 0.0)) return fail(h, QSIM_ESTATE, "measured value has zero probability (zero state)");
+    const double s = 1.0 / std::sqrt(P[v]);
+    // canonical: sub-register value bit b <-> position n-lo-m+b; positions >= nl are rank bits
+    const Ranks R = ranks_of(h);
+    const int pl = h->n - lo - m;
+    for (Handle *hm : R) {
+        uint64_t mask = 0, val = 0;
+        int zero_all = 0;
+        for (int b = 0; b < m; ++b) {
+            const int p = pl + b;
+            const uint64_t want = (v >> b) & 1;
+            if (p < hm->nl) {
+                mask |= 1ull << p;
+                val |= want << p;
+            } else if ((((uint64_t)hm->rank >> (p - hm->nl)) & 1) != want) {
+                zero_all = 1;
+            }
+        }
+        launch_collapse(hm, mask, val, s, zero_all);
+        if (int rc = after_launch(hm, "collapse")) return lift(h, R, rc);
+    }
+    return QSIM_OK;
+}
+
+int qsim_inner(qsim_t *a, qsim_t *b, qsim_c128 *out)
+{
+    QS_CHECK_HANDLE(a);
+    QS_CHECK_HANDLE(b);
+    if (!out) return QSIM_EINVAL;
+    const Ranks Ra = ranks_of(a), Rb = ranks_of(b);
+    if (a->n != b->n || Ra.size() != Rb.size() || a->world != b->world)
+        return fail(a, QSIM_EINVAL, "inner product of registers of different shapes");
+    for (size_t i = 0; i < Ra.size(); ++i)
+        if (Ra[i]->device != Rb[i]->device || Ra[i]->rank != Rb[i]->rank)
+            return fail(a, QSIM_EINVAL, "inner product of registers on different devices");
+    if (int rc = dist_canonicalize(Ra)) return lift(a, Ra, rc);
+    if (int rc = dist_canonicalize(Rb)) return lift(b, Rb, rc);
+    std::vector<std::vector<double>> parts(Ra.size(), std::vector<double>(2, 0.0));
+    for (size_t i = 0; i < Ra.size(); ++i) {
+        Handle *ha = Ra[i], *hb = Rb[i];
+        // b's shard must be complete before a's stream reads it
+        cudaEvent_t ev;
+        if (int rc = check_cuda(ha, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "inner")) return lift(a, Ra, rc);
+        cudaEventRecord(ev, hb->stream);
+        cudaStreamWaitEvent(ha->stream, ev, 0);
+        double *d_out = nullptr;
+        int rc = check_cuda(ha, cudaMalloc(&d_out, 2 * sizeof(double)), "inner buffer");
+        if (!rc) {
+            launch_inner(ha, ha->psi, hb->psi, d_out);
+            rc = after_launch(ha, "inner");
+        }
+        if (!rc) rc = check_cuda(ha, cudaMemcpyAsync(parts[i].data(), d_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, ha->stream), "inner");
+        if (!rc) rc = check_cuda(ha, cudaStreamSynchronize(ha->stream), "inner");
+        if (d_out) cudaFree(d_out);
+        cudaEventDestroy(ev);
+        if (rc) return lift(a, Ra, rc);
+    }
+    double res[2];
+    if (int rc = dist_sum_host(Ra, parts, res, 2)) return lift(a, Ra, rc);
+    out->re = res[0];
+    out->im = res[1];
+    return QSIM_OK;
 }
 
 int qsim_prob_index(qsim_t *h, uint64_t idx, double *out)

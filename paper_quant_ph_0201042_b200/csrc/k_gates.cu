@@ -128,7 +128,7 @@ void launch_apply_2x2(Handle *h, int p, uint64_t cm, uint64_t cv, const double2 
     prof_begin(h);
     k_apply_2x2<<<grid_for(h, (np + kUnroll - 1) / kUnroll), kThreads, 0, h->stream>>>(h->psi, np, p,
                                                                                       cm, cv, m);
-    prof_end(h, "k_apply_2x2", (np >> __builtin_popcountll(cm)) * 32);
+    prof_end(h, "k_apply_2x2", (np >> __builtin_popcountll(cm)) * 64);   // 2 amplitudes read + written per pair
 }
 
 void launch_apply_diag(Handle *h, int p, uint64_t cm, uint64_t cv, double2 d0, double2 d1)

@@ -113,6 +113,45 @@ __global__ void k_probs_finish(const double *__restrict__ part, uint64_t ny, uin
     }
 }
 
+// <a|b> over chunks: block c sums conj(a_i) b_i over [c*chunk, (c+1)*chunk)
+// and writes re to out_re[c], im to out_im[c] (same fixed tree as the norm).
+__global__ void __launch_bounds__(kThreads) k_chunk_inner(const double2 *__restrict__ a,
+                                                          const double2 *__restrict__ b, uint64_t chunk,
+                                                          double *__restrict__ out_re,
+                                                          double *__restrict__ out_im)
+{
+    __shared__ double sh[32];
+    const uint64_t base = (uint64_t)blockIdx.x * chunk;
+    double re = 0.0, im = 0.0;
+    for (uint64_t i = threadIdx.x; i < chunk; i += blockDim.x) {
+        const double2 x = a[base + i], y = b[base + i];
+        re = fma(x.x, y.x, fma(x.y, y.y, re));
+        im = fma(x.x, y.y, fma(-x.y, y.x, im));
+    }
+    const double sr = block_sum(re, sh);
+    const double si = block_sum(im, sh);
+    if (threadIdx.x == 0) {
+        out_re[blockIdx.x] = sr;
+        out_im[blockIdx.x] = si;
+    }
+}
+
+// Projection of a measured sub-register (R31): amplitudes whose masked bits
+// equal val are scaled by s, every other one (all of them if zero_all) is 0.
+__global__ void __launch_bounds__(kThreads) k_collapse(double2 *__restrict__ psi, uint64_t count, uint64_t mask,
+                                                       uint64_t val, double s, int zero_all)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+        if (zero_all || (i & mask) != val) {
+            psi[i] = make_double2(0.0, 0.0);
+        } else {
+            const double2 v = psi[i];
+            psi[i] = make_double2(v.x * s, v.y * s);
+        }
+    }
+}
+
 // Gaussian amplitudes (R19) generated on the device with the library's Philox.
 __global__ void __launch_bounds__(kThreads) k_init_gaussian(double2 *__restrict__ psi, uint64_t count,
                                                             uint64_t gbase, uint64_t seed)
@@ -166,6 +205,47 @@ void launch_norm(Handle *h, double *d_out)
         prof_end(h, "k_sum_doubles", nb * 8);
         sum_tree(h, h->d_red + 8 + nb, nb2, d_out);
     }
+}
+
+// tree sum of nb doubles at d_in (inside the reduction workspace, offset
+// >= 8) into d_out; two levels above 2^20 partials
+static void tree_sum_ws(Handle *h, const double *d_in, uint64_t nb, double *d_tmp, double *d_out)
+{
+    if (nb <= (1u << 20)) {
+        sum_tree(h, d_in, nb, d_out);
+        return;
+    }
+    const uint64_t nb2 = nb >> 10;
+    prof_begin(h);
+    k_sum_doubles<<<(unsigned)nb2, 1024, 0, h->stream>>>(d_in, 1024, 1024, d_tmp);
+    prof_end(h, "k_sum_doubles", nb * 8);
+    sum_tree(h, d_tmp, nb2, d_out);
+}
+
+void launch_inner(Handle *h, const double2 *a, const double2 *b, double *d_out)
+{
+    const int bb = h->nl < 12 ? h->nl : 12;
+    const uint64_t nb = h->local_dim() >> bb;
+    ensure_red(h, 2 * nb + (nb >> 9) + 16);
+    double *re = h->d_red + 8, *im = re + nb, *tmp = im + nb;
+    prof_begin(h);
+    k_chunk_inner<<<(unsigned)nb, kThreads, 0, h->stream>>>(a, b, 1ull << bb, re, im);
+    prof_end(h, "k_chunk_inner", h->local_dim() * 32);
+    tree_sum_ws(h, re, nb, tmp, d_out);
+    tree_sum_ws(h, im, nb, tmp, d_out + 1);
+}
+
+void launch_collapse(Handle *h, uint64_t mask, uint64_t val, double s, int zero_all)
+{
+    const uint64_t count = h->local_dim();
+    const uint64_t want = (count + kThreads - 1) / kThreads;
+    const uint64_t cap = (uint64_t)h->num_sms * 8;
+    prof_begin(h);
+    k_collapse<<<(unsigned)(want < cap ? want : cap), kThreads, 0, h->stream>>>(h->psi, count, mask, val, s,
+                                                                                 zero_all);
+    // zeroed amplitudes are only written; the kept ones are read and written
+    const uint64_t kept = zero_all ? 0 : count >> __builtin_popcountll(mask);
+    prof_end(h, "k_collapse", count * 16 + kept * 16);
 }
 
 void launch_probs_contig(Handle *h, int pl, int m, double *d_out)

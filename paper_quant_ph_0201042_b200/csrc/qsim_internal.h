@@ -50,6 +50,12 @@ void launch_set_one(Handle *h, uint64_t local_idx);
 void launch_init_gaussian(Handle *h, uint64_t seed);
 // sum |a|^2 over the shard -> one double on the device (d_out), tree order.
 void launch_norm(Handle *h, double *d_out);
+// <a|b> over one shard (a, b: 2^nl amplitudes on this device) -> d_out[0..1]
+// (re, im) on the device; fixed tree order.  d_out must not be in the
+// reduction workspace.
+void launch_inner(Handle *h, const double2 *a, const double2 *b, double *d_out);
+// psi[i] *= s where (i & mask) == val, 0 elsewhere (everywhere if zero_all).
+void launch_collapse(Handle *h, uint64_t mask, uint64_t val, double s, int zero_all);
 // Partial sums of |a|^2 over consecutive blocks of 2^blk_bits amplitudes.
 void launch_block_abs2(Handle *h, int blk_bits, double *d_out);
 // Marginals over the `m` physical positions [pl, pl+m) (value bit b <-> position pl+b).
@@ -198,6 +204,8 @@ struct Handle {
     // reduction workspace
     double *d_red = nullptr;
     size_t red_cap = 0;          // doubles
+    double *d_probs = nullptr;   // qsim_probs output (grow-only)
+    size_t probs_cap = 0;
     double *h_red = nullptr;     // pinned
     size_t hred_cap = 0;
     // angle noise (R15)

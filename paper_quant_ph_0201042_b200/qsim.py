@@ -96,6 +96,10 @@ _sig("qsim_set_gate_counter", _i32, _H, _u64)
 _sig("qsim_swap", _i32, _H, _i32, _i32)
 _sig("qsim_hadamard", _i32, _H, _i32, _i32)
 _sig("qsim_qft", _i32, _H, _i32, _i32, _i32)
+_sig("qsim_fft", _i32, _H, _i32, _i32, _i32)
+_sig("qsim_aqft", _i32, _H, _i32, _i32, _i32, _i32)
+_sig("qsim_measure_range", _i32, _H, _i32, _i32, _f64, _i32, C.POINTER(_u64))
+_sig("qsim_inner", _i32, _H, _H, _p)
 _sig("qsim_phase_flip", _i32, _H, _u64)
 _sig("qsim_grover", _i32, _H, _u64, _i32, _p)
 _sig("qsim_apply_perm", _i32, _H, C.POINTER(qsim_perm_t))
@@ -260,6 +264,14 @@ def qsim_qft(h, lo: int, m: int, inverse: bool = False) -> None:
     _chk(h, lib.qsim_qft(h, lo, m, int(bool(inverse))))
 
 
+def qsim_fft(h, lo: int, m: int, inverse: bool = False) -> None:
+    _chk(h, lib.qsim_fft(h, lo, m, int(bool(inverse))))
+
+
+def qsim_aqft(h, lo: int, m: int, b: int, inverse: bool = False) -> None:
+    _chk(h, lib.qsim_aqft(h, lo, m, b, int(bool(inverse))))
+
+
 def qsim_phase_flip(h, idx: int) -> None:
     _chk(h, lib.qsim_phase_flip(h, idx))
 
@@ -313,6 +325,18 @@ def qsim_measure(h, r: float) -> int:
     v = _u64()
     _chk(h, lib.qsim_measure(h, r, C.byref(v)))
     return v.value
+
+
+def qsim_measure_range(h, lo: int, m: int, r: float, collapse: bool = True) -> int:
+    v = _u64()
+    _chk(h, lib.qsim_measure_range(h, lo, m, r, int(bool(collapse)), C.byref(v)))
+    return v.value
+
+
+def qsim_inner(a, b) -> complex:
+    out = np.zeros(1, np.complex128)
+    _chk(a, lib.qsim_inner(a, b, out.ctypes.data))
+    return complex(out[0])
 
 
 # ------------------------------------------------------------------ RNG + planners

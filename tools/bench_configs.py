@@ -87,6 +87,7 @@ def cfg2(n=28):
 def cfg3(sigma):
     ne, nw = 20, 10
     h = Q.qsim_create(ne + nw)
+    W.run_cfg3(h, ne, nw, 1007, 4, sigma)      # warm-up (lazy module loading, workspaces)
     ms, wall, prof, P = timed(h, lambda: W.run_cfg3(h, ne, nw, 1007, 4, sigma))
     n = ne + nw
     gb = (2 * ne) * (1 << (n + 5)) + ne * (ne - 1) // 2 * (1 << (n + 3)) + ne // 2 * (1 << (n + 4)) \
@@ -98,12 +99,59 @@ def cfg3(sigma):
 
 def cfg4(n=32, layers=20):
     h = Q.qsim_create(n)
+    W.run_cfg4(h, n, 2, 5, 1e-3, 1e-4)          # warm-up (lazy module loading)
     ms, wall, prof, ev = timed(h, lambda: W.run_cfg4(h, n, layers, 5, 1e-3, 1e-4))
     gates = layers * (n + (n - 1) // 2)
     report(f"configs[4] noisy brickwork n={n} layers={layers}", n, ms, wall, prof,
            layers * n * (1 << (n + 5)) + layers * ((n - 1) // 2) * (1 << (n + 4)),
            {"events": ev, "gates": gates})
     Q.qsim_destroy(h)
+
+
+def f1(n=28):
+    """Row f1: the paper's Table 1 comparison on B200 -- the QFT circuit gate
+    by gate (one HBM sweep per gate, the paper's algorithm), the same circuit
+    fused into tile passes, and the FFT entry point."""
+    h = Q.qsim_create(n)
+    Q.qsim_init_gaussian(h, 3)
+    gb = n * (1 << (n + 5)) + n * (n - 1) // 2 * (1 << (n + 3)) + n // 2 * (1 << (n + 4))
+    Q.qsim_set_fusion(h, False)
+    Q.qsim_qft(h, 0, n, False)
+    ms, wall, prof, _ = timed(h, lambda: Q.qsim_qft(h, 0, n, False))
+    report(f"f1 QFT circuit n={n}, one sweep per gate (fusion off)", n, ms, wall, prof, gb)
+    Q.qsim_set_fusion(h, True)
+    Q.qsim_qft(h, 0, n, False)
+    ms, wall, prof, _ = timed(h, lambda: Q.qsim_qft(h, 0, n, False), reps=5)
+    report(f"f1 QFT circuit n={n}, fused passes", n, ms, wall, prof, gb)
+    Q.qsim_fft(h, 0, n, False)
+    ms, wall, prof, _ = timed(h, lambda: Q.qsim_fft(h, 0, n, False), reps=5)
+    report(f"f1 qsim_fft n={n}", n, ms, wall, prof, gb)
+    Q.qsim_destroy(h)
+
+
+def f4(n=28, b=8, nm=30):
+    """Row f4: approximate QFT (band b) through the gate queue, partial
+    measurement with collapse and the inner product (fidelity)."""
+    h = Q.qsim_create(n)
+    Q.qsim_init_gaussian(h, 3)
+    gates = n + sum(1 for j in range(n) for k in range(j + 1, n) if k - j <= b)
+    gb = n * (1 << (n + 5)) + (gates - n) * (1 << (n + 3)) + n // 2 * (1 << (n + 4))
+    Q.qsim_aqft(h, 0, n, b, False)
+    ms, wall, prof, _ = timed(h, lambda: Q.qsim_aqft(h, 0, n, b, False), reps=3)
+    report(f"f4 AQFT n={n} band b={b} ({gates} gates)", n, ms, wall, prof, gb)
+    Q.qsim_destroy(h)
+    ha, hb = Q.qsim_create(nm), Q.qsim_create(nm)
+    Q.qsim_init_gaussian(ha, 3)
+    Q.qsim_init_gaussian(hb, 5)
+    Q.qsim_inner(ha, hb)
+    Q.qsim_measure_range(ha, 0, 20, 0.37, False)
+    ms, wall, prof, v = timed(ha, lambda: Q.qsim_inner(ha, hb), reps=3)
+    report(f"f4 inner product n={nm}", nm, ms, wall, prof, 2 * (1 << (nm + 4)), {"inner_abs": abs(v)})
+    ms, wall, prof, y = timed(ha, lambda: Q.qsim_measure_range(ha, 0, 20, 0.37, True))
+    report(f"f4 measure qubits [0,20) of n={nm} with collapse", nm, ms, wall, prof,
+           (1 << (nm + 4)) + (1 << (nm + 5)), {"y": y, "norm_after": Q.qsim_norm(ha)})
+    Q.qsim_destroy(ha)
+    Q.qsim_destroy(hb)
 
 
 if __name__ == "__main__":
@@ -123,3 +171,7 @@ if __name__ == "__main__":
             cfg4(26, 20)
         elif w == "4":
             cfg4(32, 20)
+        elif w == "f1":
+            f1()
+        elif w == "f4":
+            f4()
