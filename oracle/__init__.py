@@ -96,6 +96,9 @@ _sig("orc_cfg3", None, _p, _i32, _i32, _u64, _u64, _u64, _f64, _p)
 _sig("orc_cfg4", _i32, _p, _i32, _i32, _u64, _f64, _f64, _p, _i32)
 _sig("orc_inject_paulis", None, _p, _i32, _u64, _u64, _u64, _f64, _p, _i32, _p)
 _sig("orc_shor_prob_succ", _f64, _u64, _u64)
+_sig("orc_traj_ht", None, _p, _i32, _i32, _u64, _f64, _f64)
+_sig("orc_traj_grover", None, _p, _i32, _u64, _i32, _u64, _f64, _f64, _p)
+_sig("orc_qft_decoherent", None, _p, _i32, _i32, _i32, _i32, C.POINTER(_Noise), _f64)
 _sig("orc_shor_semantic_state", None, _p, _i32, _u64, _u64, _u64)
 _sig("orc_shor_candidates", _i32, _u64, _i32, _u64, _p, _i32)
 _sig("orc_shor_try", _u64, _u64, _u64, _u64, _i32)
@@ -381,3 +384,27 @@ def shor_run(N, m, seed, run, improved=False, max_iter=200, stats=None):
     assert st.dtype == np.int64 and st.size == len(SHOR_STATS)
     t = _lib.orc_shor_run(N, m, seed, run, int(bool(improved)), max_iter, C.byref(f), _ptr(st))
     return t, f.value
+
+
+# ------------------------------------------------------------------ row f2: noise-experiment trajectories
+def traj_ht(n, k, seed, sigma, p):
+    """One HT-experiment trajectory (R33/R34): final state."""
+    psi = np.zeros(1 << n, np.complex128)
+    _lib.orc_traj_ht(_ptr(psi), n, k, seed, sigma, p)
+    return psi
+
+
+def traj_grover(n, k, iters, seed, sigma, p):
+    """One Grover-experiment trajectory (R35): final
+    (n+1)-qubit state (ancilla = LSB) and trace[t] = P(register = k)."""
+    psi = np.zeros(1 << (n + 1), np.complex128)
+    trace = np.zeros(max(iters, 1), np.float64)
+    _lib.orc_traj_grover(_ptr(psi), n, k, iters, seed, sigma, p, _ptr(trace))
+    return psi, trace[:iters]
+
+
+def qft_decoherent(psi, lo, m, inverse=False, noise: Noise | None = None, p=0.0):
+    """QFT circuit with angle noise and the depolarizing channel after every
+    R_d (PAPER.md:1053-1160, R36), in place."""
+    noise = noise or Noise()
+    _lib.orc_qft_decoherent(_state(psi), _nq(psi), lo, m, int(bool(inverse)), C.byref(noise._c), p)

@@ -800,6 +800,108 @@ int orc_cfg4(cplx *psi, int n, int layers, uint64_t seed, double sigma, double p
 /* Prob_succ; 969-998 improvements).  SURVEY.md §8(f) row f3.                */
 /* ------------------------------------------------------------------------ */
 
+/* ------------------------------------------------------------------------ */
+/* Noise experiments, one trajectory each (reading  */
+/* R33: trajectory t of a batch with base seed s is exactly the single-      */
+/* register circuit below run with seed s + t for both its gate noise and    */
+/* its Pauli draws).                                                         */
+/* ------------------------------------------------------------------------ */
+
+/* HT experiment (§4.3): start |0..0>; k times: the noisy
+ * H = U_R(pi/4 + x) U_P1(pi + y) on every qubit (angle-form RP, gate counter
+ * from 0), then the depolarizing channel on every qubit with epoch = the
+ * application index (reading R34: one injection point per HT application). */
+void orc_traj_ht(cplx *psi, int n, int k, uint64_t seed, double sigma, double p)
+{
+    const uint64_t dim = (uint64_t)1 << n;
+    memset(psi, 0, sizeof(cplx) * dim);
+    psi[0] = 1.0;
+    orc_noise_t nz = { seed, sigma, 0 };
+    const double ang[2] = { ORC_PI / 4.0, ORC_PI };
+    for (int i = 0; i < k; ++i) {
+        for (int q = 0; q < n; ++q) orc_apply_angles(psi, n, &nz, ORC_RP, ang, 0, 0, q);
+        int nev = 0;
+        orc_inject_paulis(psi, n, seed, (uint64_t)i, ((uint64_t)1 << n) - 1, p, NULL, 0, &nev);
+    }
+}
+
+/* Grover experiment (§5.3; reading R35): an n-qubit
+ * register (qubits 0..n-1) and the ancilla of V_f (qubit n, the LSB),
+ * prepared noiselessly in |0..0>|->.  H_n = noisy RP(pi/4, pi) on every
+ * register qubit; V_f = the noisy NOT = RP(pi/2, pi) on the ancilla,
+ * controlled by register == f (all n register qubits are controls); one
+ * G-iteration = V_{fk}, H_n, V_{f0}, H_n (the global sign -1 is dropped),
+ * then the depolarizing channel on every register qubit (epoch = iteration).
+ * trace[t] = P(register = k) after iteration t+1 (summed over the ancilla). */
+void orc_traj_grover(cplx *psi, int n, uint64_t k, int iters, uint64_t seed, double sigma, double p,
+                     double *trace)
+{
+    const int nt = n + 1;
+    const uint64_t dim = (uint64_t)1 << nt;
+    memset(psi, 0, sizeof(cplx) * dim);
+    const double r = 0.70710678118654752440;
+    psi[0] = r;                 /* |0..0>|-> : ancilla (LSB) (|0> - |1>)/sqrt2 */
+    psi[1] = -r;
+    orc_noise_t nz = { seed, sigma, 0 };
+    const double hang[2] = { ORC_PI / 4.0, ORC_PI };
+    const double xang[2] = { ORC_PI / 2.0, ORC_PI };
+    const uint64_t regmask = ((uint64_t)1 << n) - 1;    /* qubits 0..n-1 */
+    for (int q = 0; q < n; ++q) orc_apply_angles(psi, nt, &nz, ORC_RP, hang, 0, 0, q);
+    for (int t = 0; t < iters; ++t) {
+        /* control values: qubit q (0 = MSB of the register value) has bit n-1-q of f */
+        uint64_t vk = 0;
+        for (int q = 0; q < n; ++q) vk |= ((k >> (n - 1 - q)) & 1) << q;
+        orc_apply_angles(psi, nt, &nz, ORC_RP, xang, regmask, vk, n);
+        for (int q = 0; q < n; ++q) orc_apply_angles(psi, nt, &nz, ORC_RP, hang, 0, 0, q);
+        orc_apply_angles(psi, nt, &nz, ORC_RP, xang, regmask, 0, n);
+        for (int q = 0; q < n; ++q) orc_apply_angles(psi, nt, &nz, ORC_RP, hang, 0, 0, q);
+        int nev = 0;
+        orc_inject_paulis(psi, nt, seed, (uint64_t)t, regmask, p, NULL, 0, &nev);
+        if (trace) {
+            const cplx a0 = psi[2 * k], a1 = psi[2 * k + 1];
+            trace[t] = creal(a0) * creal(a0) + cimag(a0) * cimag(a0) + creal(a1) * creal(a1) + cimag(a1) * cimag(a1);
+        }
+    }
+}
+
+/* QFT with decoherence (§5.2; reading R36): the QFT
+ * circuit of orc_qft on qubits [lo, lo+m) with its angle-form noise, and the
+ * depolarizing channel on every qubit of [lo, lo+m) after each R_d gate
+ * ("each time the register is applied by the controlled rotation gate R_d"),
+ * epoch = the index of that R_d in circuit order (0, 1, ...). */
+void orc_qft_decoherent(cplx *psi, int n, int lo, int m, int inverse, orc_noise_t *nz, double p)
+{
+    const double sgn = inverse ? -1.0 : 1.0;
+    const double r = 0.70710678118654752440;
+    cplx H[4] = { r, r, r, -r };
+    uint64_t qmask = 0;
+    for (int q = lo; q < lo + m; ++q) qmask |= (uint64_t)1 << q;
+    uint64_t epoch = 0;
+    for (int j = 0; j < m; ++j) {
+        if (nz->sigma > 0.0) {
+            double ang[2] = { ORC_PI / 4.0, ORC_PI };
+            orc_apply_angles(psi, n, nz, ORC_RP, ang, 0, 0, lo + j);
+        } else {
+            orc_apply_1q(psi, n, lo + j, H);
+            nz->g += 1;
+        }
+        for (int k = j + 1; k < m; ++k) {
+            double phi = sgn * ORC_PI / ldexp(1.0, k - j);
+            uint64_t cm = (uint64_t)1 << (lo + k);
+            if (nz->sigma > 0.0) {
+                orc_apply_angles(psi, n, nz, ORC_P1, &phi, cm, cm, lo + j);
+            } else {
+                cplx R[4] = { 1.0, 0.0, 0.0, cos(phi) + I * sin(phi) };
+                orc_apply_ctrl(psi, n, cm, cm, lo + j, R);
+                nz->g += 1;
+            }
+            int nev = 0;
+            orc_inject_paulis(psi, n, nz->seed, epoch++, qmask, p, NULL, 0, &nev);
+        }
+    }
+    for (int j = 0; j < m / 2; ++j) orc_swap(psi, n, lo + j, lo + m - 1 - j);
+}
+
 /* Prob_succ(n) = (1 - phi/(n-1)) + phi/(n-1) * (1/2 * 4/pi^2 * e^-gamma / log log n),
  * natural logarithms. */
 double orc_shor_prob_succ(uint64_t n, uint64_t phi)
