@@ -267,7 +267,12 @@ typedef struct {
     uint64_t epoch;       /* injection point (counter i of the draws) */
 } qsim_noise_t;
 
-typedef struct { uint64_t epoch; int32_t qubit; int32_t pauli; /* 1 X, 2 Y, 3 Z */ } qsim_event_t;
+typedef struct {
+    uint64_t epoch;
+    int32_t qubit;
+    int32_t pauli;   /* 1 X, 2 Y, 3 Z */
+    uint64_t traj;   /* trajectory of a batched handle (qsim_set_batch), else 0 */
+} qsim_event_t;
 
 /* Depolarizing channel on pure-state trajectories: for each
  * qubit q in qubit_mask (ascending), u = u01(draw(seed, PAULI, epoch, q).a);
@@ -312,6 +317,32 @@ int qsim_measure_range(qsim_t *h, int lo, int m, double r, int collapse, uint64_
  * R32).  Fixed-order tree sums on the device, ranks combined in rank order.
  * QSIM_EINVAL if the handles differ in n, world or devices.  Synchronising. */
 int qsim_inner(qsim_t *a, qsim_t *b, qsim_c128 *out);
+
+/* ---------------------------------------------------------------- batched trajectories */
+/* Batched noisy trajectories (R33): the
+ * top b qubits [0, b) of the handle index 2^b independent trajectories of
+ * the register [b, n) -- the paper's noise experiments average 1000-10000
+ * runs.  Trajectory t draws its gate
+ * noise (qsim_set_gate_noise seed s) from s + t and its Pauli events
+ * (qsim_inject_errors seed s) from s + t, so it is exactly the single-register
+ * circuit run with seed s + t.  Gates may not act on [0, b); angle-form gates
+ * with sigma > 0 get one matrix per trajectory (built on the device), Pauli
+ * injection gives one event list over all trajectories (qubit order, then
+ * trajectory order, event.traj = t).  qsim_probs over [b, n) is the average
+ * over trajectories of each trajectory's marginal.  b must cover the rank
+ * bits of a sharded handle (trajectories shard across GPUs with no data
+ * exchange); n - b >= 9; b <= 24.  b = 0 turns batching off.  Flushes. */
+int qsim_set_batch(qsim_t *h, int b);
+
+/* Every trajectory set to the register state reg (host, 2^(n-b) amplitudes,
+ * normalised by the caller); amplitudes are stored scaled by 2^(-b/2) so the
+ * whole handle has norm 1.  Resets the layout.  QSIM_EINVAL if not batched. */
+int qsim_batch_set_state(qsim_t *h, const qsim_c128 *reg);
+
+/* out[t] = <ref|psi_t> for every trajectory t (host buffers: ref 2^(n-b)
+ * amplitudes, out 2^b values); the paper's fidelity is |out[t]| averaged
+ * (R32).  Fixed-order tree per trajectory.  Synchronising. */
+int qsim_batch_overlap(qsim_t *h, const qsim_c128 *ref, qsim_c128 *out);
 
 /* ---------------------------------------------------------------- Shor, semantic mode */
 /* Shor's factoring algorithm in the paper's semantic mode

@@ -250,15 +250,20 @@ int lift(Handle *top, const Ranks &R, int rc)
 // becomes a constant phase) and queues it; the queue is fused into tile
 // passes at the next flush (or run at once when fusion is off / the shard is
 // tiny).
-int apply_gate(const Ranks &R, uint64_t cmask, uint64_t cvals, int q, const double2 U[4])
+int apply_gate(const Ranks &R, uint64_t cmask, uint64_t cvals, int q, const double2 U[4],
+               const std::vector<const double2 *> *tabs = nullptr)
 {
-    const int diag = is_diag(U);
+    if (R[0]->batch_b && (q < R[0]->batch_b || (cmask & ((1ull << R[0]->batch_b) - 1))))
+        return fail(R[0], QSIM_EINVAL, "gate on a trajectory-index qubit of a batched handle");
+    const int diag = tabs ? 0 : is_diag(U);
     if (!diag && !is_local(R[0], q))
         if (int rc = dist_make_local(R, std::vector<int>{q})) return rc;
-    for (Handle *h : R) {
+    for (size_t ri = 0; ri < R.size(); ++ri) {
+        Handle *h = R[ri];
         QOp op;
         op.diag = diag;
         for (int k = 0; k < 4; ++k) op.u[k] = U[k];
+        if (tabs) op.tab = (*tabs)[ri];
         uint64_t lm, lv;
         if (!local_controls(h, cmask, cvals, lm, lv)) continue;
         op.cmask = lm;
@@ -275,7 +280,7 @@ int apply_gate(const Ranks &R, uint64_t cmask, uint64_t cvals, int q, const doub
             op.u[0] = make_double2(1.0, 0.0);
             op.u[3] = d;
         }
-        if (h->fuse && h->nl >= 9) {
+        if ((h->fuse && h->nl >= 9) || op.tab) {
             h->queue.push_back(op);
             if (h->queue.size() >= 4096)
                 if (int rc = flush_queue(h)) return rc;
@@ -672,6 +677,7 @@ void qsim_destroy(qsim_t *h)
     if (h->scratch) cudaFree(h->scratch);
     if (h->d_red) cudaFree(h->d_red);
     if (h->d_probs) cudaFree(h->d_probs);
+    if (h->d_tabs) cudaFree(h->d_tabs);
     if (h->h_red) cudaFreeHost(h->h_red);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -865,12 +871,63 @@ int qsim_apply_ctrl(qsim_t *h, uint64_t cmask, uint64_t cvals, int q, const qsim
     return lift(h, R, apply_gate(R, cmask, cvals, q, M));
 }
 
+// A table of 4 * B matrices in the member's arena (batch.cu); the member's
+// queue is flushed first when the arena is full (flushing consumes every
+// queued table, stream-ordered).
+static double2 *batch_table(Handle *m, uint64_t B, int &rc)
+{
+    rc = QSIM_OK;
+    const size_t need = 4 * B;
+    if (m->tabs_used + need > m->tabs_cap) {
+        if ((rc = flush_queue(m))) return nullptr;
+        m->tabs_used = 0;
+        if (need > m->tabs_cap) {
+            if (m->d_tabs) {
+                cudaStreamSynchronize(m->stream);
+                cudaFree(m->d_tabs);
+            }
+            m->d_tabs = nullptr;
+            m->tabs_cap = 0;
+            const size_t cap = std::max<size_t>(need * 64, (size_t)1 << 20);
+            if (cudaMalloc(&m->d_tabs, cap * sizeof(double2)) != cudaSuccess) {
+                cudaGetLastError();
+                rc = fail(m, QSIM_ENOMEM, "batch matrix tables");
+                return nullptr;
+            }
+            m->tabs_cap = cap;
+        }
+    }
+    double2 *p = m->d_tabs + m->tabs_used;
+    m->tabs_used += need;
+    return p;
+}
+
 int qsim_apply_angles(qsim_t *h, int kind, const double *ang, uint64_t cmask, uint64_t cvals, int q)
 {
     QS_CHECK_HANDLE(h);
     if (kind < 0 || kind > 2 || !ang) return fail(h, QSIM_EINVAL, "unknown angle-form gate kind");
     if (int rc = check_qubit(h, q)) return rc;
     if (int rc = check_ctrl(h, cmask, cvals, q)) return rc;
+    if (h->batch_b > 0 && h->sigma > 0.0) {
+        // batched trajectories: one perturbed matrix per trajectory, drawn on
+        // the device from seed + t (R33)
+        if (q < h->batch_b || (cmask & ((1ull << h->batch_b) - 1)))
+            return fail(h, QSIM_EINVAL, "gate on a trajectory-index qubit of a batched handle");
+        const Ranks R = ranks_of(h);
+        const uint64_t B = 1ull << h->batch_b;
+        std::vector<const double2 *> tabs;
+        for (Handle *m : R) {
+            int rc;
+            double2 *t = batch_table(m, B, rc);
+            if (!t) return lift(h, R, rc);
+            launch_batch_mats(m, kind, ang, h->sigma, h->noise_seed, h->gcount, B, t);
+            if ((rc = after_launch(m, "batch matrices"))) return lift(h, R, rc);
+            tabs.push_back(t);
+        }
+        h->gcount++;
+        const double2 X[4] = {make_double2(0, 0), make_double2(1, 0), make_double2(1, 0), make_double2(0, 0)};
+        return lift(h, R, apply_gate(R, cmask, cvals, q, X, &tabs));
+    }
     double2 U[4];
     angle_matrix(h, kind, ang, h->gcount, U);
     h->gcount++;
@@ -1025,6 +1082,7 @@ int qsim_grover(qsim_t *h, uint64_t mark, int iters, double *trace)
     if (h->n < 64 && mark >> h->n) return fail(h, QSIM_ERANGE, "mark >= 2^n");
     if (iters < 0) return fail(h, QSIM_EINVAL, "iters < 0");
     if (h->world > 1) return fail(h, QSIM_EINVAL, "qsim_grover runs on a single-GPU handle");
+    if (h->batch_b) return fail(h, QSIM_EINVAL, "qsim_grover on a batched handle (use gates)");
     const Ranks R = ranks_of(h);
     if (int rc = dist_canonicalize(R)) return rc;
     double *d_trace = nullptr;
@@ -1138,6 +1196,57 @@ int qsim_inject_errors(qsim_t *h, uint64_t seed, const qsim_noise_t *model, qsim
     if (!(model->p >= 0.0 && model->p <= 1.0)) return fail(h, QSIM_EINVAL, "p must be in [0, 1]");
     const Ranks R = ranks_of(h);
     int count = 0;
+    if (h->batch_b > 0) {
+        // batched trajectories (R33): trajectory t draws from seed + t; the
+        // Paulis of one qubit become one per-trajectory table gate (identity
+        // where no event); events in qubit order, then trajectory order
+        const int b = h->batch_b;
+        const uint64_t B = 1ull << b;
+        if (model->qubit_mask & ((1ull << b) - 1))
+            return fail(h, QSIM_EINVAL, "Pauli injection on trajectory-index qubits");
+        std::vector<double2> tab(4 * B);
+        const double p = model->p;
+        for (int q = b; q < h->n; ++q) {
+            if (!((model->qubit_mask >> q) & 1)) continue;
+            bool any = false;
+            for (uint64_t t = 0; t < B; ++t) {
+                // the register's own qubit index: trajectory t is the single-register circuit (R33)
+                const u64x2 d = draw(seed + t, QSIM_TAG_PAULI, model->epoch, (uint32_t)(q - b));
+                const double u = u01(d.a);
+                const int which = u < p / 3.0 ? 1 : u < 2.0 * p / 3.0 ? 2 : u < p ? 3 : 0;
+                double2 *P = &tab[4 * t];
+                if (which == 1) { P[0] = make_double2(0, 0); P[1] = make_double2(1, 0); P[2] = make_double2(1, 0); P[3] = make_double2(0, 0); }
+                else if (which == 2) { P[0] = make_double2(0, 0); P[1] = make_double2(0, -1); P[2] = make_double2(0, 1); P[3] = make_double2(0, 0); }
+                else if (which == 3) { P[0] = make_double2(1, 0); P[1] = make_double2(0, 0); P[2] = make_double2(0, 0); P[3] = make_double2(-1, 0); }
+                else { P[0] = make_double2(1, 0); P[1] = make_double2(0, 0); P[2] = make_double2(0, 0); P[3] = make_double2(1, 0); }
+                if (!which) continue;
+                any = true;
+                if (ev && count < cap) {
+                    ev[count].epoch = model->epoch;
+                    ev[count].qubit = q;
+                    ev[count].pauli = which;
+                    ev[count].traj = t;
+                }
+                ++count;
+            }
+            if (!any) continue;
+            std::vector<const double2 *> tabs;
+            for (Handle *m : R) {
+                int rc;
+                double2 *dt = batch_table(m, B, rc);
+                if (!dt) return lift(h, R, rc);
+                // pageable source: consumed before the call returns
+                if ((rc = check_cuda(m, cudaMemcpyAsync(dt, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice, m->stream), "pauli table")))
+                    return lift(h, R, rc);
+                tabs.push_back(dt);
+            }
+            const double2 X[4] = {make_double2(0, 0), make_double2(1, 0), make_double2(1, 0), make_double2(0, 0)};
+            if (int rc = apply_gate(R, 0, 0, q, X, &tabs)) return lift(h, R, rc);
+        }
+        if (nev) *nev = count;
+        if (ev && count > cap) return fail(h, QSIM_ERANGE, "event buffer too small");
+        return QSIM_OK;
+    }
     for (int q = 0; q < h->n; ++q) {
         if (!((model->qubit_mask >> q) & 1)) continue;
         const u64x2 d = draw(seed, QSIM_TAG_PAULI, model->epoch, (uint32_t)q);
@@ -1154,12 +1263,84 @@ int qsim_inject_errors(qsim_t *h, uint64_t seed, const qsim_noise_t *model, qsim
             ev[count].epoch = model->epoch;
             ev[count].qubit = q;
             ev[count].pauli = which;
+            ev[count].traj = 0;
         }
         ++count;
     }
     if (nev) *nev = count;
     if (ev && count > cap) return fail(h, QSIM_ERANGE, "event buffer too small");
     return QSIM_OK;
+}
+
+// ----------------------------------------------------------------- batched trajectories
+int qsim_set_batch(qsim_t *h, int b)
+{
+    QS_CHECK_HANDLE(h);
+    if (b < 0 || b > 24 || b >= h->n) return fail(h, QSIM_ERANGE, "batch bits outside [0, min(n, 25))");
+    if (b > 0 && b < h->kglob) return fail(h, QSIM_EINVAL, "the trajectory index must cover the rank bits");
+    if (b > 0 && h->n - b < 9) return fail(h, QSIM_ERANGE, "a batched register needs >= 9 qubits");
+    const Ranks R = ranks_of(h);
+    if (int rc = flush_all(R)) return lift(h, R, rc);
+    h->batch_b = b;
+    for (Handle *m : R) m->batch_b = b;
+    return QSIM_OK;
+}
+
+int qsim_batch_set_state(qsim_t *h, const qsim_c128 *reg)
+{
+    QS_CHECK_HANDLE(h);
+    if (!reg) return QSIM_EINVAL;
+    if (!h->batch_b) return fail(h, QSIM_EINVAL, "not a batched handle (qsim_set_batch)");
+    const Ranks R = ranks_of(h);
+    if (int rc = flush_all(R)) return lift(h, R, rc);
+    const int r = h->n - h->batch_b;
+    const double scale = 1.0 / std::sqrt((double)(1ull << h->batch_b));
+    for (Handle *m : R) {
+        for (int q = 0; q < m->n; ++q) m->pos[q] = m->n - 1 - q;   // the whole state is overwritten
+        double2 *src = nullptr;
+        int rc = check_cuda(m, cudaMalloc(&src, sizeof(double2) << r), "batch register buffer");
+        if (!rc) rc = check_cuda(m, cudaMemcpyAsync(src, reg, sizeof(double2) << r, cudaMemcpyHostToDevice, m->stream), "batch set state");
+        if (!rc) {
+            launch_batch_broadcast(m, src, r, scale);
+            rc = after_launch(m, "batch broadcast");
+        }
+        if (!rc) rc = check_cuda(m, cudaStreamSynchronize(m->stream), "batch set state");
+        if (src) cudaFree(src);
+        if (rc) return lift(h, R, rc);
+    }
+    return QSIM_OK;
+}
+
+int qsim_batch_overlap(qsim_t *h, const qsim_c128 *ref, qsim_c128 *out)
+{
+    QS_CHECK_HANDLE(h);
+    if (!ref || !out) return QSIM_EINVAL;
+    if (!h->batch_b) return fail(h, QSIM_EINVAL, "not a batched handle (qsim_set_batch)");
+    const Ranks R = ranks_of(h);
+    if (int rc = dist_canonicalize(R)) return lift(h, R, rc);
+    const int r = h->n - h->batch_b;
+    const uint64_t B = 1ull << h->batch_b;
+    std::vector<std::vector<double>> parts(R.size(), std::vector<double>(2 * B, 0.0));
+    for (size_t i = 0; i < R.size(); ++i) {
+        Handle *m = R[i];
+        const uint64_t nt = m->local_dim() >> r;
+        const uint64_t t0 = ((uint64_t)m->rank << m->nl) >> r;   // canonical: shard = a block of trajectories
+        double2 *src = nullptr;
+        double *d_out = nullptr;
+        int rc = check_cuda(m, cudaMalloc(&src, sizeof(double2) << r), "overlap buffer");
+        if (!rc) rc = check_cuda(m, cudaMalloc(&d_out, 2 * nt * sizeof(double)), "overlap buffer");
+        if (!rc) rc = check_cuda(m, cudaMemcpyAsync(src, ref, sizeof(double2) << r, cudaMemcpyHostToDevice, m->stream), "overlap");
+        if (!rc) {
+            launch_batch_overlap(m, src, r, std::sqrt((double)B), d_out);
+            rc = after_launch(m, "batch overlap");
+        }
+        if (!rc) rc = check_cuda(m, cudaMemcpyAsync(parts[i].data() + 2 * t0, d_out, 2 * nt * sizeof(double), cudaMemcpyDeviceToHost, m->stream), "overlap");
+        if (!rc) rc = check_cuda(m, cudaStreamSynchronize(m->stream), "overlap");
+        if (src) cudaFree(src);
+        if (d_out) cudaFree(d_out);
+        if (rc) return lift(h, R, rc);
+    }
+    return lift(h, R, dist_sum_host(R, parts, reinterpret_cast<double *>(out), 2 * B));
 }
 
 // ----------------------------------------------------------------- read-out

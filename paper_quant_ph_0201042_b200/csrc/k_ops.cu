@@ -94,7 +94,7 @@ void launch_ops_pass(Handle *h, const OpsLaunch &L)
     double cost = 0;
     for (int i = 0; i < P.nops; ++i) {
         const GOp &g = L.ops[i];
-        double c = (g.kind == GOP_DENSE || g.kind == GOP_DENSE2) ? 1.0 : 0.5;
+        double c = (g.kind == GOP_DENSE || g.kind == GOP_DENSE2 || g.kind == GOP_DENSET) ? 1.0 : 0.5;
         if (g.fm) c *= 0.5;
         cost += c;
     }

@@ -123,11 +123,24 @@ __device__ __forceinline__ void diag_any(double2 (&v)[NS5], double2 d0, double2 
 
 // One op on the 32 register slots of a thread (thread part tpart of the tile
 // index, tile id T).  Every field of op is warp-uniform.
-__device__ __forceinline__ void apply_op(double2 (&v)[NS5], const GOp &op, uint64_t T, uint32_t tpart)
+__device__ __forceinline__ void apply_op(double2 (&v)[NS5], const GOp &op, uint64_t T, uint32_t tpart, uint32_t traj)
 {
     if ((T & op.fm) != op.fv) return;           // fixed-bit controls (uniform)
     if ((tpart & op.tm) != op.tv) return;       // thread-part controls
     const uint32_t kind = op.kind;
+    if (kind == GOP_DENSET) {
+        // this tile's trajectory matrix (one uniform 64-byte load, L1-cached)
+        const double2 *m = op.tab + 4 * (uint64_t)traj;
+        const double2 u0 = m[0], u1 = m[1], u2 = m[2], u3 = m[3];
+        switch (op.rb) {
+        case 0: dense_any<0>(v, u0, u1, u2, u3, op.wm, op.wv); break;
+        case 1: dense_any<1>(v, u0, u1, u2, u3, op.wm, op.wv); break;
+        case 2: dense_any<2>(v, u0, u1, u2, u3, op.wm, op.wv); break;
+        case 3: dense_any<3>(v, u0, u1, u2, u3, op.wm, op.wv); break;
+        default: dense_any<4>(v, u0, u1, u2, u3, op.wm, op.wv); break;
+        }
+        return;
+    }
     if (kind == GOP_DENSE || kind == GOP_CDENSE) {
         // matrix u[4..7] where the selector (thread bit tsel or tile-id bit fsel) is 1
         const bool s = (tpart & op.tsel) != 0 || (op.fsel != 0xffu && ((T >> op.fsel) & 1u));
@@ -202,6 +215,8 @@ __device__ __forceinline__ void run_segments(double2 (&v)[NS5], const OpsLaunch 
                                              double2 *buf)
 {
     const OpsPass &P = L.P;
+    uint32_t traj = P.bat_rank;
+    for (int i = 0; i < P.nbat; ++i) traj |= (uint32_t)((T >> P.bat_fix[i]) & 1u) << P.bat_sh[i];
     uint32_t prev_stp = 0;
     uint32_t prev_wsw[RB5] = {0, 0, 0, 0, 0};
     for (int s = 0; s < P.nseg; ++s) {
@@ -231,7 +246,7 @@ __device__ __forceinline__ void run_segments(double2 (&v)[NS5], const OpsLaunch 
                 v[k] = buf[o];
             }
         }
-        for (int i = sg.op_begin; i < sg.op_end; ++i) apply_op(v, L.ops[i], T, tpart);
+        for (int i = sg.op_begin; i < sg.op_end; ++i) apply_op(v, L.ops[i], T, tpart, traj);
         prev_stp = stp;
 #pragma unroll
         for (int b = 0; b < RB5; ++b) prev_wsw[b] = wsw[b];

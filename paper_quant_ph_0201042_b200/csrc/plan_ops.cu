@@ -49,6 +49,7 @@ struct POp {
     int cs;                 // choice form: position selecting m1 (m0 where it is 0); -1: none
     double2 m0[4], m1[4];   // m1 == m0 when cs < 0
     uint64_t nmask, dmask;  // positions acted on non-diagonally / diagonally
+    const double2 *tab;     // batched handle: per-trajectory matrices (never merged)
     bool dead;
 };
 
@@ -84,7 +85,8 @@ POp from_queue(const QOp &q)
 {
     POp p;
     std::memset(&p, 0, sizeof p);
-    p.dense = !q.diag;
+    p.dense = !q.diag || q.tab;
+    p.tab = q.tab;
     p.tpos = q.tpos;
     p.cmask = q.cmask;
     p.cval = q.cval;
@@ -129,7 +131,7 @@ bool choice_form(const POp &p, const std::vector<char> &in_win, int &cs, double2
 // Merge B (applied after A, commuting with everything in between) into A.
 bool try_merge(POp &A, const POp &B, const std::vector<char> &in_win)
 {
-    if (A.tpos < 0 || A.tpos != B.tpos || !in_win[A.tpos]) return false;
+    if (A.tpos < 0 || A.tpos != B.tpos || !in_win[A.tpos] || A.tab || B.tab) return false;
     int ca, cb;
     double2 a0[4], a1[4], b0[4], b1[4];
     if (!choice_form(A, in_win, ca, a0, a1) || !choice_form(B, in_win, cb, b0, b1)) return false;
@@ -302,12 +304,25 @@ int launch_check(Handle *h, const char *what)
 
 int flush_queue(Handle *h)
 {
-    if (h->queue.empty()) return QSIM_OK;
+    if (h->queue.empty()) {
+        h->tabs_used = 0;
+        return QSIM_OK;
+    }
     std::vector<QOp> rem;
     rem.swap(h->queue);
     const int nl = h->nl;
-    const int tbits = std::min(kTileMaxBits, nl);
-    const int amax = nl <= kTileMaxBits ? nl : kTileMaxBits - 3;
+    // batched handle: trajectory-index positions are never tile bits (a tile
+    // belongs to one trajectory, whose matrices DENSET ops look up)
+    std::vector<char> is_batch(nl, 0);
+    int nbl = 0;
+    for (int q = 0; q < h->batch_b; ++q)
+        if (h->pos[q] < nl) {
+            is_batch[h->pos[q]] = 1;
+            ++nbl;
+        }
+    const int nreg = nl - nbl;
+    const int tbits = std::min(kTileMaxBits, nreg);
+    const int amax = nreg <= kTileMaxBits ? nreg : kTileMaxBits - 3;
     constexpr size_t kPassCap = 512;   // bounds the planner's work per pass
     static thread_local OpsLaunch L;   // 28 KiB, copied into the launch parameters
     while (!rem.empty()) {
@@ -343,7 +358,7 @@ int flush_queue(Handle *h)
         // touches only the amplitudes the gate changes -- worth it when the
         // masked positions are >= 3 (runs of >= 128 B, so DRAM skips whole
         // sectors).
-        if (take.size() == 1) {
+        if (take.size() == 1 && !take[0].tab) {
             const QOp &q = take[0];
             uint64_t m = q.cmask;
             if (q.diag && q.tpos >= 0 && q.u[0].x == 1.0 && q.u[0].y == 0.0) m |= 1ull << q.tpos;
@@ -359,7 +374,7 @@ int flush_queue(Handle *h)
         std::vector<int> tbit_of(nl, -1);
         for (size_t b = 0; b < act.size(); ++b) tbit_of[act[b]] = (int)b;
         for (int p = 0; p < nl && (int)tile.size() < tbits; ++p)
-            if (tbit_of[p] < 0) {
+            if (tbit_of[p] < 0 && !is_batch[p]) {
                 tbit_of[p] = (int)tile.size();
                 tile.push_back(p);
             }
@@ -373,6 +388,16 @@ int flush_queue(Handle *h)
                 fix_of[p] = P.nfix;
                 P.fin_pos[P.nfix++] = p;
             }
+        for (int q = 0; q < h->batch_b; ++q) {
+            const int p = h->pos[q];
+            const int sh = h->batch_b - 1 - q;   // qubit 0 = MSB of the trajectory index
+            if (p < nl) {
+                P.bat_fix[P.nbat] = fix_of[p];
+                P.bat_sh[P.nbat++] = sh;
+            } else {
+                P.bat_rank |= (uint32_t)(((uint64_t)h->rank >> (p - nl)) & 1u) << sh;
+            }
+        }
 
         // ---- 2. segments, 3. merging
         std::vector<POp> ops;
@@ -413,6 +438,11 @@ int flush_queue(Handle *h)
                     g.u[4 + k] = q.m1[k];
                 }
                 g.fsel = 0xff;
+                if (q.tab) {
+                    g.kind = GOP_DENSET;
+                    g.rb = (uint8_t)win_idx(q.tpos);
+                    g.tab = q.tab;
+                }
                 if (q.cs >= 0 && win_idx(q.cs) >= 0) {
                     // choice form (merged run) selected by a window bit: static slot selection
                     g.rb = (uint8_t)win_idx(q.tpos);
@@ -449,7 +479,9 @@ int flush_queue(Handle *h)
                     enc[s].push_back(g);
                     continue;
                 }
-                if (q.dense) {
+                if (q.tab) {
+                    // DENSET set above; controls below
+                } else if (q.dense) {
                     g.kind = GOP_DENSE;
                     g.rb = (uint8_t)win_idx(q.tpos);
                 } else if (q.tpos < 0) {
@@ -545,6 +577,7 @@ int flush_queue(Handle *h)
             pi = pe;
         }
     }
+    h->tabs_used = 0;   // every queued table is consumed by the launches above (stream order)
     return QSIM_OK;
 }
 

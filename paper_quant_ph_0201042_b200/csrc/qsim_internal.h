@@ -139,9 +139,12 @@ bool launch_tile_pass_tma(Handle *h, const TilePass &tp, const double2 *in, doub
 //           controlled by the same qubit, multiplied together on the host);
 //           DENSE with tsel / fsel is the same choice by a thread-part or a
 //           tile-id bit (one matrix per thread / per tile: no divergence)
+//   DENSET  2x2 on window bit rb with one matrix per trajectory of a batched
+//           handle (batch.cu): tab[4 t .. 4 t + 3], t from the tile id
 // Controls: wm/wv on the 4 window bits (slot index), tm/tv on the other tile
 // bits (thread part), fm/fv on fixed bits (tile id).
-enum { GOP_DENSE = 0, GOP_DIAGW = 1, GOP_DIAGT = 2, GOP_DIAGF = 3, GOP_PHASE = 4, GOP_CDENSE = 5, GOP_DENSE2 = 6 };
+enum { GOP_DENSE = 0, GOP_DIAGW = 1, GOP_DIAGT = 2, GOP_DIAGF = 3, GOP_PHASE = 4, GOP_CDENSE = 5, GOP_DENSE2 = 6,
+       GOP_DENSET = 7 };
 struct GOp {
     uint8_t kind, rb, wm, wv;
     uint8_t cs, cv;
@@ -153,6 +156,7 @@ struct GOp {
     uint32_t tsel;     // DENSE: thread-part bit selecting u[4..7] (0: none)
     uint32_t pad2_;
     uint64_t fm, fv;   // controls on fixed bits (tile-id mask / values)
+    const double2 *tab;   // DENSET: per-trajectory matrices (device memory)
     double2 u[8];      // dense U (u11 u12 u21 u22) or diag(u[0], u[3]); DENSE2: two matrices
 };
 constexpr int kMaxSegs = 48;
@@ -168,12 +172,16 @@ struct OpsPass {
     int nfix;
     int fin_pos[kMaxFixedBits];
     int nops, nseg;
+    // trajectory index of a tile (batched handles): t = t_rank | sum_i bit(T, bat_fix[i]) << bat_sh[i]
+    int nbat;
+    int bat_fix[24], bat_sh[24];
+    uint32_t bat_rank;
     OpsSeg seg[kMaxSegs];
 };
 // One launch: the pass geometry and its op list travel as one __grid_constant__
 // kernel parameter (<= 32 KiB), so every op read is a uniform constant-bank load
 // (no shared-memory traffic, no per-handle device buffer).
-constexpr int kOpsParam = 140;
+constexpr int kOpsParam = 136;
 struct OpsLaunch {
     OpsPass P;
     GOp ops[kOpsParam];
@@ -188,6 +196,7 @@ struct QOp {
     int tpos;          // target local position; -1 for a constant phase (diag only)
     uint64_t cmask, cval;   // controls on local positions
     double2 u[4];
+    const double2 *tab = nullptr;   // batched handle: one matrix per trajectory (then u is unused)
 };
 
 // --------------------------------------------------------------- handle
@@ -231,6 +240,10 @@ struct Handle {
     // gate queue (fused into k_ops passes at the next flush)
     std::vector<QOp> queue;
     int fuse = 1;
+    // batched trajectories (batch.cu, R33): qubits [0, batch_b) index them
+    int batch_b = 0;
+    double2 *d_tabs = nullptr;   // per-trajectory matrix tables of queued gates (reset at flush)
+    size_t tabs_cap = 0, tabs_used = 0;   // in double2
     // in-process rank group (qsim_create_group): the group handle owns the
     // member handles (one shard each); members point back at the group
     std::vector<Handle *> members;
@@ -268,6 +281,11 @@ int dist_canonicalize(const Ranks &R);                               // pos[q] =
 // per-rank host partials -> the sum over all ranks of the world, in rank order
 // (parts[i] belongs to R[i]); out may alias parts[0]
 int dist_sum_host(const Ranks &R, const std::vector<std::vector<double>> &parts, double *out, size_t count);
+// batched trajectories (batch.cu)
+void launch_batch_mats(Handle *h, int kind, const double *ang, double sigma, uint64_t seed, uint64_t g, uint64_t B,
+                       double2 *out);
+void launch_batch_broadcast(Handle *h, const double2 *src, int r, double scale);
+void launch_batch_overlap(Handle *h, const double2 *ref, int r, double scale, double *d_out);
 // one queued gate with the unfused streaming kernels (k_gates.cu)
 void run_gate_unfused(Handle *h, const QOp &op);
 // run every queued gate (fused passes); called before anything that reads or moves data

@@ -61,7 +61,7 @@ class qsim_noise_t(C.Structure):
 
 
 class qsim_event_t(C.Structure):
-    _fields_ = [("epoch", C.c_uint64), ("qubit", C.c_int32), ("pauli", C.c_int32)]
+    _fields_ = [("epoch", C.c_uint64), ("qubit", C.c_int32), ("pauli", C.c_int32), ("traj", C.c_uint64)]
 
 
 _H = C.c_void_p
@@ -100,6 +100,9 @@ _sig("qsim_fft", _i32, _H, _i32, _i32, _i32)
 _sig("qsim_aqft", _i32, _H, _i32, _i32, _i32, _i32)
 _sig("qsim_measure_range", _i32, _H, _i32, _i32, _f64, _i32, C.POINTER(_u64))
 _sig("qsim_inner", _i32, _H, _H, _p)
+_sig("qsim_set_batch", _i32, _H, _i32)
+_sig("qsim_batch_set_state", _i32, _H, _p)
+_sig("qsim_batch_overlap", _i32, _H, _p, _p)
 _sig("qsim_phase_flip", _i32, _H, _u64)
 _sig("qsim_grover", _i32, _H, _u64, _i32, _p)
 _sig("qsim_apply_perm", _i32, _H, C.POINTER(qsim_perm_t))
@@ -294,12 +297,33 @@ def qsim_apply_perm(h, kind: int, lo: int, m: int, *, elo: int = 0, em: int = 0,
     del keep
 
 
-def qsim_inject_errors(h, seed: int, p: float, qubit_mask: int, epoch: int, cap: int = 256):
+def qsim_inject_errors(h, seed: int, p: float, qubit_mask: int, epoch: int, cap: int = 256, traj: bool = False):
+    """Events as (epoch, qubit, pauli) tuples, or (epoch, qubit, pauli, traj)
+    with traj=True (batched handles)."""
     model = qsim_noise_t(p, qubit_mask, epoch)
     ev = (qsim_event_t * max(cap, 1))()
     nev = _i32(0)
     _chk(h, lib.qsim_inject_errors(h, seed, C.byref(model), ev, cap, C.byref(nev)))
+    if traj:
+        return [(int(ev[i].epoch), int(ev[i].qubit), int(ev[i].pauli), int(ev[i].traj)) for i in range(nev.value)]
     return [(int(ev[i].epoch), int(ev[i].qubit), int(ev[i].pauli)) for i in range(nev.value)]
+
+
+# ------------------------------------------------------------------ batched trajectories
+def qsim_set_batch(h, b: int) -> None:
+    _chk(h, lib.qsim_set_batch(h, b))
+
+
+def qsim_batch_set_state(h, reg) -> None:
+    reg = np.ascontiguousarray(np.asarray(reg, dtype=np.complex128))
+    _chk(h, lib.qsim_batch_set_state(h, reg.ctypes.data))
+
+
+def qsim_batch_overlap(h, ref, ntraj: int) -> np.ndarray:
+    ref = np.ascontiguousarray(np.asarray(ref, dtype=np.complex128))
+    out = np.zeros(ntraj, np.complex128)
+    _chk(h, lib.qsim_batch_overlap(h, ref.ctypes.data, out.ctypes.data))
+    return out
 
 
 # ------------------------------------------------------------------ read-out

@@ -127,3 +127,126 @@ def run_cfg4(h, n: int = 32, layers: int = 20, seed: int = 5, sigma: float = 1e-
         events += Q.qsim_inject_errors(h, seed, p, allq, layer, cap=4 * n)
     Q.qsim_set_gate_noise(h, 0, 0.0)
     return events
+
+
+# ---------------------------------------------------------------------------
+# Row f2: the paper's noise experiments as batched trajectories (R33-R36).
+# The handle holds b + (register) qubits; qubits [0, b) index the 2^b
+# trajectories, trajectory t draws from seed + t.  Averages over trajectories
+# are marginals of the batched handle (qsim_probs over the register).
+
+def run_ht_batch(h, n: int, b: int, k: int, seed: int, sigma: float, p: float):
+    """HT experiment (R34): |0..0>, k times (noisy H on every
+    qubit, then the depolarizing channel on every qubit, epoch = application).
+    Returns (average |<0|psi_t>|^2 over the 2^b trajectories, events)."""
+    Q.qsim_set_batch(h, b)
+    reg = [0j] * (1 << n)
+    reg[0] = 1.0
+    Q.qsim_batch_set_state(h, reg)
+    Q.qsim_set_gate_noise(h, seed, sigma)
+    Q.qsim_set_gate_counter(h, 0)
+    regmask = ((1 << n) - 1) << b
+    events = []
+    for i in range(k):
+        for q in range(n):
+            Q.qsim_apply_angles(h, Q.QSIM_GATE_RP, [math.pi / 4, math.pi], 0, 0, b + q)
+        events += Q.qsim_inject_errors(h, seed, p, regmask, i, cap=n << b, traj=True)
+    p0 = float(Q.qsim_probs(h, b, n)[0])
+    Q.qsim_set_gate_noise(h, 0, 0.0)
+    return p0, events
+
+
+def run_grover_batch(h, n: int, b: int, mark: int, iters: int, seed: int, sigma: float, p: float):
+    """Grover experiment (R35): register qubits [b, b+n),
+    ancilla b+n (the LSB) in |->; noisy H_n and noisy NOT in V_f (all register
+    qubits control it); depolarizing channel on the register per G-iteration.
+    Returns the trajectory-averaged P(register = mark) after each iteration."""
+    Q.qsim_set_batch(h, b)
+    r = math.sqrt(0.5)
+    reg = [0j] * (1 << (n + 1))
+    reg[0], reg[1] = r, -r
+    Q.qsim_batch_set_state(h, reg)
+    Q.qsim_set_gate_noise(h, seed, sigma)
+    Q.qsim_set_gate_counter(h, 0)
+    regq = range(b, b + n)
+    cmask = sum(1 << q for q in regq)
+    vk = sum(((mark >> (n - 1 - i)) & 1) << (b + i) for i in range(n))
+    anc = b + n
+    hang, xang = [math.pi / 4, math.pi], [math.pi / 2, math.pi]
+    for q in regq:
+        Q.qsim_apply_angles(h, Q.QSIM_GATE_RP, hang, 0, 0, q)
+    trace = []
+    for t in range(iters):
+        Q.qsim_apply_angles(h, Q.QSIM_GATE_RP, xang, cmask, vk, anc)
+        for q in regq:
+            Q.qsim_apply_angles(h, Q.QSIM_GATE_RP, hang, 0, 0, q)
+        Q.qsim_apply_angles(h, Q.QSIM_GATE_RP, xang, cmask, 0, anc)
+        for q in regq:
+            Q.qsim_apply_angles(h, Q.QSIM_GATE_RP, hang, 0, 0, q)
+        Q.qsim_inject_errors(h, seed, p, cmask, t, cap=n << b, traj=True)
+        trace.append(float(Q.qsim_probs(h, b, n)[mark]))
+    Q.qsim_set_gate_noise(h, 0, 0.0)
+    return trace
+
+
+def qft_decoherent_gates(h, lo: int, m: int, seed: int, sigma: float, p: float, inverse: bool = False,
+                         ntraj: int = 1):
+    """The QFT circuit on [lo, lo+m) gate by gate with its angle noise and the
+    depolarizing channel on [lo, lo+m) after every R_d (PAPER.md:1053-1160,
+    R36); the gate counter is the caller's.  Returns the events."""
+    sg = -1.0 if inverse else 1.0
+    r = math.sqrt(0.5)
+    H = [[r, r], [r, -r]]
+    qmask = ((1 << m) - 1) << lo
+    epoch = 0
+    events = []
+    for j in range(m):
+        if sigma > 0:
+            Q.qsim_apply_angles(h, Q.QSIM_GATE_RP, [math.pi / 4, math.pi], 0, 0, lo + j)
+        else:
+            Q.qsim_apply_1q(h, lo + j, H)
+        for k in range(j + 1, m):
+            phi = sg * math.pi / 2.0 ** (k - j)
+            cm = 1 << (lo + k)
+            if sigma > 0:
+                Q.qsim_apply_angles(h, Q.QSIM_GATE_P1, [phi], cm, cm, lo + j)
+            else:
+                Q.qsim_apply_ctrl(h, cm, cm, lo + j, [[1, 0], [0, complex(math.cos(phi), math.sin(phi))]])
+            events += Q.qsim_inject_errors(h, seed, p, qmask, epoch, cap=m * ntraj, traj=True)
+            epoch += 1
+    for j in range(m // 2):
+        Q.qsim_swap(h, lo + j, lo + m - 1 - j)
+    return events
+
+
+def shor_register_state(m: int, x: int, N: int, v: int):
+    """The semantic-mode exponent register of Shor step 3
+    prepared by the library on its own m-qubit handle, read back to the host."""
+    g = Q.qsim_create(m)
+    try:
+        Q.qsim_shor_semantic_state(g, x, N, v)
+        return Q.qsim_get_state(g, 0, 1 << m)
+    finally:
+        Q.qsim_destroy(g)
+
+
+def run_qft_fidelity_batch(h, m: int, b: int, x: int, N: int, v: int, seed: int, sigma: float, p: float):
+    """QFT-16 experiment of PAPER.md:1124-1160 (Table 7): every trajectory starts
+    in the Shor register state, runs the noisy / decoherent QFT, and its fidelity
+    |<QFT psi | psi_t>| to the ideal QFT output (library, noiseless) is
+    returned per trajectory."""
+    Q.qsim_set_batch(h, b)
+    reg = shor_register_state(m, x, N, v)
+    g = Q.qsim_create(m)
+    try:
+        Q.qsim_set_state(g, 0, reg)
+        Q.qsim_qft(g, 0, m, False)
+        ideal = Q.qsim_get_state(g, 0, 1 << m)
+    finally:
+        Q.qsim_destroy(g)
+    Q.qsim_batch_set_state(h, reg)
+    Q.qsim_set_gate_noise(h, seed, sigma)
+    Q.qsim_set_gate_counter(h, 0)
+    qft_decoherent_gates(h, b, m, seed, sigma, p, ntraj=1 << b)
+    Q.qsim_set_gate_noise(h, 0, 0.0)
+    return abs(Q.qsim_batch_overlap(h, ideal, 1 << b))
