@@ -568,9 +568,9 @@ int flush_queue(Handle *h)
                 }
                 std::fprintf(stderr,
                              "[qsim plan] nl=%d tile=%d nseg=%d nops=%d dense=%d cdense=%d dense2=%d diagw=%d "
-                             "diagt=%d diagf=%d phase=%d thread-ctrl=%d\n",
+                             "diagt=%d diagf=%d phase=%d denset=%d thread-ctrl=%d\n",
                              nl, tbits, P.nseg, P.nops, cnt[GOP_DENSE], cnt[GOP_CDENSE], cnt[GOP_DENSE2],
-                             cnt[GOP_DIAGW], cnt[GOP_DIAGT], cnt[GOP_DIAGF], cnt[GOP_PHASE], thr);
+                             cnt[GOP_DIAGW], cnt[GOP_DIAGT], cnt[GOP_DIAGF], cnt[GOP_PHASE], cnt[GOP_DENSET], thr);
             }
             launch_ops_pass(h, L);
             if (int rc = launch_check(h, "fused gate pass")) return rc;
