@@ -183,6 +183,118 @@ __global__ void __launch_bounds__(kPersistThreads) k_grover_persist(double2 *__r
     for (uint32_t i = threadIdx.x; i < chunk; i += blockDim.x) psi[base + i] = st[i];
 }
 
+// Register-resident variant (the default when the state fits): the 2^n
+// amplitudes live in the registers of a co-resident grid (<= 16 per thread),
+// and the per-iteration all-reduce is a flag-tagged slot exchange instead of
+// a grid barrier: every CTA publishes {sum of its amplitudes, alpha_k if it
+// owns k} into its slot of a parity double buffer and then stamps the slot
+// with the iteration tag (st.release); every CTA polls all slots (ld.acquire)
+// and sums them in the same fixed order, so all CTAs form the identical mean
+// with one L2 round trip and no atomics.  Parity buffers make a slot safe to
+// overwrite: a CTA can only publish iteration t+2 after every CTA has
+// published t+1, i.e. finished reading t.
+template <int A>
+__global__ void __launch_bounds__(kPersistThreads, 1) k_grover_regs(double2 *__restrict__ psi, uint64_t N, uint64_t k,
+                                                                   int iters, double *__restrict__ trace,
+                                                                   double4 *__restrict__ slots,
+                                                                   unsigned *__restrict__ tags)
+{
+    __shared__ double2 sh[32];
+    __shared__ double4 s_tot;
+    const unsigned nb = gridDim.x;
+    const uint64_t chunk = (uint64_t)A * blockDim.x;
+    const uint64_t base = (uint64_t)blockIdx.x * chunk;
+    double2 v[A];
+#pragma unroll
+    for (int j = 0; j < A; ++j) v[j] = psi[base + threadIdx.x + (uint64_t)j * blockDim.x];
+    // the owner of k: thread / register slot (static index via the unrolled loops)
+    const bool own_k = k >= base && k < base + chunk;
+    const uint32_t kl = (uint32_t)(k - base);
+    const bool own_t = own_k && (kl % blockDim.x) == threadIdx.x;
+    const int kj = (int)(kl / blockDim.x);
+    const double inv = 1.0 / (double)N;
+
+    auto exchange = [&](int it) {   // publish the partial of iteration `it` (-1: initial state), gather the total
+        double2 acc = make_double2(0.0, 0.0), ak = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < A; ++j) {
+            acc.x += v[j].x;
+            acc.y += v[j].y;
+            if (own_t && j == kj) ak = v[j];
+        }
+        acc = warp_sum2(acc);
+        ak = warp_sum2(ak);
+        const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+        if (l == 0) {
+            sh[w] = acc;
+        }
+        __shared__ double2 sak[32];
+        if (l == 0) sak[w] = ak;
+        __syncthreads();
+        const unsigned p = (unsigned)(it + 1) & 1u;
+        if (w == 0) {
+            // CTA partial: lanes < #warps hold the warp sums, fixed shuffle tree
+            const int nw = (int)(blockDim.x >> 5);
+            double2 t = l < nw ? sh[l] : make_double2(0.0, 0.0);
+            double2 a = l < nw ? sak[l] : make_double2(0.0, 0.0);
+            t = warp_sum2(t);
+            a = warp_sum2(a);
+            if (l == 0) {
+                slots[(size_t)p * nb + blockIdx.x] = make_double4(t.x, t.y, a.x, a.y);
+                // arrive (release: the slot is visible before the count), then
+                // wait until every CTA of this round has arrived
+                const unsigned target = nb * (unsigned)(it + 2);
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(tags) : "memory");
+                unsigned got;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(got) : "l"(tags) : "memory");
+                } while (got < target);
+            }
+        }
+        __syncthreads();
+        // gather: thread b < nb reads slot b (one round trip), fixed-order trees
+        double4 q = make_double4(0.0, 0.0, 0.0, 0.0);
+        if (threadIdx.x < nb) {
+            const double2 *sp = reinterpret_cast<const double2 *>(slots + (size_t)p * nb + threadIdx.x);
+            const double2 q0 = __ldcg(sp), q1 = __ldcg(sp + 1);
+            q = make_double4(q0.x, q0.y, q1.x, q1.y);
+        }
+        const double2 s1 = warp_sum2(make_double2(q.x, q.y));
+        const double2 s2 = warp_sum2(make_double2(q.z, q.w));
+        if (l == 0) {
+            sh[w] = s1;
+            sak[w] = s2;
+        }
+        __syncthreads();
+        if (w == 0) {
+            const int ng = (int)((nb + 31) >> 5);
+            double2 t = l < ng ? sh[l] : make_double2(0.0, 0.0);
+            double2 a = l < ng ? sak[l] : make_double2(0.0, 0.0);
+            t = warp_sum2(t);
+            a = warp_sum2(a);
+            if (l == 0) s_tot = make_double4(t.x, t.y, a.x, a.y);
+        }
+        __syncthreads();
+    };
+
+    exchange(-1);
+    for (int t = 0; t < iters; ++t) {
+        const double4 T = s_tot;   // sum S and alpha_k of the previous iteration
+        // after V_{f_k} the sum is S - 2 alpha_k; 2|s><s| - I maps a -> 2 mean - a
+        const double m2x = 2.0 * (T.x - 2.0 * T.z) * inv, m2y = 2.0 * (T.y - 2.0 * T.w) * inv;
+#pragma unroll
+        for (int j = 0; j < A; ++j) {
+            double2 a = v[j];
+            if (own_t && j == kj) { a.x = -a.x; a.y = -a.y; }   // V_{f_k}
+            v[j] = make_double2(m2x - a.x, m2y - a.y);
+        }
+        exchange(t);
+        if (blockIdx.x == 0 && threadIdx.x == 0 && trace) trace[t] = fma(s_tot.z, s_tot.z, s_tot.w * s_tot.w);
+    }
+#pragma unroll
+    for (int j = 0; j < A; ++j) psi[base + threadIdx.x + (uint64_t)j * blockDim.x] = v[j];
+}
+
 }  // namespace
 
 static bool try_persist(Handle *h, uint64_t mark, int iters, double *d_trace)
@@ -214,10 +326,41 @@ static bool try_persist(Handle *h, uint64_t mark, int iters, double *d_trace)
     return true;
 }
 
+static bool try_regs(Handle *h, uint64_t mark, int iters, double *d_trace)
+{
+    const uint64_t N = h->local_dim();
+    uint64_t blocks = 1;
+    while (blocks * 2 <= (uint64_t)h->num_sms && blocks * 2 <= N / kPersistThreads) blocks *= 2;
+    const uint64_t per = N / (blocks * kPersistThreads);
+    if (per < 1 || per > 16 || N % (blocks * kPersistThreads)) return false;
+    int per_sm = 0;
+    void *fn = per <= 1 ? (void *)k_grover_regs<1> : per <= 2 ? (void *)k_grover_regs<2> : per <= 4 ? (void *)k_grover_regs<4>
+             : per <= 8 ? (void *)k_grover_regs<8> : (void *)k_grover_regs<16>;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPersistThreads, 0);
+    if (per_sm < 1 || blocks > (uint64_t)per_sm * h->num_sms) return false;
+    // slots: 2 x blocks double4 (parity double buffer); tags[0]: the arrival counter
+    const size_t nd = 8 * blocks + blocks + 16;
+    ensure_red(h, 8 + nd);
+    double4 *slots = reinterpret_cast<double4 *>(h->d_red + 8);
+    unsigned *tags = reinterpret_cast<unsigned *>(h->d_red + 8 + 8 * blocks);
+    cudaMemsetAsync(tags, 0, 2 * blocks * sizeof(unsigned), h->stream);
+    void *args[] = {(void *)&h->psi, (void *)&N, (void *)&mark, (void *)&iters, (void *)&d_trace, (void *)&slots,
+                    (void *)&tags};
+    prof_begin(h);
+    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)blocks), dim3(kPersistThreads), args, 0, h->stream);
+    prof_end(h, "k_grover_regs", N * 32);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return true;
+}
+
 void launch_grover(Handle *h, uint64_t mark_local, int mark_rank, int iters, double *d_trace)
 {
     (void)mark_rank;
     const uint64_t N = h->local_dim();
+    if (!getenv("QSIM_NO_GROVER_REGS") && N >= 4096 && try_regs(h, mark_local, iters, d_trace)) return;
     // whole state in registers: <= 16 amplitudes per thread over the resident grid
     if (!getenv("QSIM_NO_GROVER_PERSIST") && N >= 4096 && try_persist(h, mark_local, iters, d_trace)) return;
     unsigned blocks = (unsigned)h->num_sms * 4;
