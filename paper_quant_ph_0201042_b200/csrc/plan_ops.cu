@@ -322,7 +322,8 @@ int flush_queue(Handle *h)
         }
     const int nreg = nl - nbl;
     const int tbits = std::min(kTileMaxBits, nreg);
-    const int amax = nreg <= kTileMaxBits ? nreg : kTileMaxBits - 3;
+    static const int npassive = std::getenv("QSIM_OPS_PASSIVE") ? std::atoi(std::getenv("QSIM_OPS_PASSIVE")) : 3;
+    const int amax = nreg <= kTileMaxBits ? nreg : kTileMaxBits - npassive;
     constexpr size_t kPassCap = 512;   // bounds the planner's work per pass
     static thread_local OpsLaunch L;   // 28 KiB, copied into the launch parameters
     while (!rem.empty()) {
