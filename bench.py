@@ -242,7 +242,9 @@ def main():
     peak, peak_kind, _ = load_peaks()
 
     # dominant kernel roofline (algorithmic bytes per launch / mean launch time)
-    dom = max(prof.items(), key=lambda kv: kv[1]["ms"]) if prof else None
+    ours = {k: v for k, v in prof.items() if not k.startswith("nccl_")}
+    comm = {k: v for k, v in prof.items() if k.startswith("nccl_")}
+    dom = max(ours.items(), key=lambda kv: kv[1]["ms"]) if ours else None
     roof = None
     if dom:
         name, d = dom
@@ -258,6 +260,21 @@ def main():
                 "bytes_per_launch": bytes_per_launch, "ms_per_launch": per_launch_ms,
                 "launches_per_step": d["launches"] / args.steps,
                 "share_of_step": d["ms"] / (ms * args.steps)}
+
+    # NVLink: shard exchanges of the sharded QFT (rank 0's view; bytes = sent +
+    # received, so per direction = half) against the measured 770 GB/s per
+    # direction per GPU (B200_PROFILING.md; 900 nominal)
+    nvlink = None
+    if comm:
+        cb = sum(v["bytes"] for v in comm.values())
+        cms = sum(v["ms"] for v in comm.values())
+        if cms > 0:
+            ach = cb / 2 / (cms * 1e-3) / 1e9
+            nvlink = {"bound": "nvlink", "achieved": ach, "peak": 770.0, "unit": "GB/s per direction",
+                      "frac": ach / 770.0, "peak_source": "B200_PROFILING.md measured peer copy (900 nominal)",
+                      "bytes_per_step": cb / args.steps, "ms_per_step": cms / args.steps,
+                      "share_of_step": cms / (ms * args.steps),
+                      "ops": {k: v["launches"] for k, v in comm.items()}}
 
     # ---------------- end to end: host buffers through the C-ABI
     shard = 1 << (n - (world.bit_length() - 1))
@@ -299,6 +316,7 @@ def main():
                        "circuit_ms": ms, "effective_frac_of_hbm_peak": value / peak,
                        "norm_after": norm},
             "roofline": roof,
+            "nvlink": nvlink,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

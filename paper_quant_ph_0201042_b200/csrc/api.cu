@@ -99,6 +99,16 @@ void prof_begin(Handle *h)
     cudaEventRecord(h->pending, h->stream);
 }
 
+// communication (NCCL / peer copies): timed like a kernel, not counted as one of ours
+void prof_end_comm(Handle *h, const char *name, uint64_t bytes)
+{
+    if (!h->prof_on || !h->pending) return;
+    cudaEvent_t b = pool_event(h);
+    cudaEventRecord(b, h->stream);
+    h->prof.push_back({name, bytes, h->pending, b});
+    h->pending = nullptr;
+}
+
 void prof_end(Handle *h, const char *name, uint64_t bytes)
 {
     h->launches++;

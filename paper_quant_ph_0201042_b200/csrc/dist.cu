@@ -38,8 +38,13 @@ static int nccl_check(Handle *h, ncclResult_t r, const char *what)
 //   {XCHG, g, -}   : swap global position g with the top local position nl-1
 //                    (rank r exchanges its half with top bit != bit g of r with
 //                    rank r ^ 2^(g-nl))
+//   {A2A, k, -}    : swap all k global positions nl..nl+k-1 with the top k
+//                    local positions nl-k..nl-1 at once: rank r sends its
+//                    block j (top local bits = j) to rank j and receives that
+//                    rank's block r -- one all-to-all of (1 - 2^-k) S per rank
+//                    instead of k pairwise exchanges of S/2 (SURVEY §8(e) ii)
 // and pos[] (logical -> physical) is updated as the steps would move the data.
-enum { STEP_LSWAP = 0, STEP_XCHG = 1 };
+enum { STEP_LSWAP = 0, STEP_XCHG = 1, STEP_A2A = 2 };
 struct Step { int kind, a, b; };
 
 static int qubit_at(const std::vector<int> &pos, int p)
@@ -51,16 +56,42 @@ static int qubit_at(const std::vector<int> &pos, int p)
 
 static void apply_step(std::vector<int> &pos, int nl, const Step &s)
 {
+    if (s.kind == STEP_A2A) {
+        for (int i = 0; i < s.a; ++i) {
+            const int qa = qubit_at(pos, nl - s.a + i), qb = qubit_at(pos, nl + i);
+            std::swap(pos[qa], pos[qb]);
+        }
+        return;
+    }
     const int pa = s.a, pb = s.kind == STEP_LSWAP ? s.b : nl - 1;
     const int qa = qubit_at(pos, pa), qb = qubit_at(pos, pb);
     std::swap(pos[qa], pos[qb]);
 }
 
 static int plan_make_local(int n, int nl, std::vector<int> &pos, const std::vector<int> &need,
-                           std::vector<Step> &steps)
+                           std::vector<Step> &steps, bool allow_a2a = true)
 {
     std::vector<char> needed(n, 0);
     for (int q : need) needed[q] = 1;
+    const int k = n - nl;
+    int nglob = 0;
+    for (int q : need) nglob += pos[q] >= nl;
+    if (allow_a2a && k >= 2 && nglob >= 2 && nl - k >= 0) {
+        // every global qubit local with one all-to-all: first move needed
+        // qubits out of the top k local positions (the victims)
+        for (int p = nl - k; p < nl; ++p) {
+            if (!needed[qubit_at(pos, p)]) continue;
+            int dst = -1;
+            for (int d = nl - k - 1; d >= 0 && dst < 0; --d)
+                if (!needed[qubit_at(pos, d)]) dst = d;
+            if (dst < 0) return QSIM_EINVAL;
+            steps.push_back({STEP_LSWAP, dst, p});
+            apply_step(pos, nl, steps.back());
+        }
+        steps.push_back({STEP_A2A, k, -1});
+        apply_step(pos, nl, steps.back());
+        return QSIM_OK;
+    }
     for (int q : need) {
         const int g = pos[q];
         if (g < nl) continue;
@@ -89,7 +120,7 @@ static int plan_canonical_globals(int n, int nl, std::vector<int> &pos, std::vec
         if (pos[want] >= nl) {
             // bring it local first (it sits on a global position > g, so the
             // positions already placed are not touched)
-            if (int rc = plan_make_local(n, nl, pos, std::vector<int>{want}, steps)) return rc;
+            if (int rc = plan_make_local(n, nl, pos, std::vector<int>{want}, steps, false)) return rc;
         }
         const int p = pos[want];
         if (p != nl - 1) {
@@ -124,10 +155,12 @@ static int exchange_nccl(Handle *h, int g)
     const uint64_t half = h->local_dim() >> 1;
     if (int rc = ensure_scratch(h)) return rc;
     double2 *mine = h->psi + (uint64_t)(1 - b) * half;
+    prof_begin(h);
     if (int rc = nccl_check(h, ncclGroupStart(), "ncclGroupStart")) return rc;
     ncclSend(mine, half * 2, ncclDouble, partner, h->comm, h->stream);
     ncclRecv(h->scratch, half * 2, ncclDouble, partner, h->comm, h->stream);
     if (int rc = nccl_check(h, ncclGroupEnd(), "ncclGroupEnd")) return rc;
+    prof_end_comm(h, "nccl_pair_exchange", half * 32);
     cudaError_t e = cudaMemcpyAsync(mine, h->scratch, half * sizeof(double2), cudaMemcpyDeviceToDevice, h->stream);
     if (e != cudaSuccess) return check_cuda(h, e, "exchange copy");
     return QSIM_OK;
@@ -135,6 +168,64 @@ static int exchange_nccl(Handle *h, int g)
     (void)g;
     return fail(h, QSIM_ENCCL, "built without NCCL");
 #endif
+}
+
+static int alltoall_nccl(Handle *h, int k)
+{
+#ifndef QSIM_NO_NCCL
+    const uint64_t blk = h->local_dim() >> k;
+    if (int rc = ensure_scratch(h)) return rc;
+    prof_begin(h);
+    if (int rc = nccl_check(h, ncclGroupStart(), "ncclGroupStart")) return rc;
+    for (int p = 0; p < h->world; ++p) {
+        if (p == h->rank) continue;
+        ncclSend(h->psi + (uint64_t)p * blk, blk * 2, ncclDouble, p, h->comm, h->stream);
+        ncclRecv(h->scratch + (uint64_t)p * blk, blk * 2, ncclDouble, p, h->comm, h->stream);
+    }
+    if (int rc = nccl_check(h, ncclGroupEnd(), "ncclGroupEnd")) return rc;
+    prof_end_comm(h, "nccl_alltoall", (uint64_t)(h->world - 1) * blk * 32);
+    cudaError_t e = cudaMemcpyAsync(h->scratch + (uint64_t)h->rank * blk, h->psi + (uint64_t)h->rank * blk,
+                                    blk * sizeof(double2), cudaMemcpyDeviceToDevice, h->stream);
+    if (e != cudaSuccess) return check_cuda(h, e, "all-to-all copy");
+    swap_buffers(h);
+    return QSIM_OK;
+#else
+    (void)k;
+    return fail(h, QSIM_ENCCL, "built without NCCL");
+#endif
+}
+
+// In-process group: member r pulls block r of every member p into block p of
+// its scratch shard (peer copies), ordered after every member's pending work;
+// then every member swaps shard and scratch.
+static int alltoall_group(const Ranks &R, int k)
+{
+    const size_t P = R.size();
+    const uint64_t blk = R[0]->local_dim() >> k;
+    for (Handle *m : R)
+        if (int rc = ensure_scratch(m)) return rc;
+    std::vector<cudaEvent_t> pre(P), post(P);
+    for (size_t i = 0; i < P; ++i) {
+        cudaEventCreateWithFlags(&pre[i], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&post[i], cudaEventDisableTiming);
+        cudaEventRecord(pre[i], R[i]->stream);
+    }
+    for (size_t r = 0; r < P; ++r) {
+        for (size_t m = 0; m < P; ++m) cudaStreamWaitEvent(R[r]->stream, pre[m], 0);
+        for (size_t p = 0; p < P; ++p)
+            cudaMemcpyAsync(R[r]->scratch + p * blk, R[p]->psi + r * blk, blk * sizeof(double2), cudaMemcpyDefault,
+                            R[r]->stream);
+        cudaEventRecord(post[r], R[r]->stream);
+    }
+    for (size_t m = 0; m < P; ++m)
+        for (size_t r = 0; r < P; ++r) cudaStreamWaitEvent(R[m]->stream, post[r], 0);
+    for (Handle *m : R) swap_buffers(m);
+    for (size_t i = 0; i < P; ++i) {
+        cudaEventDestroy(pre[i]);
+        cudaEventDestroy(post[i]);
+    }
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? QSIM_OK : check_cuda(R[0], e, "group all-to-all");
 }
 
 static int exchange_pair(Handle *A, Handle *B, int g)
@@ -166,6 +257,12 @@ static int run_steps(const Ranks &R, const std::vector<Step> &steps)
     for (const Step &st : steps) {
         if (st.kind == STEP_LSWAP) {
             for (Handle *h : R) launch_swap_local(h, st.a, st.b);
+        } else if (st.kind == STEP_A2A) {
+            if (group) {
+                if (int rc = alltoall_group(R, st.a)) return rc;
+            } else {
+                if (int rc = alltoall_nccl(R[0], st.a)) return rc;
+            }
         } else if (group) {
             const int gb = st.a - R[0]->nl;
             for (size_t r = 0; r < R.size(); ++r) {

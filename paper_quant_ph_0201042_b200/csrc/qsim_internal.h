@@ -256,6 +256,7 @@ struct Handle {
 // enabled; prof_end also counts the launch.
 void prof_begin(Handle *h);
 void prof_end(Handle *h, const char *name, uint64_t bytes);
+void prof_end_comm(Handle *h, const char *name, uint64_t bytes);   // exchanges: bytes sent + received
 
 // error helpers
 int fail(Handle *h, int code, const std::string &msg);

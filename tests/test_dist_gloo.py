@@ -5,8 +5,9 @@ dist.cu) decides which shard exchanges bring global qubits local and how the
 logical -> physical map changes.  Here each rank holds its shard as a numpy
 array, the planned steps are executed with the exchange the library performs
 (rank r swaps the half of its shard whose top local bit differs from its bit g
-with rank r ^ 2^(g - nl)), and the re-assembled state must
-equal the original state read through the map.  No GPU is involved.
+with rank r ^ 2^(g - nl); or the all-to-all that swaps
+every global position with the top local positions at once), and the
+re-assembled state must equal the original state read through the map.  No GPU is involved.
 """
 import os
 import socket
@@ -65,6 +66,22 @@ def _worker(rank, world, port, n, seqs, q):
             for kind, a, b in steps:
                 if kind == 0:
                     shard = _swap_local_bits(shard, a, b)
+                elif kind == 2:
+                    # all-to-all: block j (top a local bits) -> rank j, block rank <- rank j's block
+                    blk = shard.size >> a
+                    out = shard.copy()
+                    reqs, bufs = [], {}
+                    for p in range(world):
+                        if p == rank:
+                            continue
+                        send = torch.from_numpy(np.ascontiguousarray(shard[p * blk:(p + 1) * blk]).view(np.float64).copy())
+                        bufs[p] = torch.empty_like(send)
+                        reqs += [dist.isend(send, p), dist.irecv(bufs[p], p)]
+                    for r_ in reqs:
+                        r_.wait()
+                    for p, t in bufs.items():
+                        out[p * blk:(p + 1) * blk] = t.numpy().view(complex)
+                    shard = out
                 else:
                     gb = a - nl
                     partner = rank ^ (1 << gb)
@@ -107,6 +124,8 @@ def _worker(rank, world, port, n, seqs, q):
     (2, 6, [[0], [1, 0], [5], [0, 3]]),
     (4, 7, [[0, 1], [1], [2, 0, 6], [3, 4, 5]]),
     (4, 5, [[0, 1, 2], [3, 4], [1]]),
+    (8, 7, [[0, 1, 2], [3], [0, 4, 5], [6, 1]]),
+    (4, 6, [[0, 1], [2, 3], [0, 5]]),
 ])
 def test_sharded_exchanges_preserve_the_state(world, n, seqs):
     ctx = mp.get_context("spawn")
