@@ -30,6 +30,7 @@ sys.path.insert(0, ROOT)
 
 N_QUBITS = 28
 SEED = 3
+METRIC = "state-vector GB/s per gate (QFT circuit; % HBM peak in roofline) & circuit time"
 WORKLOAD = "configs[2]: QFT circuit, n=28 complex128 (4 GiB), seeded complex-Gaussian input"
 
 
@@ -138,12 +139,17 @@ def run_reference(args):
     t = statistics.mean(times)
     value = gb / t / 1e9
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    # same metric / unit / config as our arm; each step is a bounded sample
+    # of the workload (the same circuit at n = n_sample), in the same per-gate unit
+    gb_full, ng_full = gate_bytes(N_QUBITS)
     line = {
-        "impl": "reference", "metric": "state-vector GB/s per gate (QFT circuit)", "value": value, "unit": "GB/s",
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
         "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD + f" -- reference arm: the CPU oracle on a bounded sample n={n_sample}",
-                   "n": n_sample, "gates": ng},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded complex Gaussian, DESIGN.md R19)",
+        "config": {"workload": WORKLOAD, "n": N_QUBITS, "gates": ng_full, "gate_bytes": gb_full,
+                   "state_bytes": 16 << N_QUBITS, "parallelism": "cpu-oracle",
+                   "sample": f"each step: the same QFT circuit on a seeded Gaussian n={n_sample} state "
+                             f"({ng} gates) run by the CPU oracle (plain C + OpenMP)"},
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "oracle",
                          "sample": f"oracle QFT circuit, n={n_sample}, {steps} timed runs"},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -306,7 +312,7 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": "state-vector GB/s per gate (QFT circuit; % HBM peak in roofline) & circuit time",
+            "metric": METRIC,
             "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded complex Gaussian, DESIGN.md R19)",
