@@ -37,6 +37,7 @@ int check_cuda(Handle *h, cudaError_t e, const char *what)
 
 void ensure_red(Handle *h, size_t doubles)
 {
+    cudaSetDevice(h->device);
     if (h->red_cap >= doubles) return;
     if (h->d_red) {
         cudaStreamSynchronize(h->stream);
@@ -55,6 +56,7 @@ void ensure_red(Handle *h, size_t doubles)
 
 void ensure_hred(Handle *h, size_t doubles)
 {
+    cudaSetDevice(h->device);
     if (h->hred_cap >= doubles) return;
     if (h->h_red) cudaFreeHost(h->h_red);
     size_t cap = std::max<size_t>(doubles, 1 << 12);
@@ -70,6 +72,7 @@ void ensure_hred(Handle *h, size_t doubles)
 
 int ensure_scratch(Handle *h)
 {
+    cudaSetDevice(h->device);
     if (h->scratch) return QSIM_OK;
     cudaError_t e = cudaMalloc(&h->scratch, sizeof(double2) * h->local_dim());
     if (e != cudaSuccess) {
@@ -94,6 +97,7 @@ static cudaEvent_t pool_event(Handle *h)
 
 void prof_begin(Handle *h)
 {
+    cudaSetDevice(h->device);   // rank groups may span devices: launch on the member's own
     if (!h->prof_on) return;
     h->pending = pool_event(h);
     cudaEventRecord(h->pending, h->stream);
@@ -701,6 +705,7 @@ int qsim_set_fusion(qsim_t *h, int enable)
     QS_CHECK_HANDLE(h);
     const Ranks R = ranks_of(h);
     for (Handle *m : R) {
+        cudaSetDevice(m->device);
         if (int rc = flush_queue(m)) return lift(h, R, rc);
         m->fuse = enable ? 1 : 0;
     }
@@ -764,6 +769,7 @@ int qsim_sync(qsim_t *h)
     QS_CHECK_HANDLE(h);
     const Ranks R = ranks_of(h);
     for (Handle *m : R) {
+        cudaSetDevice(m->device);
         if (int rc = flush_queue(m)) return lift(h, R, rc);
         if (int rc = check_cuda(m, cudaStreamSynchronize(m->stream), "qsim_sync")) return lift(h, R, rc);
     }
@@ -777,6 +783,7 @@ int qsim_set_basis(qsim_t *h, uint64_t idx)
     if (h->n < 64 && idx >> h->n) return fail(h, QSIM_ERANGE, "basis index >= 2^n");
     const Ranks R = ranks_of(h);
     for (Handle *m : R) {
+        cudaSetDevice(m->device);
         m->queue.clear();   // the state is overwritten
         for (int q = 0; q < m->n; ++q) m->pos[q] = m->n - 1 - q;
         launch_zero(m);
@@ -792,6 +799,7 @@ static int global_norm(qsim_t *h, const Ranks &R, double *out)
     std::vector<std::vector<double>> parts(R.size(), std::vector<double>(1, 0.0));
     for (size_t i = 0; i < R.size(); ++i) {
         Handle *m = R[i];
+        cudaSetDevice(m->device);
         if (int rc = flush_queue(m)) return lift(h, R, rc);
         launch_norm(m, m->d_red);
         if (int rc = after_launch(m, "norm")) return lift(h, R, rc);
@@ -808,6 +816,7 @@ int qsim_init_gaussian(qsim_t *h, uint64_t seed)
     QS_CHECK_HANDLE(h);
     const Ranks R = ranks_of(h);
     for (Handle *m : R) {
+        cudaSetDevice(m->device);
         m->queue.clear();   // the state is overwritten
         for (int q = 0; q < m->n; ++q) m->pos[q] = m->n - 1 - q;
         launch_init_gaussian(m, seed);
@@ -815,6 +824,7 @@ int qsim_init_gaussian(qsim_t *h, uint64_t seed)
     double s = 0.0;
     if (int rc = global_norm(h, R, &s)) return rc;
     for (Handle *m : R) {
+        cudaSetDevice(m->device);
         launch_scale(m, 1.0 / std::sqrt(s));
         if (int rc = after_launch(m, "init_gaussian")) return lift(h, R, rc);
     }
@@ -835,6 +845,7 @@ static int copy_state(qsim_t *h, uint64_t off, uint64_t cnt, qsim_c128 *host, bo
         if (off < lo || off + cnt > hi) return fail(h, QSIM_ERANGE, "slice not owned by this rank");
     }
     for (Handle *m : R) {
+        cudaSetDevice(m->device);
         const uint64_t lo = (uint64_t)m->rank << m->nl, hi = lo + m->local_dim();
         const uint64_t a = std::max(off, lo), b = std::min(off + cnt, hi);
         if (a >= b) continue;
@@ -1074,6 +1085,7 @@ int qsim_phase_flip(qsim_t *h, uint64_t idx)
     if (h->n < 64 && idx >> h->n) return fail(h, QSIM_ERANGE, "index >= 2^n");
     const Ranks R = ranks_of(h);
     for (Handle *m : R) {
+        cudaSetDevice(m->device);
         if (int rc = flush_queue(m)) return lift(h, R, rc);
         // physical location of logical index idx
         uint64_t phys = 0;
@@ -1158,6 +1170,7 @@ int qsim_apply_perm(qsim_t *h, const qsim_perm_t *f)
     for (int q = f->lo; q < f->lo + f->m; ++q) need.push_back(q);
     if (int rc = dist_make_local(R, need)) return lift(h, R, rc);
     for (Handle *m : R) {
+        cudaSetDevice(m->device);
         PermDesc d;
         std::memset(&d, 0, sizeof d);
         d.kind = f->kind;
@@ -1242,6 +1255,7 @@ int qsim_inject_errors(qsim_t *h, uint64_t seed, const qsim_noise_t *model, qsim
             if (!any) continue;
             std::vector<const double2 *> tabs;
             for (Handle *m : R) {
+                cudaSetDevice(m->device);
                 int rc;
                 double2 *dt = batch_table(m, B, rc);
                 if (!dt) return lift(h, R, rc);
@@ -1306,6 +1320,7 @@ int qsim_batch_set_state(qsim_t *h, const qsim_c128 *reg)
     const int r = h->n - h->batch_b;
     const double scale = 1.0 / std::sqrt((double)(1ull << h->batch_b));
     for (Handle *m : R) {
+        cudaSetDevice(m->device);
         for (int q = 0; q < m->n; ++q) m->pos[q] = m->n - 1 - q;   // the whole state is overwritten
         double2 *src = nullptr;
         int rc = check_cuda(m, cudaMalloc(&src, sizeof(double2) << r), "batch register buffer");
@@ -1333,6 +1348,7 @@ int qsim_batch_overlap(qsim_t *h, const qsim_c128 *ref, qsim_c128 *out)
     std::vector<std::vector<double>> parts(R.size(), std::vector<double>(2 * B, 0.0));
     for (size_t i = 0; i < R.size(); ++i) {
         Handle *m = R[i];
+        cudaSetDevice(m->device);
         const uint64_t nt = m->local_dim() >> r;
         const uint64_t t0 = ((uint64_t)m->rank << m->nl) >> r;   // canonical: shard = a block of trajectories
         double2 *src = nullptr;
@@ -1378,6 +1394,7 @@ int qsim_probs(qsim_t *h, int lo, int m, double *out)
     std::vector<std::vector<double>> parts(R.size(), std::vector<double>(ny, 0.0));
     for (size_t i = 0; i < R.size(); ++i) {
         Handle *hm = R[i];
+        cudaSetDevice(hm->device);
         if (hm->probs_cap < nyl) {
             if (hm->d_probs) {
                 cudaStreamSynchronize(hm->stream);
@@ -1441,6 +1458,7 @@ int qsim_measure_range(qsim_t *h, int lo, int m, double r, int collapse, uint64_
     const Ranks R = ranks_of(h);
     const int pl = h->n - lo - m;
     for (Handle *hm : R) {
+        cudaSetDevice(hm->device);
         uint64_t mask = 0, val = 0;
         int zero_all = 0;
         for (int b = 0; b < m; ++b) {
@@ -1475,6 +1493,7 @@ int qsim_inner(qsim_t *a, qsim_t *b, qsim_c128 *out)
     std::vector<std::vector<double>> parts(Ra.size(), std::vector<double>(2, 0.0));
     for (size_t i = 0; i < Ra.size(); ++i) {
         Handle *ha = Ra[i], *hb = Rb[i];
+        cudaSetDevice(ha->device);
         // b's shard must be complete before a's stream reads it
         cudaEvent_t ev;
         if (int rc = check_cuda(ha, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "inner")) return lift(a, Ra, rc);
@@ -1509,6 +1528,7 @@ int qsim_prob_index(qsim_t *h, uint64_t idx, double *out)
     std::vector<std::vector<double>> parts(R.size(), std::vector<double>(1, 0.0));
     for (size_t i = 0; i < R.size(); ++i) {
         Handle *m = R[i];
+        cudaSetDevice(m->device);
         if ((int)(idx >> m->nl) != m->rank) continue;
         double2 a;
         if (int rc = check_cuda(m, cudaMemcpyAsync(&a, m->psi + (idx & (m->local_dim() - 1)), sizeof a,
@@ -1535,6 +1555,7 @@ int qsim_measure(qsim_t *h, double r, uint64_t *idx)
     std::vector<std::vector<double>> parts(R.size(), std::vector<double>(total, 0.0));
     for (size_t i = 0; i < R.size(); ++i) {
         Handle *m = R[i];
+        cudaSetDevice(m->device);
         double *d_blk = nullptr;
         if (cudaMalloc(&d_blk, nb * sizeof(double)) != cudaSuccess) {
             cudaGetLastError();
@@ -1569,6 +1590,7 @@ int qsim_measure(qsim_t *h, double r, uint64_t *idx)
     std::vector<std::vector<double>> res(R.size(), std::vector<double>(1, 0.0));
     for (size_t i = 0; i < R.size(); ++i) {
         Handle *m = R[i];
+        cudaSetDevice(m->device);
         if (m->rank != owner) continue;
         std::vector<double2> amp(blen);
         const uint64_t loc = ((uint64_t)sel * blen) & (m->local_dim() - 1);
@@ -1613,6 +1635,7 @@ int qsim_shor_semantic_state(qsim_t *h, uint64_t x, uint64_t N, uint64_t v)
     std::vector<std::vector<double>> parts(R.size(), std::vector<double>(1, 0.0));
     for (size_t i = 0; i < R.size(); ++i) {
         Handle *m = R[i];
+        cudaSetDevice(m->device);
         m->queue.clear();   // the state is overwritten
         for (int q = 0; q < m->n; ++q) m->pos[q] = m->n - 1 - q;
         ensure_red(m, 1);

@@ -138,6 +138,7 @@ __global__ void __launch_bounds__(1024) k_batch_overlap(const double2 *__restric
 void launch_batch_mats(Handle *h, int kind, const double *ang, double sigma, uint64_t seed, uint64_t g, uint64_t B,
                        double2 *out)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     double a[4] = {0, 0, 0, 0};
     const int na = kind == QSIM_GATE_RP ? 2 : kind == QSIM_GATE_P1 ? 1 : 4;
     for (int s = 0; s < na; ++s) a[s] = ang[s];
@@ -149,6 +150,7 @@ void launch_batch_mats(Handle *h, int kind, const double *ang, double sigma, uin
 
 void launch_batch_broadcast(Handle *h, const double2 *src, int r, double scale)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     const uint64_t count = h->local_dim();
     const uint64_t want = (count + 255) / 256;
     const uint64_t cap = (uint64_t)h->num_sms * 8;
@@ -159,6 +161,7 @@ void launch_batch_broadcast(Handle *h, const double2 *src, int r, double scale)
 
 void launch_batch_overlap(Handle *h, const double2 *ref, int r, double scale, double *d_out)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     const uint64_t ntraj = h->local_dim() >> r;
     prof_begin(h);
     k_batch_overlap<<<(unsigned)ntraj, 1024, 0, h->stream>>>(h->psi, ref, r, scale, d_out);

@@ -122,6 +122,7 @@ static unsigned grid_for(const Handle *h, uint64_t work)
 
 void launch_apply_2x2(Handle *h, int p, uint64_t cm, uint64_t cv, const double2 U[4])
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     Mat m;
     for (int k = 0; k < 4; ++k) m.u[k] = U[k];
     const uint64_t np = h->local_dim() >> 1;
@@ -133,6 +134,7 @@ void launch_apply_2x2(Handle *h, int p, uint64_t cm, uint64_t cv, const double2 
 
 void launch_apply_diag(Handle *h, int p, uint64_t cm, uint64_t cv, double2 d0, double2 d1)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     // diag(d0, d1) = two masked phase multiplications (skip the identity halves)
     const bool one0 = d0.x == 1.0 && d0.y == 0.0, one1 = d1.x == 1.0 && d1.y == 0.0;
     const uint64_t bit = 1ull << p;
@@ -142,6 +144,7 @@ void launch_apply_diag(Handle *h, int p, uint64_t cm, uint64_t cv, double2 d0, d
 
 void launch_phase_mask(Handle *h, uint64_t mask, uint64_t val, double2 ph)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     MaskBits mb;
     mb.nb = 0;
     for (int b = 0; b < h->nl; ++b)
@@ -154,6 +157,7 @@ void launch_phase_mask(Handle *h, uint64_t mask, uint64_t val, double2 ph)
 
 void launch_swap_local(Handle *h, int p1, int p2)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     if (p1 == p2) return;
     if (p1 > p2) { int t = p1; p1 = p2; p2 = t; }
     const uint64_t count = h->local_dim() >> 2;
@@ -164,6 +168,7 @@ void launch_swap_local(Handle *h, int p1, int p2)
 
 void launch_scale(Handle *h, double s)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     const uint64_t count = h->local_dim();
     prof_begin(h);
     k_scale<<<grid_for(h, count), kThreads, 0, h->stream>>>(h->psi, count, s);
@@ -172,11 +177,13 @@ void launch_scale(Handle *h, double s)
 
 void launch_zero(Handle *h)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     cudaMemsetAsync(h->psi, 0, sizeof(double2) * h->local_dim(), h->stream);
 }
 
 void launch_set_one(Handle *h, uint64_t local_idx)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     prof_begin(h);
     k_set_one<<<1, 1, 0, h->stream>>>(h->psi, local_idx);
     prof_end(h, "k_set_one", 16);

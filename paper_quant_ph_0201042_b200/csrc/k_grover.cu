@@ -358,6 +358,7 @@ static bool try_regs(Handle *h, uint64_t mark, int iters, double *d_trace)
 
 void launch_grover(Handle *h, uint64_t mark_local, int mark_rank, int iters, double *d_trace)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     (void)mark_rank;
     const uint64_t N = h->local_dim();
     if (!getenv("QSIM_NO_GROVER_REGS") && N >= 4096 && try_regs(h, mark_local, iters, d_trace)) return;

@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(kOpsThreads, 2) k_ops_pass(const __grid_consta
 
 void launch_ops_pass(Handle *h, const OpsLaunch &L)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     const OpsPass &P = L.P;
     // memory-bound passes (little FP64 work per amplitude) stream best through
     // the TMA ring; FP64-bound ones through two CTAs per SM (k_ops_pass)
@@ -100,11 +101,10 @@ void launch_ops_pass(Handle *h, const OpsLaunch &L)
     }
     if (cost <= tma_max && launch_ops_pass_tma(h, L)) return;
     const size_t smem = sizeof(double2) << P.tbits;
-    static bool attr = false;
-    if (!attr) {
+    static uint64_t attr = 0;
+    if (first_use_on_device(attr)) {
         cudaFuncSetAttribute(k_ops_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(sizeof(double2) << kTileMaxBits));
-        attr = true;
     }
     const int threads = 1 << (P.tbits - RB5);
     int per_sm = 1;

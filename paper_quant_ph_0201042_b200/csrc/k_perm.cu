@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(256) k_perm_generic(const double2 *__restrict_
 
 void launch_perm(Handle *h, const PermDesc &d)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     PermArgs a;
     a.kind = d.kind;
     a.wm = d.wm;

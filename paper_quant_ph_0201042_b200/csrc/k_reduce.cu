@@ -177,6 +177,7 @@ static void sum_tree(Handle *h, const double *d_in, uint64_t count, double *d_ou
 
 void launch_block_abs2(Handle *h, int blk_bits, double *d_out)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     const uint64_t chunk = 1ull << blk_bits;
     const uint64_t nb = h->local_dim() >> blk_bits;
     prof_begin(h);
@@ -186,6 +187,7 @@ void launch_block_abs2(Handle *h, int blk_bits, double *d_out)
 
 void launch_norm(Handle *h, double *d_out)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     // chunks of 2^12 (or the whole shard if smaller), then one tree over them
     const int bb = h->nl < 12 ? h->nl : 12;
     const uint64_t nb = h->local_dim() >> bb;
@@ -224,6 +226,7 @@ static void tree_sum_ws(Handle *h, const double *d_in, uint64_t nb, double *d_tm
 
 void launch_inner(Handle *h, const double2 *a, const double2 *b, double *d_out)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     const int bb = h->nl < 12 ? h->nl : 12;
     const uint64_t nb = h->local_dim() >> bb;
     ensure_red(h, 2 * nb + (nb >> 9) + 16);
@@ -237,6 +240,7 @@ void launch_inner(Handle *h, const double2 *a, const double2 *b, double *d_out)
 
 void launch_collapse(Handle *h, uint64_t mask, uint64_t val, double s, int zero_all)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     const uint64_t count = h->local_dim();
     const uint64_t want = (count + kThreads - 1) / kThreads;
     const uint64_t cap = (uint64_t)h->num_sms * 8;
@@ -250,6 +254,7 @@ void launch_collapse(Handle *h, uint64_t mask, uint64_t val, double s, int zero_
 
 void launch_probs_contig(Handle *h, int pl, int m, double *d_out)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     const uint64_t ny = 1ull << m;
     const uint64_t rest = h->local_dim() >> m;
     // chunks so that the grid has >= ~2 waves of blocks
@@ -268,6 +273,7 @@ void launch_probs_contig(Handle *h, int pl, int m, double *d_out)
 
 void launch_init_gaussian(Handle *h, uint64_t seed)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     const uint64_t count = h->local_dim();
     const uint64_t gbase = (uint64_t)h->rank << h->nl;
     const uint64_t want = (count + kThreads - 1) / kThreads;

@@ -168,11 +168,13 @@ static void launch_shor(Handle *h, bool write, uint64_t x, uint64_t N, uint64_t 
 
 void launch_shor_count(Handle *h, uint64_t x, uint64_t N, uint64_t v, unsigned long long *d_count)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     launch_shor(h, false, x, N, v, 0.0, d_count);
 }
 
 void launch_shor_write(Handle *h, uint64_t x, uint64_t N, uint64_t v, double amp)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     launch_shor(h, true, x, N, v, amp, nullptr);
 }
 

@@ -201,11 +201,10 @@ template <int NM>
 static void launch_nm(Handle *h, const TilePass &tp, const double2 *in, double2 *out)
 {
     const size_t smem = (sizeof(double2) << tp.tbits) + 1024 * sizeof(double2);
-    static bool attr_done = false;
-    if (!attr_done) {
+    static uint64_t attr_done = 0;
+    if (first_use_on_device(attr_done)) {
         cudaFuncSetAttribute(k_tile_pass<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)((sizeof(double2) << kTileMaxBits) + 1024 * sizeof(double2)));
-        attr_done = true;
     }
     const int threads = 1 << (tp.tbits - kRegBits);
     int per_sm = 1;
@@ -237,6 +236,7 @@ void finish_tile_pass(TilePass &tp)
 
 void launch_tile_pass(Handle *h, const TilePass &tp_in, const double2 *in, double2 *out)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     if (launch_tile_pass_tma(h, tp_in, in, out)) return;
     TilePass tp = tp_in;
     finish_tile_pass(tp);

@@ -587,11 +587,11 @@ bool build_side(const double2 *base, int nl, const std::vector<int> &pos_of_tile
 template <int NM>
 void launch_tma_nm(Handle *h, const CUtensorMap &im, const CUtensorMap &om, const TilePass &tp, const TmaArgs &ta)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     const size_t smem = (size_t)kStages * kTileBytes + 1024 * sizeof(double2) + kStages * sizeof(uint64_t);
-    static bool attr = false;
-    if (!attr) {
+    static uint64_t attr = 0;
+    if (first_use_on_device(attr)) {
         cudaFuncSetAttribute(k_tile_tma<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
     }
     const uint64_t ntiles = 1ull << tp.nfix;
     const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)h->num_sms);
@@ -603,11 +603,11 @@ void launch_tma_nm(Handle *h, const CUtensorMap &im, const CUtensorMap &om, cons
 template <int A, bool INV, bool HONLY>
 void launch_fixed(Handle *h, const CUtensorMap &im, const CUtensorMap &om, const TilePass &tp, const TmaArgs &ta)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     const size_t smem = (size_t)kStages * kTileBytes + 1024 * sizeof(double2) + kStages * sizeof(uint64_t);
-    static bool attr = false;
-    if (!attr) {
+    static uint64_t attr = 0;
+    if (first_use_on_device(attr)) {
         cudaFuncSetAttribute(k_qft_tma<A, INV, HONLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
     }
     const uint64_t ntiles = 1ull << tp.nfix;
     const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)h->num_sms);
@@ -619,6 +619,7 @@ void launch_fixed(Handle *h, const CUtensorMap &im, const CUtensorMap &om, const
 template <int A>
 bool launch_fixed_a(Handle *h, const CUtensorMap &im, const CUtensorMap &om, const TilePass &tp, const TmaArgs &ta)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     if (tp.hadamard_only) launch_fixed<A, false, true>(h, im, om, tp, ta);
     else if (tp.inverse) launch_fixed<A, true, false>(h, im, om, tp, ta);
     else launch_fixed<A, false, false>(h, im, om, tp, ta);
@@ -631,6 +632,7 @@ bool launch_fixed_a(Handle *h, const CUtensorMap &im, const CUtensorMap &om, con
 // Returns false (nothing launched) when the geometry does not fit.
 bool launch_tile_pass_tma(Handle *h, const TilePass &tp_in, const double2 *in, double2 *out)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     if (tp_in.tbits != kTmaTileBits || getenv("QSIM_NO_TMA")) return false;
     TilePass tp = tp_in;
     finish_tile_pass(tp);
@@ -672,6 +674,7 @@ bool launch_tile_pass_tma(Handle *h, const TilePass &tp_in, const double2 *in, d
 
 bool launch_ops_pass_tma(Handle *h, const OpsLaunch &L)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     const OpsPass &P = L.P;
     if (P.tbits != kTmaTileBits || getenv("QSIM_NO_TMA")) return false;
     std::vector<int> fid(h->nl, -1);
@@ -682,10 +685,9 @@ bool launch_ops_pass_tma(Handle *h, const OpsLaunch &L)
     std::memset(&ta, 0, sizeof ta);
     if (!build_side(h->psi, h->nl, tp, fid, im, ta.in_first, ta.in_len, ta.in_rank)) return false;
     const size_t smem = (size_t)kStages * kTileBytes + 8 * sizeof(uint64_t);
-    static bool attr = false;
-    if (!attr) {
+    static uint64_t attr = 0;
+    if (first_use_on_device(attr)) {
         cudaFuncSetAttribute(k_ops_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
     }
     const uint64_t ntiles = 1ull << P.nfix;
     const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)h->num_sms);

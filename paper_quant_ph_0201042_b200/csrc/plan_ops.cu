@@ -294,6 +294,7 @@ bool plan_log()
 
 int launch_check(Handle *h, const char *what)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return check_cuda(h, e, what);
     if (h->poisoned) return fail(h, QSIM_ECUDA, h->err);
@@ -304,6 +305,7 @@ int launch_check(Handle *h, const char *what)
 
 int flush_queue(Handle *h)
 {
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
     if (h->queue.empty()) {
         h->tabs_used = 0;
         return QSIM_OK;

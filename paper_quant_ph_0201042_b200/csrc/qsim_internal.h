@@ -252,6 +252,18 @@ struct Handle {
     uint64_t local_dim() const { return (uint64_t)1 << nl; }
 };
 
+// Function attributes (dynamic smem limits) are per device: true the first
+// time it is called for the current device (per call site).
+inline bool first_use_on_device(uint64_t &mask)
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (mask & bit) return false;
+    mask |= bit;
+    return true;
+}
+
 // per-launch profiling (qsim_profile): events around every kernel launch when
 // enabled; prof_end also counts the launch.
 void prof_begin(Handle *h);
