@@ -1496,8 +1496,10 @@ int qsim_inner(qsim_t *a, qsim_t *b, qsim_c128 *out)
         cudaSetDevice(ha->device);
         // b's shard must be complete before a's stream reads it
         cudaEvent_t ev;
-        if (int rc = check_cuda(ha, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "inner")) return lift(a, Ra, rc);
+        cudaSetDevice(hb->device);   // the event lives on b's device
+        if (int rc = check_cuda(hb, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "inner")) return lift(a, Ra, rc);
         cudaEventRecord(ev, hb->stream);
+        cudaSetDevice(ha->device);
         cudaStreamWaitEvent(ha->stream, ev, 0);
         double *d_out = nullptr;
         int rc = check_cuda(ha, cudaMalloc(&d_out, 2 * sizeof(double)), "inner buffer");

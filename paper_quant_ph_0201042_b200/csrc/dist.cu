@@ -206,19 +206,23 @@ static int alltoall_group(const Ranks &R, int k)
         if (int rc = ensure_scratch(m)) return rc;
     std::vector<cudaEvent_t> pre(P), post(P);
     for (size_t i = 0; i < P; ++i) {
+        cudaSetDevice(R[i]->device);   // events live on their stream's device
         cudaEventCreateWithFlags(&pre[i], cudaEventDisableTiming);
         cudaEventCreateWithFlags(&post[i], cudaEventDisableTiming);
         cudaEventRecord(pre[i], R[i]->stream);
     }
     for (size_t r = 0; r < P; ++r) {
+        cudaSetDevice(R[r]->device);
         for (size_t m = 0; m < P; ++m) cudaStreamWaitEvent(R[r]->stream, pre[m], 0);
         for (size_t p = 0; p < P; ++p)
             cudaMemcpyAsync(R[r]->scratch + p * blk, R[p]->psi + r * blk, blk * sizeof(double2), cudaMemcpyDefault,
                             R[r]->stream);
         cudaEventRecord(post[r], R[r]->stream);
     }
-    for (size_t m = 0; m < P; ++m)
+    for (size_t m = 0; m < P; ++m) {
+        cudaSetDevice(R[m]->device);
         for (size_t r = 0; r < P; ++r) cudaStreamWaitEvent(R[m]->stream, post[r], 0);
+    }
     for (Handle *m : R) swap_buffers(m);
     for (size_t i = 0; i < P; ++i) {
         cudaEventDestroy(pre[i]);
@@ -234,10 +238,13 @@ static int exchange_pair(Handle *A, Handle *B, int g)
     const uint64_t half = A->local_dim() >> 1;
     if (int rc = ensure_scratch(A)) return rc;
     double2 *ha = A->psi + half, *hb = B->psi;
+    // an event lives on its stream's device (the members may sit on different GPUs)
     cudaEvent_t eb, ea;
+    cudaSetDevice(B->device);
     cudaEventCreateWithFlags(&eb, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ea, cudaEventDisableTiming);
     cudaEventRecord(eb, B->stream);
+    cudaSetDevice(A->device);
+    cudaEventCreateWithFlags(&ea, cudaEventDisableTiming);
     cudaStreamWaitEvent(A->stream, eb, 0);
     const size_t bytes = half * sizeof(double2);
     cudaMemcpyAsync(A->scratch, ha, bytes, cudaMemcpyDefault, A->stream);
