@@ -270,8 +270,12 @@ int apply_gate(const Ranks &R, uint64_t cmask, uint64_t cvals, int q, const doub
     if (R[0]->batch_b && (q < R[0]->batch_b || (cmask & ((1ull << R[0]->batch_b) - 1))))
         return fail(R[0], QSIM_EINVAL, "gate on a trajectory-index qubit of a batched handle");
     const int diag = tabs ? 0 : is_diag(U);
-    if (!diag && !is_local(R[0], q))
+    if (!diag && !is_local(R[0], q)) {
+        // rank groups: the gate reads the partner's shard over peer memory
+        // (one kernel, no layout change); otherwise swap q onto a local bit
+        if (!tabs && dist_remote_gate_available(R)) return dist_remote_gate(R, cmask, cvals, q, U);
         if (int rc = dist_make_local(R, std::vector<int>{q})) return rc;
+    }
     for (size_t ri = 0; ri < R.size(); ++ri) {
         Handle *h = R[ri];
         QOp op;
@@ -687,6 +691,8 @@ void qsim_destroy(qsim_t *h)
 #ifndef QSIM_NO_NCCL
     if (h->comm) ncclCommDestroy(h->comm);
 #endif
+    for (size_t i = 0; i < h->peer_buf.size(); ++i)
+        if ((int)(i / 2) != h->rank && h->peer_buf[i]) cudaIpcCloseMemHandle(h->peer_buf[i]);
     if (h->psi) cudaFree(h->psi);
     if (h->scratch) cudaFree(h->scratch);
     if (h->d_red) cudaFree(h->d_red);

@@ -15,6 +15,7 @@
 // pairwise exchanges, local positions by one bit-permutation pass.
 // Host-side partial results are combined in fixed rank order (allgather,
 // then summed on the host), so results are deterministic.
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -287,6 +288,211 @@ static int run_steps(const Ranks &R, const std::vector<Step> &steps)
         }
     }
     return QSIM_OK;
+}
+
+// ---------------------------------------------------------------- fused remote gate
+#ifndef QSIM_NO_NCCL
+// Multi-process world: map every rank's two shard allocations into this
+// process (cudaIpcGetMemHandle / OpenMemHandle, handles exchanged with one
+// NCCL all-gather).  Collective; all ranks agree on success (min-reduce), so
+// either every rank uses the remote path or none does.
+static int ipc_setup(Handle *h)
+{
+    if (h->ipc_state) return h->ipc_state;
+    h->ipc_state = -1;
+    if (ensure_scratch(h)) return -1;
+    h->own_buf[0] = h->psi;
+    h->own_buf[1] = h->scratch;
+    const int W = h->world;
+    const size_t hs = sizeof(cudaIpcMemHandle_t);
+    std::vector<unsigned char> mine(2 * hs, 0), all(2 * hs * W, 0);
+    int ok = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t *>(mine.data()), h->own_buf[0]) == cudaSuccess &&
+             cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t *>(mine.data() + hs), h->own_buf[1]) == cudaSuccess;
+    cudaGetLastError();
+    unsigned char *d_in = nullptr, *d_out = nullptr;
+    int *d_ok = nullptr;
+    if (cudaMalloc(&d_in, mine.size()) != cudaSuccess || cudaMalloc(&d_out, all.size()) != cudaSuccess ||
+        cudaMalloc(&d_ok, sizeof(int)) != cudaSuccess) {
+        cudaGetLastError();
+        ok = 0;   // still take part in the collectives below
+    }
+    if (d_in && d_out && d_ok) {
+        cudaMemcpyAsync(d_in, mine.data(), mine.size(), cudaMemcpyHostToDevice, h->stream);
+        ncclAllGather(d_in, d_out, mine.size(), ncclUint8, h->comm, h->stream);
+        cudaMemcpyAsync(all.data(), d_out, all.size(), cudaMemcpyDeviceToHost, h->stream);
+        cudaStreamSynchronize(h->stream);
+    }
+    h->peer_buf.assign(2 * W, nullptr);
+    for (int r = 0; r < W && ok; ++r) {
+        if (r == h->rank) {
+            h->peer_buf[2 * r] = h->own_buf[0];
+            h->peer_buf[2 * r + 1] = h->own_buf[1];
+            continue;
+        }
+        for (int k = 0; k < 2 && ok; ++k) {
+            cudaIpcMemHandle_t ih;
+            std::memcpy(&ih, all.data() + (2 * r + k) * hs, hs);
+            void *p = nullptr;
+            if (cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                cudaGetLastError();
+                ok = 0;
+            }
+            h->peer_buf[2 * r + k] = static_cast<double2 *>(p);
+        }
+    }
+    // agree: min over ranks
+    if (d_ok) {
+        cudaMemcpyAsync(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice, h->stream);
+        ncclAllReduce(d_ok, d_ok, 1, ncclInt, ncclMin, h->comm, h->stream);
+        cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, h->stream);
+        cudaStreamSynchronize(h->stream);
+    }
+    if (d_in) cudaFree(d_in);
+    if (d_out) cudaFree(d_out);
+    if (d_ok) cudaFree(d_ok);
+    cudaGetLastError();
+    h->ipc_state = ok ? 1 : -1;
+    return h->ipc_state;
+}
+#endif
+
+bool dist_remote_gate_available(const Ranks &R)
+{
+    static const bool off = std::getenv("QSIM_NO_REMOTE_GATES") != nullptr;
+    if (off) return false;
+    if (R.size() > 1) return true;   // in-process rank group: every shard is addressable (peer access)
+#ifndef QSIM_NO_NCCL
+    Handle *h = R[0];
+    if (h->world > 1 && h->comm) return ipc_setup(h) == 1;
+#endif
+    return false;
+}
+
+#ifndef QSIM_NO_NCCL
+// Multi-process variant: which of its two allocations is each rank's current
+// shard (one all-gather of a parity byte), the peer-memory kernel, then a
+// stream-ordered barrier (1-element all-reduce) before anyone reuses a shard
+// its partner may still be reading.
+static int remote_gate_world(Handle *h, uint64_t cmask, uint64_t cvals, int q, const double2 U[4])
+{
+    if (int rc = flush_queue(h)) return rc;
+    const int W = h->world, nl = h->nl;
+    const int gb = h->pos[q] - nl;
+    const int partner = h->rank ^ (1 << gb);
+    uint64_t m = 0, v = 0;
+    bool part = true;
+    for (int c = 0; c < h->n && part; ++c) {
+        if (!((cmask >> c) & 1)) continue;
+        const int p = h->pos[c];
+        const uint64_t want = (cvals >> c) & 1;
+        if (p < nl) {
+            m |= 1ull << p;
+            v |= want << p;
+        } else if ((((uint64_t)h->rank >> (p - nl)) & 1) != want) {
+            part = false;
+        }
+    }
+    unsigned char par = h->psi == h->own_buf[0] ? 0 : 1;
+    std::vector<unsigned char> pars(W, 0);
+    unsigned char *d = nullptr;
+    if (cudaMalloc(&d, W + 1) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(h, QSIM_ENOMEM, "remote gate buffer");
+    }
+    cudaMemcpyAsync(d, &par, 1, cudaMemcpyHostToDevice, h->stream);
+    if (int rc = nccl_check(h, ncclAllGather(d, d + 1, 1, ncclUint8, h->comm, h->stream), "ncclAllGather")) return rc;
+    cudaMemcpyAsync(pars.data(), d + 1, W, cudaMemcpyDeviceToHost, h->stream);
+    cudaStreamSynchronize(h->stream);
+    cudaFree(d);
+    if (part) {
+        const int b = (h->rank >> gb) & 1;
+        const double2 *theirs = h->peer_buf[2 * partner + pars[partner]];
+        launch_apply_2x2_remote(h, theirs, h->scratch, m, v, U[2 * b + b], U[2 * b + (1 - b)]);
+    }
+    // barrier: every rank's kernel has finished reading its partner's shard
+    double *dz = nullptr;
+    if (cudaMalloc(&dz, sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(h, QSIM_ENOMEM, "remote gate barrier");
+    }
+    cudaMemsetAsync(dz, 0, sizeof(double), h->stream);
+    int rc = nccl_check(h, ncclAllReduce(dz, dz, 1, ncclDouble, ncclSum, h->comm, h->stream), "barrier");
+    cudaStreamSynchronize(h->stream);
+    cudaFree(dz);
+    if (rc) return rc;
+    if (part) swap_buffers(h);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? QSIM_OK : check_cuda(h, e, "remote gate");
+}
+#endif
+
+// Every participating rank r computes its half of each pair from its own
+// shard and its partner's (r ^ 2^(g-nl)) into its scratch shard; once both
+// kernels of a pair are done (cross-stream events) the ranks swap shard and
+// scratch.  No layout change, no staging copies.
+int dist_remote_gate(const Ranks &R, uint64_t cmask, uint64_t cvals, int q, const double2 U[4])
+{
+#ifndef QSIM_NO_NCCL
+    if (R.size() == 1) return remote_gate_world(R[0], cmask, cvals, q, U);
+#endif
+    if (int rc = flush_all(R)) return rc;
+    const size_t P = R.size();
+    const int nl = R[0]->nl;
+    const int gb = R[0]->pos[q] - nl;
+    std::vector<char> part(P, 0);
+    std::vector<uint64_t> lm(P), lv(P);
+    for (size_t r = 0; r < P; ++r) {
+        Handle *h = R[r];
+        uint64_t m = 0, v = 0;
+        bool ok = true;
+        for (int c = 0; c < h->n && ok; ++c) {
+            if (!((cmask >> c) & 1)) continue;
+            const int p = h->pos[c];
+            const uint64_t want = (cvals >> c) & 1;
+            if (p < nl) {
+                m |= 1ull << p;
+                v |= want << p;
+            } else if ((((uint64_t)h->rank >> (p - nl)) & 1) != want) {
+                ok = false;
+            }
+        }
+        part[r] = ok;
+        lm[r] = m;
+        lv[r] = v;
+        if (ok)
+            if (int rc = ensure_scratch(h)) return rc;
+    }
+    std::vector<cudaEvent_t> pre(P), post(P);
+    for (size_t r = 0; r < P; ++r) {
+        cudaSetDevice(R[r]->device);
+        cudaEventCreateWithFlags(&pre[r], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&post[r], cudaEventDisableTiming);
+        cudaEventRecord(pre[r], R[r]->stream);
+    }
+    for (size_t r = 0; r < P; ++r) {
+        if (!part[r]) continue;
+        Handle *h = R[r];
+        const size_t p = r ^ ((size_t)1 << gb);
+        const int b = (h->rank >> gb) & 1;
+        cudaSetDevice(h->device);
+        cudaStreamWaitEvent(h->stream, pre[p], 0);   // the partner's shard is final
+        launch_apply_2x2_remote(h, R[p]->psi, h->scratch, lm[r], lv[r], U[2 * b + b], U[2 * b + (1 - b)]);
+        cudaEventRecord(post[r], h->stream);
+    }
+    for (size_t r = 0; r < P; ++r) {
+        if (!part[r]) continue;
+        const size_t p = r ^ ((size_t)1 << gb);
+        cudaSetDevice(R[r]->device);
+        cudaStreamWaitEvent(R[r]->stream, post[p], 0);   // the partner has read our shard
+    }
+    for (size_t r = 0; r < P; ++r) {
+        if (part[r]) swap_buffers(R[r]);
+        cudaSetDevice(R[r]->device);
+        cudaEventDestroy(pre[r]);
+        cudaEventDestroy(post[r]);
+    }
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? QSIM_OK : check_cuda(R[0], e, "remote gate");
 }
 
 int flush_all(const Ranks &R)

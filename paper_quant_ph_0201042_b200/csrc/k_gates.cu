@@ -109,6 +109,30 @@ __global__ void __launch_bounds__(kThreads) k_scale(double2 *__restrict__ psi, u
     }
 }
 
+// A 2x2 gate on a qubit that sits on a rank bit, computed in one kernel over
+// peer memory (SURVEY §8(e) fused alternative): the partner rank holds the
+// other row of every pair at the same local index, so this rank's output is
+// out_i = a * mine_i + c * theirs_i (a, c = this rank's row of U), reading
+// `theirs` straight from the partner's shard over NVLink -- the exchange and
+// the gate are one pass (16 B read local + 16 B read remote + 16 B written per
+// amplitude).  Amplitudes failing the local controls are copied.
+__global__ void __launch_bounds__(kThreads) k_apply_2x2_remote(const double2 *__restrict__ mine,
+                                                               const double2 *__restrict__ theirs,
+                                                               double2 *__restrict__ out, uint64_t count,
+                                                               uint64_t cm, uint64_t cv, double2 a, double2 c)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+        const double2 x = __ldcs(mine + i);
+        if ((i & cm) == cv) {
+            const double2 y = __ldcs(theirs + i);
+            __stcs(out + i, cfma2(a, x, c, y));
+        } else {
+            __stcs(out + i, x);
+        }
+    }
+}
+
 __global__ void k_set_one(double2 *psi, uint64_t i) { psi[i] = make_double2(1.0, 0.0); }
 
 }  // namespace
@@ -179,6 +203,17 @@ void launch_zero(Handle *h)
 {
     cudaSetDevice(h->device);   // members of a rank group may live on different devices
     cudaMemsetAsync(h->psi, 0, sizeof(double2) * h->local_dim(), h->stream);
+}
+
+void launch_apply_2x2_remote(Handle *h, const double2 *theirs, double2 *out, uint64_t cm, uint64_t cv, double2 a,
+                             double2 c)
+{
+    cudaSetDevice(h->device);
+    const uint64_t count = h->local_dim();
+    const uint64_t matching = count >> __builtin_popcountll(cm);
+    prof_begin(h);
+    k_apply_2x2_remote<<<grid_for(h, count), kThreads, 0, h->stream>>>(h->psi, theirs, out, count, cm, cv, a, c);
+    prof_end(h, "k_apply_2x2_remote", count * 32 + matching * 16);
 }
 
 void launch_set_one(Handle *h, uint64_t local_idx)

@@ -34,6 +34,10 @@ struct Handle;
 
 // Dense 2x2 on local position p; applied where (i & cmask) == cval (local mask).
 void launch_apply_2x2(Handle *h, int p, uint64_t cmask, uint64_t cval, const double2 U[4]);
+// 2x2 on a rank-bit qubit from the partner's shard over peer memory (out != psi):
+// out_i = a psi_i + c theirs_i where (i & cmask) == cval, psi_i elsewhere.
+void launch_apply_2x2_remote(Handle *h, const double2 *theirs, double2 *out, uint64_t cmask, uint64_t cval, double2 a,
+                             double2 c);
 // Diagonal diag(d0, d1) on local position p (both entries applied), controlled.
 void launch_apply_diag(Handle *h, int p, uint64_t cmask, uint64_t cval, double2 d0, double2 d1);
 // Multiply every amplitude with (i & mask) == val by ph.
@@ -244,6 +248,12 @@ struct Handle {
     int batch_b = 0;
     double2 *d_tabs = nullptr;   // per-trajectory matrix tables of queued gates (reset at flush)
     size_t tabs_cap = 0, tabs_used = 0;   // in double2
+    // multi-process world: peers' shard buffers mapped with CUDA IPC for the
+    // fused remote gate (dist.cu), set up on first use (ipc_state: 0 not yet,
+    // 1 ready, -1 unavailable)
+    int ipc_state = 0;
+    double2 *own_buf[2] = {nullptr, nullptr};   // this rank's two allocations (psi / scratch at setup)
+    std::vector<double2 *> peer_buf;            // 2 * world: rank r's allocations 0 and 1
     // in-process rank group (qsim_create_group): the group handle owns the
     // member handles (one shard each); members point back at the group
     std::vector<Handle *> members;
@@ -290,6 +300,10 @@ inline Ranks ranks_of(Handle *h) { return h->members.empty() ? Ranks{h} : h->mem
 
 // distributed layer (dist.cu): every step runs on all ranks of R in lock step
 int dist_make_local(const Ranks &R, const std::vector<int> &need);   // make logical qubits local
+// a non-diagonal gate on a rank-bit qubit in one peer-memory kernel per rank
+// (in-process rank groups); false: not available here (use dist_make_local)
+bool dist_remote_gate_available(const Ranks &R);
+int dist_remote_gate(const Ranks &R, uint64_t cmask, uint64_t cvals, int q, const double2 U[4]);
 int dist_canonicalize(const Ranks &R);                               // pos[q] = n-1-q everywhere
 // per-rank host partials -> the sum over all ranks of the world, in rank order
 // (parts[i] belongs to R[i]); out may alias parts[0]
