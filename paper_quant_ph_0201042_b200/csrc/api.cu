@@ -271,9 +271,11 @@ int apply_gate(const Ranks &R, uint64_t cmask, uint64_t cvals, int q, const doub
         return fail(R[0], QSIM_EINVAL, "gate on a trajectory-index qubit of a batched handle");
     const int diag = tabs ? 0 : is_diag(U);
     if (!diag && !is_local(R[0], q)) {
-        // rank groups: the gate reads the partner's shard over peer memory
-        // (one kernel, no layout change); otherwise swap q onto a local bit
-        if (!tabs && dist_remote_gate_available(R)) return dist_remote_gate(R, cmask, cvals, q, U);
+        // one sweep per gate (fusion off): the gate reads the partner's shard
+        // over peer memory (one kernel, no layout change, no exchange).  With
+        // fusion on, q is swapped onto a local bit instead, so this and the
+        // following gates on q join fused passes.
+        if (!tabs && !R[0]->fuse && dist_remote_gate_available(R)) return dist_remote_gate(R, cmask, cvals, q, U);
         if (int rc = dist_make_local(R, std::vector<int>{q})) return rc;
     }
     for (size_t ri = 0; ri < R.size(); ++ri) {
@@ -715,6 +717,7 @@ int qsim_set_fusion(qsim_t *h, int enable)
         if (int rc = flush_queue(m)) return lift(h, R, rc);
         m->fuse = enable ? 1 : 0;
     }
+    h->fuse = enable ? 1 : 0;   // a group handle's own flag (read by qsim_qft) follows its members
     return QSIM_OK;
 }
 
