@@ -178,9 +178,10 @@ void mat_up2(double p, double2 U[4])
 int kind_nangles(int kind) { return kind == QSIM_GATE_RP ? 2 : kind == QSIM_GATE_P1 ? 1 : 4; }
 
 // Angle-form matrix (R12-R15), perturbed when sigma > 0.
-void angle_matrix(const Handle *h, int kind, const double *ang, uint64_t g, double2 U[4])
+// the perturbed angles of gate g: ang[s] + sigma z(draw(seed, OPNOISE, g, s)) (R12-R13)
+void noisy_angles(const Handle *h, int kind, const double *ang, uint64_t g, double a[4])
 {
-    double a[4] = {0, 0, 0, 0};
+    for (int s = 0; s < 4; ++s) a[s] = 0.0;
     const int na = kind_nangles(kind);
     for (int s = 0; s < na; ++s) {
         a[s] = ang[s];
@@ -190,6 +191,12 @@ void angle_matrix(const Handle *h, int kind, const double *ang, uint64_t g, doub
             a[s] += h->sigma * z;
         }
     }
+}
+
+void angle_matrix(const Handle *h, int kind, const double *ang, uint64_t g, double2 U[4])
+{
+    double a[4];
+    noisy_angles(h, kind, ang, g, a);
     double2 A[4], B[4], C[4];
     if (kind == QSIM_GATE_RP) {
         mat_ur(a[0], A); mat_up1(a[1], B); mat_mul(A, B, U);
@@ -369,7 +376,22 @@ TilePass make_pass(const Handle *h, const std::vector<int> &tile_pos, const std:
 // run stays contiguous, so each pass is one <= 5-D TMA box per tile.
 // Several ranks: before each pass the block's wires are made local (shard
 // exchanges), passes run in place, and the closing swaps are a relabelling.
-int fused_range(const Ranks &R, int lo, int m, int qft, int inverse)
+// The QFT circuit with per-gate data (operational error, PAPER.md:540-569;
+// approximate QFT) in the wire numbering of fused_range:
+// H[w] = the matrix of H(lo+w), phi[i][k] / e[i][k] (i < k) = the angle /
+// phase factor of the R between wires i and k (0 when the gate is absent).
+struct GenCircuit {
+    int m;
+    std::vector<double> Hr;   // 4 m: H(lo+w) = Hr[w] diag(1, e^{i hph[w]})
+    std::vector<double> hph;  // m
+    std::vector<double> phi;  // m m
+    std::vector<double2> e;   // m m
+};
+
+constexpr int kGenInfeasible = 1000;   // dry run: a pass the generalised kernel cannot take
+
+int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCircuit *gc = nullptr,
+                bool dry = false, bool even = false)
 {
     // default 7: a 2^12 tile then carries >= 5 passive bits, i.e. 512-byte runs, which
     // the TMA streams at ~96% of HBM peak (10 wires -> 64-byte runs, ~70%)
@@ -380,7 +402,7 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse)
     std::vector<int> gsize(G, m / G);
     for (int g = 0; g < m % G; ++g) gsize[g]++;
     const bool block_moves = qft && h0->world == 1;
-    if (block_moves && G > 1 && gsize[0] < amax) {
+    if (block_moves && G > 1 && gsize[0] < amax && !even) {
         // the first block lands on the lowest positions; with >= 7 wires its
         // last register window stays clear of the 3 lowest, so the store keeps
         // 128-byte thread runs and the pass fits the specialised kernel
@@ -454,7 +476,29 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse)
                 }
             }
             plan_tile_maps(tp);
-            if (moved_fixed) {
+            if (gc) {
+                if (dry) {
+                    if (!qft_gen_feasible(h, tp)) return kGenInfeasible;
+                    continue;
+                }
+                QftGen gg;
+                std::memset(&gg, 0, sizeof gg);
+                for (int u = 0; u < a; ++u) {
+                    const int w = a0 + u;
+                    for (int k = 0; k < 4; ++k) gg.Hr[u][k] = gc->Hr[4 * w + k];
+                    gg.hph[u] = gc->hph[w];
+                    for (int u2 = 0; u2 < u; ++u2) gg.ein[u][u2] = gc->e[(a0 + u2) * m + w];
+                    for (int i = 0; i < a0; ++i) gg.phe[u][i] = gc->phi[i * m + w];
+                }
+                double2 *out = h->psi;
+                if (moved_fixed) {
+                    if (ensure_scratch(h)) return QSIM_ENOMEM;
+                    out = h->scratch;
+                }
+                if (!launch_qft_gen_tma(h, tp, gg, h->psi, out))
+                    return fail(h, QSIM_ECUDA, "generalised QFT pass geometry changed after the dry run");
+                if (moved_fixed) swap_buffers(h);
+            } else if (moved_fixed) {
                 if (ensure_scratch(h)) return QSIM_ENOMEM;
                 launch_tile_pass(h, tp, h->psi, h->scratch);
                 swap_buffers(h);
@@ -1054,6 +1098,68 @@ static int qft_gates(qsim_t *h, const Ranks &R, int lo, int m, int band, int inv
     return QSIM_OK;
 }
 
+// qft_gates(h, R, lo, m, band, inverse, count = true) as fused passes
+// (k_qft_gen): the matrices and angles the gate-by-gate path would apply --
+// the same Philox draws, in the same gate-counter order -- handed to the
+// generalised kernel.  Returns 1 (nothing done) when the register does not
+// fit the pass geometry; the caller then runs qft_gates.
+static int fused_qft_gen(qsim_t *h, const Ranks &R, int lo, int m, int band, int inverse)
+{
+    static const bool off = getenv("QSIM_NO_QFT_GEN") != nullptr;
+    if (off || h->world != 1 || R.size() != 1 || h->batch_b > 0 || !h->fuse || h->nl < 9 || m > h->nl || m < 4 ||
+        m > kGenEarly)
+        return 1;
+    // geometry first (no state change besides the canonical relabel fused_range does anyway)
+    GenCircuit gc;
+    gc.m = m;
+    bool even = false;
+    int rc = fused_range(R, lo, m, 1, inverse, &gc, true, false);
+    if (rc == kGenInfeasible) {
+        even = true;
+        rc = fused_range(R, lo, m, 1, inverse, &gc, true, true);
+    }
+    if (rc == kGenInfeasible) return 1;
+    if (rc) return lift(h, R, rc);
+    const double sgn = inverse ? -1.0 : 1.0;
+    const double r = M_SQRT1_2;
+    const bool noisy = h->sigma > 0.0;
+    gc.Hr.assign(4 * m, 0.0);
+    gc.hph.assign(m, 0.0);
+    gc.phi.assign((size_t)m * m, 0.0);
+    gc.e.assign((size_t)m * m, make_double2(1, 0));
+    uint64_t g = h->gcount;
+    for (int j = 0; j < m; ++j) {
+        // H = RP(pi/4, pi) = U_R(a0) U_P1(a1) = [[c, -s], [s, c]] diag(1, e^{i a1}) (R14)
+        double Hr[4] = {r, r, r, -r}, ph = 0.0;
+        if (noisy) {
+            const double ang[2] = {M_PI / 4.0, M_PI};
+            double a[4];
+            noisy_angles(h, QSIM_GATE_RP, ang, g, a);
+            const double c = std::cos(a[0]), s = std::sin(a[0]);
+            Hr[0] = c; Hr[1] = -s; Hr[2] = s; Hr[3] = c;
+            ph = a[1];
+        }
+        g++;
+        for (int k = 0; k < 4; ++k) gc.Hr[4 * j + k] = Hr[k];
+        gc.hph[j] = ph;
+        for (int k = j + 1; k < m; ++k) {
+            if (k - j > band) continue;
+            double phi = sgn * M_PI / std::ldexp(1.0, k - j);
+            if (noisy) {
+                double a[4];
+                noisy_angles(h, QSIM_GATE_P1, &phi, g, a);
+                phi = a[0];
+            }
+            gc.e[(size_t)j * m + k] = make_double2(std::cos(phi), std::sin(phi));
+            gc.phi[(size_t)j * m + k] = phi;
+            g++;
+        }
+    }
+    if ((rc = fused_range(R, lo, m, 1, inverse, &gc, false, even))) return lift(h, R, rc);
+    h->gcount = g;
+    return QSIM_OK;
+}
+
 int qsim_qft(qsim_t *h, int lo, int m, int inverse)
 {
     QS_CHECK_HANDLE(h);
@@ -1064,6 +1170,11 @@ int qsim_qft(qsim_t *h, int lo, int m, int inverse)
         // noiseless: fused passes (constant gates, R25)
         h->gcount += (uint64_t)m + (uint64_t)m * (m - 1) / 2;
         return lift(h, R, fused_range(R, lo, m, 1, inverse));
+    }
+    if (h->sigma > 0.0) {
+        // operational error: the perturbed gates as fused passes when the geometry allows
+        const int rc = fused_qft_gen(h, R, lo, m, m, inverse);
+        if (rc != 1) return rc;
     }
     // noisy, or fusion off (the paper's one sweep per gate)
     return qft_gates(h, R, lo, m, m, inverse, true);
@@ -1085,7 +1196,10 @@ int qsim_aqft(qsim_t *h, int lo, int m, int b, int inverse)
     if (lo < 0 || m < 0 || lo + m > h->n || b < 0) return fail(h, QSIM_ERANGE, "range outside [0, n) or b < 0");
     if (m == 0) return QSIM_OK;
     if (b >= m - 1) return qsim_qft(h, lo, m, inverse);
-    return qft_gates(h, ranks_of(h), lo, m, b, inverse, true);
+    const Ranks R = ranks_of(h);
+    const int rc = fused_qft_gen(h, R, lo, m, b, inverse);
+    if (rc != 1) return rc;
+    return qft_gates(h, R, lo, m, b, inverse, true);
 }
 
 int qsim_phase_flip(qsim_t *h, uint64_t idx)

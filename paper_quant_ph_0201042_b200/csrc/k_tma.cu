@@ -412,6 +412,234 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Generalised QFT pass (QftGen, qsim_internal.h): the block / window /
+// pipeline structure of k_qft_tma, with per-gate data instead of exact roots
+// of unity -- noisy H matrices (real 2x2 after their column phase) and noisy
+// or missing R_d.  All phases on b_u = 1 before H(u) from outside the pass
+// (H's column phase, the R gates of earlier blocks) are one diagonal applied
+// at load time: exp(i theta_u), theta_u = hph[u] + the angles of the early
+// wires set in this thread (computed once) + those set in the tile id (one
+// sincos per wire per tile, shared by the CTA through shared memory).  The
+// in-block R gates follow k_qft_tma: a per-thread factor for the thread bits
+// and per-slot factors for the window bits, applied once per amplitude.
+template <int A>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_qft_gen(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
+              const __grid_constant__ TilePass tp, const __grid_constant__ TmaArgs ta,
+              const __grid_constant__ QftGen g, uint64_t ntiles)
+{
+    static_assert(kRegBits == 4 && kTmaTileBits == 12 && A >= 4 && A <= 10, "window layout");
+    constexpr int NST = (A + 3) / 4;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    double2 *bufs = reinterpret_cast<double2 *>(smem_raw);
+    double2 *tileE = bufs + kStages * (1u << kTmaTileBits);   // [2][kGenWires]
+    uint64_t *full = reinterpret_cast<uint64_t *>(tileE + 2 * kGenWires);
+    const uint32_t tid = threadIdx.x;
+    // e^{i (angles of the early wires on fixed bits set in tile T)} for wire tid
+    auto tile_phase = [&](uint64_t T, int slot) {
+        double th = 0.0;
+        for (int e = 0; e < tp.n_ef; ++e)
+            if ((T >> tp.ef_bit[e]) & 1u) th += g.phe[tid][tp.ef_w[e]];
+        double sn, cs;
+        sincos(th, &sn, &cs);
+        tileE[slot * kGenWires + tid] = make_double2(cs, sn);
+    };
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid < A && blockIdx.x < ntiles) tile_phase(blockIdx.x, 0);
+    __syncthreads();
+    if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&in_map) : "memory");
+        for (uint64_t q = 0; q < kStages - 1; ++q) {
+            const uint64_t T = blockIdx.x + q * gridDim.x;
+            if (T >= ntiles) break;
+            int c[5];
+            coords(ta.in_first, ta.in_len, T, c);
+            mbar_expect_tx(&full[q], kTileBytes);
+            tma_load(bufs + (size_t)q * (1u << kTmaTileBits), &in_map, c, &full[q]);
+        }
+    }
+    constexpr int tb = kTmaTileBits - kRegBits;
+    uint32_t tpart[NST], stp[NST];
+#pragma unroll
+    for (int m = 0; m < NST; ++m) {
+        tpart[m] = thread_part(tp.map[m], tb, tid);
+        stp[m] = swz(tpart[m]);
+    }
+    uint32_t lin = 0, lout = 0;
+    for (int t = 0; t < tb; ++t) {
+        lin |= ((tid >> t) & 1u) << ta.in_rank[tp.map[0].order[t]];
+        lout |= ((tid >> t) & 1u) << ta.out_rank[tp.map[NST - 1].order[t]];
+    }
+    uint32_t pin[kRegBits], pout[kRegBits];
+#pragma unroll
+    for (int b = 0; b < kRegBits; ++b) {
+        pin[b] = 1u << ta.in_rank[tp.map[0].win[b]];
+        pout[b] = 1u << ta.out_rank[tp.map[NST - 1].win[b]];
+    }
+    // per thread: theta_u without the tile part; wires 4.. (thread bits of
+    // map 0) summed into one factor, wires 0..3 (map 0's window) kept apart
+    double2 thrE[4], athr;
+    {
+        double thw[A];
+#pragma unroll
+        for (int u = 0; u < A; ++u) {
+            double s = g.hph[u];
+            for (int e = 0; e < tp.n_et; ++e)
+                if ((tpart[0] >> tp.et_bit[e]) & 1u) s += g.phe[u][tp.et_w[e]];
+            for (int i = 0; i < kGenEarly && i < 64; ++i)
+                if ((tp.y_const >> i) & 1u) s += g.phe[u][i];
+            thw[u] = s;
+        }
+        double sa = 0.0;
+#pragma unroll
+        for (int u = 4; u < A; ++u)
+            if ((tpart[0] >> u) & 1u) sa += thw[u];
+        double sn, cs;
+        sincos(sa, &sn, &cs);
+        athr = make_double2(cs, sn);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            sincos(thw[u], &sn, &cs);
+            thrE[u] = make_double2(cs, sn);
+        }
+    }
+    // per thread: in-block phases of the earlier wires that are thread bits of
+    // the wire's own map (windows >= 1)
+    double2 pth[A > 4 ? A : 5];
+#pragma unroll
+    for (int u = 4; u < A; ++u) {
+        const int s = u / 4;
+        const int w0 = (4 * s + 4 <= A) ? 4 * s : A - 4;
+        double2 p = make_double2(1.0, 0.0);
+        for (int u2 = 0; u2 < w0; ++u2)
+            if ((tpart[s] >> u2) & 1u) p = cmul(p, g.ein[u][u2]);
+        pth[u] = p;
+    }
+
+    uint64_t j = 0;
+    for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x, ++j) {
+        const int st = (int)(j % kStages);
+        double2 *buf = bufs + (size_t)st * (1u << kTmaTileBits);
+        // outer phases: slot k gets athr * prod(tile part of thread wires) * prod_{b in k} e_b
+        double2 f[NS];
+        {
+            const double2 *tE = tileE + (j & 1) * kGenWires;
+            double2 at = athr;
+#pragma unroll
+            for (int u = 4; u < A; ++u) {
+                const double2 x = tE[u];
+                const bool on = (tpart[0] >> u) & 1u;
+                at = cmul(at, make_double2(on ? x.x : 1.0, on ? x.y : 0.0));
+            }
+            f[0] = at;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const double2 eb = cmul(thrE[b], tE[b]);
+#pragma unroll
+                for (int q = 0; q < (1 << b); ++q) f[q | (1 << b)] = cmul(f[q], eb);
+            }
+        }
+        const uint64_t Tn = T + gridDim.x;
+        if (tid < A && Tn < ntiles) tile_phase(Tn, (int)((j + 1) & 1));
+        mbar_wait(&full[st], (uint32_t)((j / kStages) & 1));
+        double2 v[NS];
+        {
+            uint32_t o[NS];
+            o[0] = lin;
+#pragma unroll
+            for (int b = 0; b < kRegBits; ++b)
+#pragma unroll
+                for (int q = 0; q < (1 << b); ++q) o[q | (1 << b)] = o[q] | pin[b];
+#pragma unroll
+            for (int k = 0; k < NS; ++k) v[k] = cmul(buf[o[k]], f[k]);
+        }
+#pragma unroll
+        for (int s = 0; s < NST; ++s) {
+            if (s > 0) {
+                uint32_t o[NS];
+                o[0] = stp[s - 1];
+#pragma unroll
+                for (int b = 0; b < kRegBits; ++b)
+#pragma unroll
+                    for (int q = 0; q < (1 << b); ++q) o[q | (1 << b)] = o[q] ^ tp.wswz[s - 1][b];
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < NS; ++k) buf[o[k]] = v[k];
+                o[0] = stp[s];
+#pragma unroll
+                for (int b = 0; b < kRegBits; ++b)
+#pragma unroll
+                    for (int q = 0; q < (1 << b); ++q) o[q | (1 << b)] = o[q] ^ tp.wswz[s][b];
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < NS; ++k) v[k] = buf[o[k]];
+            }
+            const int w0 = (4 * s + 4 <= A) ? 4 * s : A - 4;
+#pragma unroll
+            for (int rb = 0; rb < 4; ++rb) {
+                const int u = w0 + rb;
+                if (u < 4 * s) continue;   // carried wire (already transformed)
+                // in-block R gates of the earlier wires: factor F[lower window bits]
+                if (u >= 4 || rb > 0) {
+                    double2 F[1 << 3];
+                    F[0] = u >= 4 ? pth[u] : make_double2(1.0, 0.0);
+#pragma unroll
+                    for (int r2 = 0; r2 < rb; ++r2) {
+                        const double2 E = g.ein[u][w0 + r2];
+#pragma unroll
+                        for (int q = 0; q < (1 << r2); ++q) F[q | (1 << r2)] = cmul(F[q], E);
+                    }
+#pragma unroll
+                    for (int k = 0; k < NS; ++k) {
+                        if (!(k & (1 << rb))) continue;
+                        const int q = k & ((1 << rb) - 1);
+                        if (u < 4 && q == 0) continue;   // factor 1
+                        v[k] = cmul(v[k], F[q]);
+                    }
+                }
+                const double h0 = g.Hr[u][0], h1 = g.Hr[u][1], h2 = g.Hr[u][2], h3 = g.Hr[u][3];
+#pragma unroll
+                for (int k = 0; k < NS; ++k) {
+                    if (k & (1 << rb)) continue;
+                    const double2 x = v[k], y = v[k | (1 << rb)];
+                    v[k] = make_double2(fma(h0, x.x, h1 * y.x), fma(h0, x.y, h1 * y.y));
+                    v[k | (1 << rb)] = make_double2(fma(h2, x.x, h3 * y.x), fma(h2, x.y, h3 * y.y));
+                }
+            }
+        }
+        {
+            uint32_t o[NS];
+            o[0] = lout;
+#pragma unroll
+            for (int b = 0; b < kRegBits; ++b)
+#pragma unroll
+                for (int q = 0; q < (1 << b); ++q) o[q | (1 << b)] = o[q] | pout[b];
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < NS; ++k) buf[o[k]] = v[k];
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            int c[5];
+            coords(ta.out_first, ta.out_len, T, c);
+            tma_store(&out_map, c, buf);
+            bulk_wait_read<1>();
+            const uint64_t Tn2 = T + (uint64_t)(kStages - 1) * gridDim.x;
+            if (Tn2 < ntiles) {
+                const int sn = (int)((j + kStages - 1) % kStages);
+                coords(ta.in_first, ta.in_len, Tn2, c);
+                mbar_expect_tx(&full[sn], kTileBytes);
+                tma_load(bufs + (size_t)sn * (1u << kTmaTileBits), &in_map, c, &full[sn]);
+            }
+        }
+    }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // Gate-list pass on the TMA pipeline (in place), for passes whose FP64 work
 // hides under the transfer: tiles stream in by TMA while the previous tile's
 // segments run in registers (ops_common.cuh, transposes in the stage buffer),
@@ -668,6 +896,72 @@ bool launch_tile_pass_tma(Handle *h, const TilePass &tp_in, const double2 *in, d
     case 4: launch_tma_nm<4>(h, im, om, tp, ta); break;
     case 5: launch_tma_nm<5>(h, im, om, tp, ta); break;
     default: launch_tma_nm<6>(h, im, om, tp, ta); break;
+    }
+    return true;
+}
+
+template <int A>
+void launch_gen_a(Handle *h, const CUtensorMap &im, const CUtensorMap &om, const TilePass &tp, const TmaArgs &ta,
+                  const QftGen &g)
+{
+    const size_t smem = (size_t)kStages * kTileBytes + 2 * kGenWires * sizeof(double2) + kStages * sizeof(uint64_t);
+    static uint64_t attr = 0;
+    if (first_use_on_device(attr))
+        cudaFuncSetAttribute(k_qft_gen<A>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const uint64_t ntiles = 1ull << tp.nfix;
+    const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)h->num_sms);
+    prof_begin(h);
+    k_qft_gen<A><<<grid, kThreads, smem, h->stream>>>(im, om, tp, ta, g, ntiles);
+    prof_end(h, "k_qft_gen", (1ull << (tp.tbits + tp.nfix)) * 32);
+}
+
+// geometry of a generalised pass: tensor maps and the specialised window layout
+static bool gen_geometry(Handle *h, const TilePass &tp_in, const double2 *in, double2 *out, TilePass &tp,
+                         CUtensorMap &im, CUtensorMap &om, TmaArgs &ta)
+{
+    if (tp_in.tbits != kTmaTileBits || getenv("QSIM_NO_TMA")) return false;
+    tp = tp_in;
+    finish_tile_pass(tp);
+    const int nst = (tp.a + 3) / 4;
+    if (tp.a < 4 || tp.a > kGenWires || tp.nmaps != nst || !tp.twiddle_fast) return false;
+    for (int e = 0; e < tp.n_et; ++e) if (tp.et_w[e] >= kGenEarly) return false;
+    for (int e = 0; e < tp.n_ef; ++e) if (tp.ef_w[e] >= kGenEarly) return false;
+    if (tp.y_const >> kGenEarly) return false;
+    std::vector<int> fid_in(h->nl, -1), fid_out(h->nl, -1);
+    for (int f = 0; f < tp.nfix; ++f) {
+        fid_in[tp.fin_pos[f]] = f;
+        fid_out[tp.fout_pos[f]] = f;
+    }
+    std::vector<int> tin(tp.in_pos, tp.in_pos + tp.tbits), tout(tp.out_pos, tp.out_pos + tp.tbits);
+    std::memset(&ta, 0, sizeof ta);
+    if (!build_side(in, h->nl, tin, fid_in, im, ta.in_first, ta.in_len, ta.in_rank)) return false;
+    if (!build_side(out, h->nl, tout, fid_out, om, ta.out_first, ta.out_len, ta.out_rank)) return false;
+    return true;
+}
+
+bool qft_gen_feasible(Handle *h, const TilePass &tp_in)
+{
+    TilePass tp;
+    CUtensorMap im, om;
+    TmaArgs ta;
+    return gen_geometry(h, tp_in, h->psi, h->psi, tp, im, om, ta);
+}
+
+bool launch_qft_gen_tma(Handle *h, const TilePass &tp_in, const QftGen &g, const double2 *in, double2 *out)
+{
+    cudaSetDevice(h->device);
+    TilePass tp;
+    CUtensorMap im, om;
+    TmaArgs ta;
+    if (!gen_geometry(h, tp_in, in, out, tp, im, om, ta)) return false;
+    switch (tp.a) {
+    case 4: launch_gen_a<4>(h, im, om, tp, ta, g); break;
+    case 5: launch_gen_a<5>(h, im, om, tp, ta, g); break;
+    case 6: launch_gen_a<6>(h, im, om, tp, ta, g); break;
+    case 7: launch_gen_a<7>(h, im, om, tp, ta, g); break;
+    case 8: launch_gen_a<8>(h, im, om, tp, ta, g); break;
+    case 9: launch_gen_a<9>(h, im, om, tp, ta, g); break;
+    default: launch_gen_a<10>(h, im, om, tp, ta, g); break;
     }
     return true;
 }

@@ -131,6 +131,29 @@ void finish_tile_pass(TilePass &tp);
 // TMA-pipelined variant (k_tma.cu); false = geometry unsupported, nothing launched
 bool launch_tile_pass_tma(Handle *h, const TilePass &tp, const double2 *in, double2 *out);
 
+// Generalised QFT pass (k_tma.cu k_qft_gen): the same block structure with
+// arbitrary per-gate data -- the noisy H matrices and R_d angles of a circuit
+// with operational error or the R_d of an approximate QFT
+// left out.  Active wire u (tile bit u) of the pass:
+// before its H, the amplitudes with b_u = 1 get exp(i (hph[u] + sum_{earlier
+// wires i, y_i = 1} phe[u][i])) (H's column phase and the earlier blocks: a
+// twiddle per tile) times prod_{u' < u, b_u' = 1} ein[u][u'] (this block);
+// then the real 2x2 Hr[u].  Every H of the paper's circuits has this form:
+// U_R(t) U_P1(p) = [[c, -s e^{ip}], [s, c e^{ip}]] and the
+// exact H (t = pi/4, p = pi) with the phase folded into the real part.
+// phe[u][i] = angle of R(a0+u, i), ein[u][u'] = e^{i angle of R(a0+u, a0+u')}.
+constexpr int kGenWires = 10;
+constexpr int kGenEarly = 48;
+struct QftGen {
+    double Hr[kGenWires][4];
+    double hph[kGenWires];
+    double2 ein[kGenWires][kGenWires];
+    double phe[kGenWires][kGenEarly];
+};
+// true: launched; false: the pass geometry does not fit the kernel (nothing launched)
+bool launch_qft_gen_tma(Handle *h, const TilePass &tp, const QftGen &g, const double2 *in, double2 *out);
+bool qft_gen_feasible(Handle *h, const TilePass &tp);
+
 // Fused gate-list passes (k_ops.cu): ops of one pass, applied per tile.
 // Op kinds (encoded per segment on the host, so the kernel's per-op work is
 // a few uniform tests and statically indexed register updates):

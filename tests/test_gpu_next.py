@@ -121,6 +121,45 @@ def test_aqft_fidelity_against_exact_qft_via_inner(mk):
     assert f == pytest.approx(1.0, abs=1e-12)
 
 
+# ------------------------------------------------------------------ noisy QFT as fused passes
+@pytest.mark.parametrize("n,lo,m,inverse", [(18, 0, 18, False), (18, 3, 12, True), (20, 0, 20, False),
+                                            (12, 0, 9, False), (15, 2, 13, True), (11, 0, 8, False),
+                                            (22, 1, 21, True)])
+def test_noisy_qft_fused_matches_oracle(mk, n, lo, m, inverse):
+    """Operational error on every H and R_d of the QFT: the
+    generalised fused passes (k_qft_gen) against the oracle's gate-by-gate
+    circuit with the same Philox draws, and the gate counter advanced by the
+    number of gates."""
+    psi = rand_state(n, 5 * n + m)
+    h = mk(n, psi)
+    Q.qsim_set_gate_noise(h, 11, 2e-2)
+    Q.qsim_set_gate_counter(h, 100)
+    Q.qsim_qft(h, lo, m, inverse)
+    ref = psi.copy()
+    nz = O.Noise(seed=11, sigma=2e-2, g=100)
+    O.qft(ref, lo, m, inverse, noise=nz)
+    assert maxdiff(get(h, n), ref) < TOL
+    assert Q.qsim_get_gate_counter(h) == nz.g
+
+
+def test_noisy_qft_fused_equals_unfused_after_gates(mk):
+    """A non-canonical layout (gates queued, swaps relabelled) before the noisy
+    QFT: fused passes and the one-sweep-per-gate path give the same state."""
+    n = 19
+    psi = rand_state(n, 77)
+    out = []
+    for fuse in (True, False):
+        h = mk(n, psi)
+        Q.qsim_set_fusion(h, fuse)
+        Q.qsim_set_gate_noise(h, 3, 1e-2)
+        Q.qsim_swap(h, 0, 7)
+        Q.qsim_hadamard(h, 2, 5)
+        Q.qsim_qft(h, 1, 17, False)
+        Q.qsim_qft(h, 0, 19, True)
+        out.append(get(h, n))
+    assert maxdiff(out[0], out[1]) < TOL
+
+
 # ------------------------------------------------------------------ f4: partial measurement
 @pytest.mark.parametrize("world", [1, 2, 4])
 @pytest.mark.parametrize("lo,m", [(0, 3), (4, 5), (9, 5), (0, 14), (2, 1)])
