@@ -1,4 +1,4 @@
-"""Run one config once (for ncu captures): python tools/run_cfg.py 3n|4|4s"""
+"""Run one config once (for ncu captures): python tools/run_cfg.py 3n|4|4m|4s"""
 import os
 import sys
 
@@ -13,6 +13,9 @@ if w == "3n":
 elif w == "4s":
     h = Q.qsim_create(26)
     W.run_cfg4(h, 26, 20, 5, 1e-3, 1e-4)
+elif w == "4m":
+    h = Q.qsim_create(30)
+    W.run_cfg4(h, 30, 20, 5, 1e-3, 1e-4)
 elif w == "4":
     h = Q.qsim_create(32)
     W.run_cfg4(h, 32, 20, 5, 1e-3, 1e-4)
