@@ -26,6 +26,55 @@ __device__ __forceinline__ double2 cfma2(double2 u, double2 x, double2 v, double
     return make_double2(re, im);
 }
 
+// (x, y) <- (u0 x + u1 y, u2 x + u3 y) in place.  Written in PTX with in-out
+// operands so the results land in the slots' own registers: the op
+// interpreter joins every op's code path at the loop head, and a result left
+// in a temporary costs a register move per double there (the compiler cannot
+// overwrite x while y' still needs it; here the y parts of both outputs are
+// formed first, then y', then x' with x read by the instruction that
+// overwrites it).  16 FP64 instructions, as in cfma2.
+__device__ __forceinline__ void pair_inplace(double2 &x, double2 &y, double2 u0, double2 u1, double2 u2, double2 u3)
+{
+    asm("{\n\t.reg .f64 tr, ti, sr, si, ir, ii, q;\n\t"
+        "mul.rn.f64 tr, %6, %2;\n\t"
+        "neg.f64 q, %7;\n\t"
+        "fma.rn.f64 tr, q, %3, tr;\n\t"
+        "mul.rn.f64 ti, %6, %3;\n\t"
+        "fma.rn.f64 ti, %7, %2, ti;\n\t"
+        "mul.rn.f64 sr, %10, %2;\n\t"
+        "neg.f64 q, %11;\n\t"
+        "fma.rn.f64 sr, q, %3, sr;\n\t"
+        "mul.rn.f64 si, %10, %3;\n\t"
+        "fma.rn.f64 si, %11, %2, si;\n\t"
+        "fma.rn.f64 %2, %8, %0, sr;\n\t"
+        "neg.f64 q, %9;\n\t"
+        "fma.rn.f64 %2, q, %1, %2;\n\t"
+        "fma.rn.f64 %3, %8, %1, si;\n\t"
+        "fma.rn.f64 %3, %9, %0, %3;\n\t"
+        "neg.f64 q, %5;\n\t"
+        "fma.rn.f64 ir, q, %1, tr;\n\t"
+        "fma.rn.f64 ii, %5, %0, ti;\n\t"
+        "fma.rn.f64 %0, %4, %0, ir;\n\t"
+        "fma.rn.f64 %1, %4, %1, ii;\n\t"
+        "}"
+        : "+d"(x.x), "+d"(x.y), "+d"(y.x), "+d"(y.y)
+        : "d"(u0.x), "d"(u0.y), "d"(u1.x), "d"(u1.y), "d"(u2.x), "d"(u2.y), "d"(u3.x), "d"(u3.y));
+}
+
+// x <- d x in place (see pair_inplace)
+__device__ __forceinline__ void cmul_inplace(double2 &x, double2 d)
+{
+    asm("{\n\t.reg .f64 t, u, q;\n\t"
+        "mul.rn.f64 t, %3, %1;\n\t"
+        "mul.rn.f64 u, %3, %0;\n\t"
+        "neg.f64 q, t;\n\t"
+        "fma.rn.f64 %0, %2, %0, q;\n\t"
+        "fma.rn.f64 %1, %2, %1, u;\n\t"
+        "}"
+        : "+d"(x.x), "+d"(x.y)
+        : "d"(d.x), "d"(d.y));
+}
+
 // dense 2x2 (u0 u1; u2 u3) on window bit B for every slot pair whose window
 // controls (wm, wv) match
 template <int B, bool WC>
@@ -36,9 +85,7 @@ __device__ __forceinline__ void dense_rb(double2 (&v)[NS5], double2 u0, double2 
     for (int k = 0; k < NS5; ++k) {
         if (k & (1 << B)) continue;
         if (WC && ((k & wm) != wv)) continue;
-        const double2 x = v[k], y = v[k | (1 << B)];
-        v[k] = cfma2(u0, x, u1, y);
-        v[k | (1 << B)] = cfma2(u2, x, u3, y);
+        pair_inplace(v[k], v[k | (1 << B)], u0, u1, u2, u3);
     }
 }
 
@@ -50,9 +97,7 @@ __device__ __forceinline__ void cdense_rb(double2 (&v)[NS5], double2 u0, double2
     for (int k = 0; k < NS5; ++k) {
         if (k & (1 << B)) continue;
         if (((k >> C) & 1) != CV) continue;
-        const double2 x = v[k], y = v[k | (1 << B)];
-        v[k] = cfma2(u0, x, u1, y);
-        v[k | (1 << B)] = cfma2(u2, x, u3, y);
+        pair_inplace(v[k], v[k | (1 << B)], u0, u1, u2, u3);
     }
 }
 
@@ -66,9 +111,7 @@ __device__ __forceinline__ void dense2_rb(double2 (&v)[NS5], const GOp &op)
     for (int k = 0; k < NS5; ++k) {
         if (k & (1 << B)) continue;
         const bool s = (k >> C) & 1;
-        const double2 x = v[k], y = v[k | (1 << B)];
-        v[k] = cfma2(s ? b0 : a0, x, s ? b1 : a1, y);
-        v[k | (1 << B)] = cfma2(s ? b2 : a2, x, s ? b3 : a3, y);
+        pair_inplace(v[k], v[k | (1 << B)], s ? b0 : a0, s ? b1 : a1, s ? b2 : a2, s ? b3 : a3);
     }
 }
 
@@ -79,8 +122,8 @@ __device__ __forceinline__ void diag_rb(double2 (&v)[NS5], double2 d0, double2 d
 #pragma unroll
     for (int k = 0; k < NS5; ++k) {
         if (WC && ((k & wm) != wv)) continue;
-        if (k & (1 << B)) v[k] = cmul(v[k], d1);
-        else if (!D0ONE) v[k] = cmul(v[k], d0);
+        if (k & (1 << B)) cmul_inplace(v[k], d1);
+        else if (!D0ONE) cmul_inplace(v[k], d0);
     }
 }
 
@@ -90,7 +133,7 @@ __device__ __forceinline__ void phase_all(double2 (&v)[NS5], double2 d, uint32_t
 #pragma unroll
     for (int k = 0; k < NS5; ++k) {
         if (WC && ((k & wm) != wv)) continue;
-        v[k] = cmul(v[k], d);
+        cmul_inplace(v[k], d);
     }
 }
 
