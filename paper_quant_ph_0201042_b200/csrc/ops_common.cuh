@@ -137,109 +137,81 @@ __device__ __forceinline__ void phase_all(double2 (&v)[NS5], double2 d, uint32_t
     }
 }
 
-template <int B>
-__device__ __forceinline__ void dense_any(double2 (&v)[NS5], double2 u0, double2 u1, double2 u2, double2 u3,
-                                          uint32_t wm, uint32_t wv)
-{
-    if (wm) dense_rb<B, true>(v, u0, u1, u2, u3, wm, wv);
-    else dense_rb<B, false>(v, u0, u1, u2, u3, 0, 0);
-}
-
-template <int B>
-__device__ __forceinline__ void diag_any(double2 (&v)[NS5], double2 d0, double2 d1, uint32_t wm, uint32_t wv)
-{
-    const bool one = d0.x == 1.0 && d0.y == 0.0;
-    if (wm) {
-        if (one) diag_rb<B, true, true>(v, d0, d1, wm, wv);
-        else diag_rb<B, true, false>(v, d0, d1, wm, wv);
-    } else {
-        if (one) diag_rb<B, false, true>(v, d0, d1, 0, 0);
-        else diag_rb<B, false, false>(v, d0, d1, 0, 0);
-    }
-}
-
-#define QS_CD(B, C)                                                            \
-    case (B) * 16 + (C) * 2 + 0: cdense_rb<B, C, 0>(v, u0, u1, u2, u3); break; \
-    case (B) * 16 + (C) * 2 + 1: cdense_rb<B, C, 1>(v, u0, u1, u2, u3); break;
+#define QS_RB5(BASE, F)                        \
+    case (BASE) + 0: F(0); break;              \
+    case (BASE) + 1: F(1); break;              \
+    case (BASE) + 2: F(2); break;              \
+    case (BASE) + 3: F(3); break;              \
+    case (BASE) + 4: F(4); break;
+#define QS_CD(B, C)                                                                              \
+    case OPC_CDENSE + (B) * 10 + (C) * 2 + 0: cdense_rb<B, C, 0>(v, u0, u1, u2, u3); break;    \
+    case OPC_CDENSE + (B) * 10 + (C) * 2 + 1: cdense_rb<B, C, 1>(v, u0, u1, u2, u3); break;
 #define QS_D2(B, C) \
-    case (B) * 8 + (C): dense2_rb<B, C>(v, op); break;
+    case OPC_DENSE2 + (B) * 5 + (C): dense2_rb<B, C>(v, op); break;
+#define QS_DW(B)                                                                                   \
+    case OPC_DIAGW + (B) * 4 + 0: diag_rb<B, false, false>(v, op.u[0], op.u[3], 0, 0); break;       \
+    case OPC_DIAGW + (B) * 4 + 1: diag_rb<B, false, true>(v, op.u[0], op.u[3], 0, 0); break;        \
+    case OPC_DIAGW + (B) * 4 + 2: diag_rb<B, true, false>(v, op.u[0], op.u[3], op.wm, op.wv); break; \
+    case OPC_DIAGW + (B) * 4 + 3: diag_rb<B, true, true>(v, op.u[0], op.u[3], op.wm, op.wv); break;
+#define QS_DN(B) dense_rb<B, false>(v, u0, u1, u2, u3, 0, 0)
+#define QS_DNW(B) dense_rb<B, true>(v, u0, u1, u2, u3, op.wm, op.wv)
 
 // One op on the 32 register slots of a thread (thread part tpart of the tile
-// index, tile id T).  Every field of op is warp-uniform.
-__device__ __forceinline__ void apply_op(double2 (&v)[NS5], const GOp &op, uint64_t T, uint32_t tpart, uint32_t traj)
+// index, tile id T).  Every field of op is warp-uniform; code = op.code,
+// fetched by the caller one op ahead, selects the case in one indexed branch.
+__device__ __forceinline__ void apply_op(double2 (&v)[NS5], const GOp &op, uint32_t code, uint64_t T, uint32_t tpart,
+                                         uint32_t traj)
 {
-    if ((T & op.fm) != op.fv) return;           // fixed-bit controls (uniform)
-    if ((tpart & op.tm) != op.tv) return;       // thread-part controls
-    const uint32_t kind = op.kind;
-    if (kind == GOP_DENSET) {
-        // this tile's trajectory matrix (one uniform 64-byte load, L1-cached)
-        const double2 *m = op.tab + 4 * (uint64_t)traj;
+    if ((code & kOpChkFixed) && (T & op.fm) != op.fv) return;          // fixed-bit controls
+    if ((code & kOpChkThread) && (tpart & op.tm) != op.tv) return;     // thread-part controls
+    const uint32_t c = code & 0xffu;
+    if (c < OPC_DENSE2) {
+        // dense forms: the matrix (u[4..7] where the selector is 1; DENSET: this
+        // tile's trajectory matrix, one uniform 64-byte load, L1-cached)
+        const double2 *m = op.u;
+        if (c >= OPC_DENSET && c < OPC_CDENSE) m = op.tab + 4 * (uint64_t)traj;
+        else if ((code & kOpSel) &&
+                 ((tpart & op.tsel) != 0 || (op.fsel != 0xffu && ((T >> op.fsel) & 1u))))
+            m = op.u + 4;
         const double2 u0 = m[0], u1 = m[1], u2 = m[2], u3 = m[3];
-        switch (op.rb) {
-        case 0: dense_any<0>(v, u0, u1, u2, u3, op.wm, op.wv); break;
-        case 1: dense_any<1>(v, u0, u1, u2, u3, op.wm, op.wv); break;
-        case 2: dense_any<2>(v, u0, u1, u2, u3, op.wm, op.wv); break;
-        case 3: dense_any<3>(v, u0, u1, u2, u3, op.wm, op.wv); break;
-        default: dense_any<4>(v, u0, u1, u2, u3, op.wm, op.wv); break;
-        }
-        return;
-    }
-    if (kind == GOP_DENSE || kind == GOP_CDENSE) {
-        // matrix u[4..7] where the selector (thread bit tsel or tile-id bit fsel) is 1
-        const bool s = (tpart & op.tsel) != 0 || (op.fsel != 0xffu && ((T >> op.fsel) & 1u));
-        const int o = s ? 4 : 0;
-        const double2 u0 = op.u[o], u1 = op.u[o + 1], u2 = op.u[o + 2], u3 = op.u[o + 3];
-        if (kind == GOP_DENSE) {
-            switch (op.rb) {
-            case 0: dense_any<0>(v, u0, u1, u2, u3, op.wm, op.wv); break;
-            case 1: dense_any<1>(v, u0, u1, u2, u3, op.wm, op.wv); break;
-            case 2: dense_any<2>(v, u0, u1, u2, u3, op.wm, op.wv); break;
-            case 3: dense_any<3>(v, u0, u1, u2, u3, op.wm, op.wv); break;
-            default: dense_any<4>(v, u0, u1, u2, u3, op.wm, op.wv); break;
-            }
-        } else {
-            switch (op.rb * 16 + op.cs * 2 + op.cv) {
-                QS_CD(0, 1) QS_CD(0, 2) QS_CD(0, 3) QS_CD(0, 4)
-                QS_CD(1, 0) QS_CD(1, 2) QS_CD(1, 3) QS_CD(1, 4)
-                QS_CD(2, 0) QS_CD(2, 1) QS_CD(2, 3) QS_CD(2, 4)
-                QS_CD(3, 0) QS_CD(3, 1) QS_CD(3, 2) QS_CD(3, 4)
-                QS_CD(4, 0) QS_CD(4, 1) QS_CD(4, 2) QS_CD(4, 3)
-            default: break;
-            }
-        }
-        return;
-    }
-    if (kind == GOP_DENSE2) {
-        switch (op.rb * 8 + op.cs) {
-            QS_D2(0, 1) QS_D2(0, 2) QS_D2(0, 3) QS_D2(0, 4)
-            QS_D2(1, 0) QS_D2(1, 2) QS_D2(1, 3) QS_D2(1, 4)
-            QS_D2(2, 0) QS_D2(2, 1) QS_D2(2, 3) QS_D2(2, 4)
-            QS_D2(3, 0) QS_D2(3, 1) QS_D2(3, 2) QS_D2(3, 4)
-            QS_D2(4, 0) QS_D2(4, 1) QS_D2(4, 2) QS_D2(4, 3)
+        switch (c) {
+            QS_RB5(OPC_DENSE, QS_DN)
+            QS_RB5(OPC_DENSE + 5, QS_DNW)
+            QS_RB5(OPC_DENSET, QS_DN)
+            QS_RB5(OPC_DENSET + 5, QS_DNW)
+            QS_CD(0, 1) QS_CD(0, 2) QS_CD(0, 3) QS_CD(0, 4)
+            QS_CD(1, 0) QS_CD(1, 2) QS_CD(1, 3) QS_CD(1, 4)
+            QS_CD(2, 0) QS_CD(2, 1) QS_CD(2, 3) QS_CD(2, 4)
+            QS_CD(3, 0) QS_CD(3, 1) QS_CD(3, 2) QS_CD(3, 4)
+            QS_CD(4, 0) QS_CD(4, 1) QS_CD(4, 2) QS_CD(4, 3)
         default: break;
         }
         return;
     }
-    if (kind == GOP_DIAGW) {
-        const double2 d0 = op.u[0], d1 = op.u[3];
-        switch (op.rb) {
-        case 0: diag_any<0>(v, d0, d1, op.wm, op.wv); break;
-        case 1: diag_any<1>(v, d0, d1, op.wm, op.wv); break;
-        case 2: diag_any<2>(v, d0, d1, op.wm, op.wv); break;
-        case 3: diag_any<3>(v, d0, d1, op.wm, op.wv); break;
-        default: diag_any<4>(v, d0, d1, op.wm, op.wv); break;
+    switch (c) {
+        QS_D2(0, 1) QS_D2(0, 2) QS_D2(0, 3) QS_D2(0, 4)
+        QS_D2(1, 0) QS_D2(1, 2) QS_D2(1, 3) QS_D2(1, 4)
+        QS_D2(2, 0) QS_D2(2, 1) QS_D2(2, 3) QS_D2(2, 4)
+        QS_D2(3, 0) QS_D2(3, 1) QS_D2(3, 2) QS_D2(3, 4)
+        QS_D2(4, 0) QS_D2(4, 1) QS_D2(4, 2) QS_D2(4, 3)
+        QS_DW(0) QS_DW(1) QS_DW(2) QS_DW(3) QS_DW(4)
+    default: {
+        const uint32_t kind = op.kind;
+        double2 d;
+        if (kind == GOP_DIAGT) d = (tpart & op.tb) ? op.u[3] : op.u[0];
+        else if (kind == GOP_DIAGF) d = ((T >> op.fbit) & 1u) ? op.u[3] : op.u[0];
+        else d = op.u[3];
+        if (!(d.x == 1.0 && d.y == 0.0)) {
+            if (op.wm) phase_all<true>(v, d, op.wm, op.wv);
+            else phase_all<false>(v, d, op.wm, op.wv);
         }
-        return;
-    }
-    double2 d;
-    if (kind == GOP_DIAGT) d = (tpart & op.tb) ? op.u[3] : op.u[0];
-    else if (kind == GOP_DIAGF) d = ((T >> op.fbit) & 1u) ? op.u[3] : op.u[0];
-    else d = op.u[3];
-    if (!(d.x == 1.0 && d.y == 0.0)) {
-        if (op.wm) phase_all<true>(v, d, op.wm, op.wv);
-        else phase_all<false>(v, d, op.wm, op.wv);
+    } break;
     }
 }
+#undef QS_RB5
+#undef QS_DW
+#undef QS_DN
+#undef QS_DNW
 #undef QS_CD
 #undef QS_D2
 
@@ -289,7 +261,13 @@ __device__ __forceinline__ void run_segments(double2 (&v)[NS5], const OpsLaunch 
                 v[k] = buf[o];
             }
         }
-        for (int i = sg.op_begin; i < sg.op_end; ++i) apply_op(v, L.ops[i], T, tpart, traj);
+        // the next op's dispatch word is fetched while this op runs
+        uint32_t code = sg.op_begin < sg.op_end ? L.ops[sg.op_begin].code : 0u;
+        for (int i = sg.op_begin; i < sg.op_end; ++i) {
+            const uint32_t c = code;
+            if (i + 1 < sg.op_end) code = L.ops[i + 1].code;
+            apply_op(v, L.ops[i], c, T, tpart, traj);
+        }
         prev_stp = stp;
 #pragma unroll
         for (int b = 0; b < RB5; ++b) prev_wsw[b] = wsw[b];

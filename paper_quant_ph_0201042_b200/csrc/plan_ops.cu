@@ -286,6 +286,27 @@ std::vector<Segment> schedule(const std::vector<POp> &ops, int nl, const std::ve
     return segs;
 }
 
+// The interpreter's dispatch word of an encoded op (qsim_internal.h OPC_*):
+// one case id for (kind, window bits, window controls) plus the run-time
+// checks the op needs, so the device takes one indexed branch per op.
+uint32_t op_code(const GOp &g)
+{
+    uint32_t c = OPC_OTHER;
+    const uint32_t wc = g.wm != 0;
+    switch (g.kind) {
+    case GOP_DENSE: c = OPC_DENSE + g.rb + 5 * wc; break;
+    case GOP_DENSET: c = OPC_DENSET + g.rb + 5 * wc; break;
+    case GOP_CDENSE: c = OPC_CDENSE + g.rb * 10 + g.cs * 2 + g.cv; break;
+    case GOP_DENSE2: c = OPC_DENSE2 + g.rb * 5 + g.cs; break;
+    case GOP_DIAGW: c = OPC_DIAGW + g.rb * 4 + 2 * wc + (g.u[0].x == 1.0 && g.u[0].y == 0.0); break;
+    default: break;
+    }
+    if (g.fm) c |= kOpChkFixed;
+    if (g.tm) c |= kOpChkThread;
+    if (g.kind == GOP_DENSE && (g.tsel != 0 || g.fsel != 0xff)) c |= kOpSel;
+    return c;
+}
+
 bool plan_log()
 {
     static const bool on = std::getenv("QSIM_PLAN_LOG") != nullptr;
@@ -559,7 +580,11 @@ int flush_queue(Handle *h)
                     std::stable_sort(rest.begin(), rest.end(), [&](int x, int y) { return tile[x] < tile[y]; });
                 for (size_t t = 0; t < rest.size(); ++t) os.order[t] = rest[t];
                 os.op_begin = P.nops;
-                for (size_t i = pieces[k].b; i < pieces[k].e; ++i) L.ops[P.nops++] = enc[pieces[k].seg][i];
+                for (size_t i = pieces[k].b; i < pieces[k].e; ++i) {
+                    GOp &g = L.ops[P.nops++];
+                    g = enc[pieces[k].seg][i];
+                    g.code = op_code(g);
+                }
                 os.op_end = P.nops;
             }
             if (plan_log()) {

@@ -181,10 +181,23 @@ struct GOp {
     uint32_t tb;       // DIAGT: mask of the target tile bit
     uint32_t fbit;     // DIAGF: tile-id bit of the target
     uint32_t tsel;     // DENSE: thread-part bit selecting u[4..7] (0: none)
-    uint32_t pad2_;
+    uint32_t code;     // dispatch word (op_code(), plan_ops.cu): case id | kOpChk* flags
     uint64_t fm, fv;   // controls on fixed bits (tile-id mask / values)
     const double2 *tab;   // DENSET: per-trajectory matrices (device memory)
     double2 u[8];      // dense U (u11 u12 u21 u22) or diag(u[0], u[3]); DENSE2: two matrices
+};
+// GOp::code: bits 0-7 the interpreter's case (ops_common.cuh apply_op), plus
+// which run-time checks the op needs
+constexpr uint32_t kOpChkFixed = 1u << 8;    // fm / fv
+constexpr uint32_t kOpChkThread = 1u << 9;   // tm / tv
+constexpr uint32_t kOpSel = 1u << 10;        // tsel / fsel matrix choice
+enum {
+    OPC_DENSE = 0,      // + rb (+5: window controls)
+    OPC_DENSET = 10,    // + rb (+5: window controls)
+    OPC_CDENSE = 20,    // + rb*10 + cs*2 + cv
+    OPC_DENSE2 = 70,    // + rb*5 + cs
+    OPC_DIAGW = 95,     // + rb*4 + 2*(window controls) + (d0 == 1)
+    OPC_OTHER = 115     // PHASE / DIAGT / DIAGF
 };
 constexpr int kMaxSegs = 48;
 constexpr int kOpsRegBits = 5;   // gate-list passes: 32 amplitudes per thread
