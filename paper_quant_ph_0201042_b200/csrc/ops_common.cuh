@@ -169,7 +169,7 @@ __device__ __forceinline__ void apply_op(double2 (&v)[NS5], const GOp &op, uint3
         // dense forms: the matrix (u[4..7] where the selector is 1; DENSET: this
         // tile's trajectory matrix, one uniform 64-byte load, L1-cached)
         const double2 *m = op.u;
-        if (c >= OPC_DENSET && c < OPC_CDENSE) m = op.tab + 4 * (uint64_t)traj;
+        if (code & kOpTraj) m = op.tab + 4 * (uint64_t)traj;
         else if ((code & kOpSel) &&
                  ((tpart & op.tsel) != 0 || (op.fsel != 0xffu && ((T >> op.fsel) & 1u))))
             m = op.u + 4;
@@ -177,8 +177,6 @@ __device__ __forceinline__ void apply_op(double2 (&v)[NS5], const GOp &op, uint3
         switch (c) {
             QS_RB5(OPC_DENSE, QS_DN)
             QS_RB5(OPC_DENSE + 5, QS_DNW)
-            QS_RB5(OPC_DENSET, QS_DN)
-            QS_RB5(OPC_DENSET + 5, QS_DNW)
             QS_CD(0, 1) QS_CD(0, 2) QS_CD(0, 3) QS_CD(0, 4)
             QS_CD(1, 0) QS_CD(1, 2) QS_CD(1, 3) QS_CD(1, 4)
             QS_CD(2, 0) QS_CD(2, 1) QS_CD(2, 3) QS_CD(2, 4)

@@ -295,7 +295,7 @@ uint32_t op_code(const GOp &g)
     const uint32_t wc = g.wm != 0;
     switch (g.kind) {
     case GOP_DENSE: c = OPC_DENSE + g.rb + 5 * wc; break;
-    case GOP_DENSET: c = OPC_DENSET + g.rb + 5 * wc; break;
+    case GOP_DENSET: c = (OPC_DENSE + g.rb + 5 * wc) | kOpTraj; break;
     case GOP_CDENSE: c = OPC_CDENSE + g.rb * 10 + g.cs * 2 + g.cv; break;
     case GOP_DENSE2: c = OPC_DENSE2 + g.rb * 5 + g.cs; break;
     case GOP_DIAGW: c = OPC_DIAGW + g.rb * 4 + 2 * wc + (g.u[0].x == 1.0 && g.u[0].y == 0.0); break;

@@ -191,9 +191,9 @@ struct GOp {
 constexpr uint32_t kOpChkFixed = 1u << 8;    // fm / fv
 constexpr uint32_t kOpChkThread = 1u << 9;   // tm / tv
 constexpr uint32_t kOpSel = 1u << 10;        // tsel / fsel matrix choice
+constexpr uint32_t kOpTraj = 1u << 11;       // DENSET: the tile's trajectory matrix from op.tab
 enum {
-    OPC_DENSE = 0,      // + rb (+5: window controls)
-    OPC_DENSET = 10,    // + rb (+5: window controls)
+    OPC_DENSE = 0,      // + rb (+5: window controls); DENSET too (kOpTraj)
     OPC_CDENSE = 20,    // + rb*10 + cs*2 + cv
     OPC_DENSE2 = 70,    // + rb*5 + cs
     OPC_DIAGW = 95,     // + rb*4 + 2*(window controls) + (d0 == 1)
