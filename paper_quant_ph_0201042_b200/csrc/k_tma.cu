@@ -28,6 +28,7 @@
 #include "qsim_internal.h"
 #include "ops_common.cuh"
 #include "tile_common.cuh"
+#include "mbar.cuh"
 
 namespace qs {
 
@@ -48,38 +49,6 @@ struct TmaArgs {
     // smem amplitude index of each tile bit in the load / store boxes
     int in_rank[kTileMaxBits], out_rank[kTileMaxBits];
 };
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p)
-{
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
-{
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
-{
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
-{
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
 
 __device__ __forceinline__ void tma_load(void *dst, const CUtensorMap *map, const int (&c)[5], uint64_t *bar)
 {
