@@ -309,7 +309,7 @@ void launch_perm(Handle *h, const PermDesc &d)
             cudaFuncSetAttribute(k_perm_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_perm_ring, kPermConsumers + 32, smem);
-        per_sm = std::max(1, std::min(per_sm, 2));
+        per_sm = std::max(1, std::min(per_sm, 3));
         const uint64_t cap = (uint64_t)h->num_sms * per_sm;
         prof_begin(h);
         k_perm_ring<<<(unsigned)(nruns < cap ? nruns : cap), kPermConsumers + 32, smem, h->stream>>>(h->psi, nruns,
