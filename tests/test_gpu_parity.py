@@ -275,6 +275,35 @@ def test_cfg3_modexp_fused_equals_modmul_chain(reg):
     assert np.array_equal(s1, ref) and np.array_equal(s2, ref)   # bit-exact
 
 
+@pytest.mark.parametrize("ne,nw,N,a", [(6, 5, 31, 3), (8, 11, 2047, 5), (12, 11, 1999, 7), (10, 10, 1007, 558),
+                                        (4, 12, 4093, 3), (3, 6, 35, 1)])
+def test_modexp_run_sizes_bit_exact(reg, ne, nw, N, a):
+    """MODEXP on runs of 2^5 .. 2^12 amplitudes (the bulk-copy ring up to 2^11,
+    the one-CTA-per-run kernel above), base 1 (every run inactive): bit-exact
+    against the oracle's chain of controlled MODMULs."""
+    psi = rand_state(ne + nw, ne * 31 + nw)
+    h = reg(ne + nw, psi)
+    Q.qsim_apply_perm(h, Q.QSIM_PERM_MODEXP, ne, nw, elo=0, em=ne, base=a, modulus=N)
+    ref = psi.copy()
+    for j in range(ne):
+        cm = 1 << (ne - 1 - j)
+        O.modmul(ref, ne, nw, cm, cm, pow(a, 1 << j, N), N)
+    assert np.array_equal(get(h, ne + nw), ref)
+
+
+@pytest.mark.parametrize("c", [1, 4, 1006])
+def test_modmul_controlled_runs_bit_exact(reg, c):
+    """MODMUL with a control qubit outside the work register (half the runs
+    inactive) and c = 1 (identity): bit-exact against the oracle."""
+    ne, nw, N = 7, 10, 1007
+    psi = rand_state(ne + nw, c)
+    h = reg(ne + nw, psi)
+    Q.qsim_apply_perm(h, Q.QSIM_PERM_MODMUL, ne, nw, ctrl_mask=1 << 2, ctrl_vals=1 << 2, mult=c, modulus=N)
+    ref = psi.copy()
+    O.modmul(ref, ne, nw, 1 << 2, 1 << 2, c, N)
+    assert np.array_equal(get(h, ne + nw), ref)
+
+
 def test_cfg3_full_size_fejer(reg):
     """n = 30 (16 GiB), sigma = 0: P(e) against the exact closed form."""
     from _closed_forms import fejer_distribution, order
