@@ -100,6 +100,12 @@ void launch_ops_pass(Handle *h, const OpsLaunch &L)
         cost += c;
     }
     if (cost <= tma_max && launch_ops_pass_tma(h, L)) return;
+    // moderate FP64 work: the ping-pong TMA kernel overlaps loads with both
+    // warpgroups' arithmetic (configs[3]'s 9-gate H passes: 11.9 -> 10.6 ms);
+    // heavier lists stay on two CTAs per SM (configs[4]'s 25-gate passes are
+    // 10% faster there: no stage-buffer read of the first segment)
+    static const double pp_max = std::getenv("QSIM_OPS_PP_MAX") ? std::atof(std::getenv("QSIM_OPS_PP_MAX")) : 12.0;
+    if (cost <= pp_max && launch_ops_pass_pp(h, L)) return;
     const size_t smem = sizeof(double2) << P.tbits;
     static uint64_t attr = 0;
     if (first_use_on_device(attr)) {

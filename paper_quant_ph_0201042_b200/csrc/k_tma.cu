@@ -697,6 +697,99 @@ __global__ void __launch_bounds__(ops::kOpsThreads, 1)
     if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Gate-list pass for FP64-heavy op lists: two 128-thread warpgroups per CTA
+// (one CTA per SM) work on alternate tiles (ping-pong) -- eight warps per SM
+// doing FP64, as k_ops_pass's two CTAs -- while the tiles arrive by TMA into
+// a 3-stage ring: the load of tile j+3 leaves as soon as tile j's last
+// transpose has been read, instead of each thread's serialised gather.
+// Results go from registers straight to HBM (the stage is free at once).
+__global__ void __launch_bounds__(2 * ops::kOpsThreads, 1)
+    k_ops_pp(const __grid_constant__ CUtensorMap map, const __grid_constant__ OpsLaunch L,
+             const __grid_constant__ TmaArgs ta, double2 *psi, uint64_t ntiles)
+{
+    using namespace ops;
+    static_assert(kTmaTileBits == kTileMaxBits && kStages == 3, "tile / ring");
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    double2 *bufs = reinterpret_cast<double2 *>(smem_raw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(bufs + kStages * (1u << kTmaTileBits));
+    const OpsPass &P = L.P;
+    const uint32_t wg = threadIdx.x / kOpsThreads;
+    const uint32_t tid = threadIdx.x % kOpsThreads;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map) : "memory");
+        for (uint64_t q = 0; q < kStages; ++q) {
+            const uint64_t T = blockIdx.x + q * gridDim.x;
+            if (T >= ntiles) break;
+            int c[5];
+            coords(ta.in_first, ta.in_len, T, c);
+            mbar_expect_tx(&full[q], kTileBytes);
+            tma_load(bufs + (size_t)q * (1u << kTmaTileBits), &map, c, &full[q]);
+        }
+    }
+    const int tb = kTmaTileBits - RB5;
+    const OpsSeg &s0 = P.seg[0];
+    const OpsSeg &sL = P.seg[P.nseg - 1];
+    uint32_t lin = 0;
+    uint64_t tout = 0;
+    for (int t = 0; t < tb; ++t) {
+        lin |= ((tid >> t) & 1u) << ta.in_rank[s0.order[t]];
+        tout |= (uint64_t)((tid >> t) & 1u) << P.in_pos[sL.order[t]];
+    }
+    uint32_t pin[RB5];
+    uint64_t pout[RB5];
+#pragma unroll
+    for (int b = 0; b < RB5; ++b) {
+        pin[b] = 1u << ta.in_rank[s0.win[b]];
+        pout[b] = 1ull << P.in_pos[sL.win[b]];
+    }
+    const WgSync sync{1u + wg};
+    for (uint64_t j = wg;; j += 2) {
+        const uint64_t T = blockIdx.x + j * gridDim.x;
+        if (T >= ntiles) break;
+        const int st = (int)(j % kStages);
+        double2 *buf = bufs + (size_t)st * (1u << kTmaTileBits);
+        mbar_wait(&full[st], (uint32_t)((j / kStages) & 1));
+        double2 v[NS5];
+#pragma unroll
+        for (int k = 0; k < NS5; ++k) {
+            uint32_t o = lin;
+#pragma unroll
+            for (int b = 0; b < RB5; ++b)
+                if (k & (1 << b)) o |= pin[b];
+            v[k] = buf[o];
+        }
+        run_segments(v, L, T, tid, tb, buf, sync);
+        // the stage is no longer read: the next load into it may leave
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        sync();
+        if (tid == 0) {
+            const uint64_t Tn = T + (uint64_t)kStages * gridDim.x;
+            if (Tn < ntiles) {
+                int c[5];
+                coords(ta.in_first, ta.in_len, Tn, c);
+                mbar_expect_tx(&full[st], kTileBytes);
+                tma_load(buf, &map, c, &full[st]);
+            }
+        }
+        uint64_t ib = 0;
+        for (int f = 0; f < P.nfix; ++f) ib |= ((T >> f) & 1u) << P.fin_pos[f];
+        const uint64_t base = ib | tout;
+#pragma unroll
+        for (int k = 0; k < NS5; ++k) {
+            uint64_t o = base;
+#pragma unroll
+            for (int b = 0; b < RB5; ++b)
+                if (k & (1 << b)) o |= pout[b];
+            psi[o] = v[k];
+        }
+    }
+}
+
 // ------------------------------------------------------------------ host
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
@@ -957,6 +1050,36 @@ bool launch_ops_pass_tma(Handle *h, const OpsLaunch &L)
     prof_begin(h);
     k_ops_tma<<<grid, ops::kOpsThreads, smem, h->stream>>>(im, L, ta, ntiles);
     prof_end(h, "k_ops_tma", (1ull << (P.tbits + P.nfix)) * 32);
+    return true;
+}
+
+}  // namespace qs
+
+namespace qs {
+
+// FP64-heavy gate-list pass through k_ops_pp; false = the tile is not a <= 5-D box
+bool launch_ops_pass_pp(Handle *h, const OpsLaunch &L)
+{
+    cudaSetDevice(h->device);
+    const OpsPass &P = L.P;
+    static const bool off = getenv("QSIM_NO_OPS_PP") != nullptr;
+    if (P.tbits != kTmaTileBits || off || getenv("QSIM_NO_TMA")) return false;
+    std::vector<int> fid(h->nl, -1);
+    for (int f = 0; f < P.nfix; ++f) fid[P.fin_pos[f]] = f;
+    std::vector<int> tp(P.in_pos, P.in_pos + P.tbits);
+    CUtensorMap im;
+    TmaArgs ta;
+    std::memset(&ta, 0, sizeof ta);
+    if (!build_side(h->psi, h->nl, tp, fid, im, ta.in_first, ta.in_len, ta.in_rank)) return false;
+    const size_t smem = (size_t)kStages * kTileBytes + 8 * sizeof(uint64_t);
+    static uint64_t attr = 0;
+    if (first_use_on_device(attr))
+        cudaFuncSetAttribute(k_ops_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const uint64_t ntiles = 1ull << P.nfix;
+    const unsigned grid = (unsigned)std::min<uint64_t>((ntiles + 1) / 2, (uint64_t)h->num_sms);
+    prof_begin(h);
+    k_ops_pp<<<grid, 2 * ops::kOpsThreads, smem, h->stream>>>(im, L, ta, h->psi, ntiles);
+    prof_end(h, "k_ops_pp", (1ull << (P.tbits + P.nfix)) * 32);
     return true;
 }
 

@@ -224,8 +224,22 @@ __device__ __forceinline__ uint32_t seg_thread_part(const OpsSeg &s, int tb, uin
 // The segments of one tile: v holds the tile in segment 0's register map on
 // entry and in the last segment's map on exit; buf (2^tbits double2, shared)
 // carries the transposes between register windows.
+// barrier over the threads that share one tile buffer: the whole CTA, or one
+// 128-thread warpgroup (named barrier 1 + wg) in the ping-pong kernel
+struct CtaSync {
+    __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+struct WgSync {
+    uint32_t id;
+    __device__ __forceinline__ void operator()() const
+    {
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kOpsThreads) : "memory");
+    }
+};
+
+template <class Sync = CtaSync>
 __device__ __forceinline__ void run_segments(double2 (&v)[NS5], const OpsLaunch &L, uint64_t T, uint32_t tid, int tb,
-                                             double2 *buf)
+                                             double2 *buf, Sync sync = Sync())
 {
     const OpsPass &P = L.P;
     uint32_t traj = P.bat_rank;
@@ -240,7 +254,7 @@ __device__ __forceinline__ void run_segments(double2 (&v)[NS5], const OpsLaunch 
 #pragma unroll
         for (int b = 0; b < RB5; ++b) wsw[b] = swz(1u << sg.win[b]);
         if (s > 0) {
-            __syncthreads();   // previous readers of the tile buffer are done
+            sync();   // previous readers of the tile buffer are done
 #pragma unroll
             for (int k = 0; k < NS5; ++k) {
                 uint32_t o = prev_stp;
@@ -249,7 +263,7 @@ __device__ __forceinline__ void run_segments(double2 (&v)[NS5], const OpsLaunch 
                     if (k & (1 << b)) o ^= prev_wsw[b];
                 buf[o] = v[k];
             }
-            __syncthreads();
+            sync();
 #pragma unroll
             for (int k = 0; k < NS5; ++k) {
                 uint32_t o = stp;

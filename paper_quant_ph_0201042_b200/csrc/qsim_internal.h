@@ -228,7 +228,8 @@ struct OpsLaunch {
 };
 static_assert(sizeof(OpsLaunch) <= 32000, "kernel parameter space");
 void launch_ops_pass(Handle *h, const OpsLaunch &L);
-bool launch_ops_pass_tma(Handle *h, const OpsLaunch &L);   // k_tma.cu; false: geometry unsupported
+bool launch_ops_pass_tma(Handle *h, const OpsLaunch &L);
+bool launch_ops_pass_pp(Handle *h, const OpsLaunch &L);   // k_tma.cu ping-pong; false: geometry   // k_tma.cu; false: geometry unsupported
 
 // A queued gate in physical local positions (api.cu gate queue).
 struct QOp {
