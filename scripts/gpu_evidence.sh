@@ -16,3 +16,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_qf
 echo "ncu rc=$?"; tail -2 gpurun_out/ncu_qft.log
 ncu -i gpurun_out/prof_qft.ncu-rep --page details > gpurun_out/prof_qft_details.txt 2>&1
 ncu -i gpurun_out/prof_qft.ncu-rep --page raw --csv > gpurun_out/prof_qft_raw.csv 2>&1
+rm -f gpurun_out/prof_qft.ncu-rep
