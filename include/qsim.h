@@ -192,6 +192,16 @@ int qsim_swap(qsim_t *h, int q1, int q2);
  * §2.3.1), with the constant H = (1/sqrt2)(1 1; 1 -1). */
 int qsim_hadamard(qsim_t *h, int lo, int m);
 
+/* H on every qubit of [lo, lo+m) as the paper's angle-form gate
+ * H = U_R(pi/4) U_P1(pi) (the H of its noisy circuits,
+ * PAPER.md:738-747): exactly the m calls qsim_apply_angles(h,
+ * QSIM_GATE_RP, {pi/4, pi}, 0, 0, q) for q = lo .. lo+m-1 -- with gate noise
+ * each H draws its two angle perturbations from the gate counter, which
+ * advances by m.  Executed as fused HBM passes where the register allows
+ * (single GPU, no trajectory batch), else gate by gate.  QSIM_ERANGE if the
+ * range leaves [0, n). */
+int qsim_hadamard_angles(qsim_t *h, int lo, int m);
+
 /* QFT (inverse = 0) or inverse QFT (inverse = 1) on the sub-register of
  * qubits [lo, lo+m), qubit lo its MSB (§2.3.2; DESIGN.md
  * R6-R8): beta_x = 2^(-m/2) sum_y e^(+-2 pi i x y / 2^m) alpha_y on the

@@ -1103,7 +1103,7 @@ static int qft_gates(qsim_t *h, const Ranks &R, int lo, int m, int band, int inv
 // the same Philox draws, in the same gate-counter order -- handed to the
 // generalised kernel.  Returns 1 (nothing done) when the register does not
 // fit the pass geometry; the caller then runs qft_gates.
-static int fused_qft_gen(qsim_t *h, const Ranks &R, int lo, int m, int band, int inverse)
+static int fused_qft_gen(qsim_t *h, const Ranks &R, int lo, int m, int band, int inverse, bool honly = false)
 {
     static const bool off = getenv("QSIM_NO_QFT_GEN") != nullptr;
     if (off || h->world != 1 || R.size() != 1 || h->batch_b > 0 || !h->fuse || h->nl < 9 || m > h->nl || m < 4 ||
@@ -1113,10 +1113,10 @@ static int fused_qft_gen(qsim_t *h, const Ranks &R, int lo, int m, int band, int
     GenCircuit gc;
     gc.m = m;
     bool even = false;
-    int rc = fused_range(R, lo, m, 1, inverse, &gc, true, false);
+    int rc = fused_range(R, lo, m, honly ? 0 : 1, inverse, &gc, true, false);
     if (rc == kGenInfeasible) {
         even = true;
-        rc = fused_range(R, lo, m, 1, inverse, &gc, true, true);
+        rc = fused_range(R, lo, m, honly ? 0 : 1, inverse, &gc, true, true);
     }
     if (rc == kGenInfeasible) return 1;
     if (rc) return lift(h, R, rc);
@@ -1155,8 +1155,27 @@ static int fused_qft_gen(qsim_t *h, const Ranks &R, int lo, int m, int band, int
             g++;
         }
     }
-    if ((rc = fused_range(R, lo, m, 1, inverse, &gc, false, even))) return lift(h, R, rc);
+    if ((rc = fused_range(R, lo, m, honly ? 0 : 1, inverse, &gc, false, even))) return lift(h, R, rc);
     h->gcount = g;
+    return QSIM_OK;
+}
+
+int qsim_hadamard_angles(qsim_t *h, int lo, int m)
+{
+    QS_CHECK_HANDLE(h);
+    if (lo < 0 || m < 0 || lo + m > h->n) return fail(h, QSIM_ERANGE, "range outside [0, n)");
+    if (m == 0) return QSIM_OK;
+    const Ranks R = ranks_of(h);
+    if (h->sigma > 0.0) {
+        // the generalised QFT passes with no R_d (band 0) in Hadamard mode
+        // (passes in place, no block moves): H(lo+j) drawn at counter g0 + j
+        // as in the gate-by-gate loop
+        const int rc = fused_qft_gen(h, R, lo, m, 0, 0, true);
+        if (rc != 1) return rc;
+    }
+    const double ang[2] = {M_PI / 4.0, M_PI};
+    for (int q = lo; q < lo + m; ++q)
+        if (int rc = qsim_apply_angles(h, QSIM_GATE_RP, ang, 0, 0, q)) return rc;
     return QSIM_OK;
 }
 
@@ -1514,7 +1533,8 @@ int qsim_probs(qsim_t *h, int lo, int m, double *out)
     const uint64_t ny = 1ull << m;
     const int mloc = ph <= nl ? m : (pl < nl ? nl - pl : 0);
     const uint64_t nyl = 1ull << mloc;
-    std::vector<std::vector<double>> parts(R.size(), std::vector<double>(ny, 0.0));
+    std::vector<std::vector<double>> parts;
+    if (R.size() > 1 || mloc != m) parts.assign(R.size(), std::vector<double>(ny, 0.0));
     for (size_t i = 0; i < R.size(); ++i) {
         Handle *hm = R[i];
         cudaSetDevice(hm->device);
@@ -1541,6 +1561,11 @@ int qsim_probs(qsim_t *h, int lo, int m, double *out)
         if (!rc) rc = check_cuda(hm, cudaStreamSynchronize(hm->stream), "probs");
         const double *part = hm->h_red;
         if (rc) return lift(h, R, rc);
+        if (R.size() == 1 && mloc == m) {
+            // one shard holds the whole range: the pinned staging is the result
+            std::memcpy(out, part, ny * sizeof(double));
+            return QSIM_OK;
+        }
         // y = (rank bits inside the range) << mloc | y_loc
         uint64_t yhi = 0;
         if (ph > nl) {

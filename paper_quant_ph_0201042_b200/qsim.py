@@ -98,6 +98,7 @@ _sig("qsim_hadamard", _i32, _H, _i32, _i32)
 _sig("qsim_qft", _i32, _H, _i32, _i32, _i32)
 _sig("qsim_fft", _i32, _H, _i32, _i32, _i32)
 _sig("qsim_aqft", _i32, _H, _i32, _i32, _i32, _i32)
+_sig("qsim_hadamard_angles", _i32, _H, _i32, _i32)
 _sig("qsim_measure_range", _i32, _H, _i32, _i32, _f64, _i32, C.POINTER(_u64))
 _sig("qsim_inner", _i32, _H, _H, _p)
 _sig("qsim_set_batch", _i32, _H, _i32)
@@ -269,6 +270,12 @@ def qsim_qft(h, lo: int, m: int, inverse: bool = False) -> None:
 
 def qsim_fft(h, lo: int, m: int, inverse: bool = False) -> None:
     _chk(h, lib.qsim_fft(h, lo, m, int(bool(inverse))))
+
+
+def qsim_hadamard_angles(h, lo: int, m: int) -> None:
+    """H = U_R(pi/4) U_P1(pi) on every qubit of [lo, lo+m), counted and noisy
+    like qsim_apply_angles (fused passes where possible)."""
+    _chk(h, lib.qsim_hadamard_angles(h, lo, m))
 
 
 def qsim_aqft(h, lo: int, m: int, b: int, inverse: bool = False) -> None:

@@ -94,8 +94,7 @@ def run_cfg3(h, ne: int = 20, nw: int = 10, N: int = 1007, seed: int = 4, sigma:
     Q.qsim_set_gate_noise(h, seed, sigma)
     Q.qsim_set_gate_counter(h, 0)
     if sigma > 0:
-        for q in range(ne):
-            Q.qsim_apply_angles(h, Q.QSIM_GATE_RP, [math.pi / 4, math.pi], 0, 0, q)
+        Q.qsim_hadamard_angles(h, 0, ne)             # = ne angle-form H gates (counter + noise)
     else:
         Q.qsim_hadamard(h, 0, ne)
         Q.qsim_set_gate_counter(h, ne)

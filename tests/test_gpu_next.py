@@ -4,6 +4,8 @@ qsim_aqft (approximate QFT), qsim_measure_range (partial
 measurement with collapse, PAPER.md:391-404) and qsim_inner (fidelity,
 PAPER.md:1127-1128), against the pinned oracle (tests/test_oracle_next.py).
 Single handles and in-process rank groups (sub-registers on rank bits)."""
+import math
+
 import numpy as np
 import pytest
 
@@ -140,6 +142,30 @@ def test_noisy_qft_fused_matches_oracle(mk, n, lo, m, inverse):
     O.qft(ref, lo, m, inverse, noise=nz)
     assert maxdiff(get(h, n), ref) < TOL
     assert Q.qsim_get_gate_counter(h) == nz.g
+
+
+@pytest.mark.parametrize("n,lo,m,sigma", [(20, 0, 20, 1e-2), (18, 3, 12, 5e-2), (12, 2, 3, 1e-2), (16, 0, 16, 0.0),
+                                          (11, 0, 8, 1e-3)])
+def test_hadamard_angles_equals_angle_gate_loop(mk, n, lo, m, sigma):
+    """qsim_hadamard_angles = m angle-form H gates U_R(pi/4) U_P1(pi)
+     in qubit order with the same Philox draws: the fused
+    passes (k_qft_gen, no R_d, reversal undone by relabelling) against the
+    oracle's gate loop, and the counter advanced by m."""
+    psi = rand_state(n, 3 * n + m)
+    h = mk(n, psi)
+    Q.qsim_set_gate_noise(h, 21, sigma)
+    Q.qsim_set_gate_counter(h, 7)
+    Q.qsim_hadamard_angles(h, lo, m)
+    ref = psi.copy()
+    nz = O.Noise(seed=21, sigma=sigma, g=7)
+    for q in range(lo, lo + m):
+        O.apply_angles(ref, nz, O.RP, [math.pi / 4, math.pi], 0, 0, q)
+    assert maxdiff(get(h, n), ref) < TOL
+    assert Q.qsim_get_gate_counter(h) == nz.g == 7 + m
+    # the layout stays consistent for what follows
+    Q.qsim_qft(h, 0, n, False)
+    O.qft(ref, 0, n, False, noise=nz)
+    assert maxdiff(get(h, n), ref) < TOL
 
 
 def test_noisy_qft_fused_equals_unfused_after_gates(mk):
