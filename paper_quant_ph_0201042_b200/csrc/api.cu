@@ -946,23 +946,25 @@ int qsim_apply_ctrl(qsim_t *h, uint64_t cmask, uint64_t cvals, int q, const qsim
 }
 
 // A table of 4 * B matrices in the member's arena (batch.cu); the member's
-// queue is flushed first when the arena is full (flushing consumes every
-// queued table, stream-ordered).
+// queue is flushed first when the producers' half of the arena is full
+// (flushing consumes every queued table, stream-ordered).  The other half
+// takes the planner's merged products (plan_ops.cu try_merge_tab).
 static double2 *batch_table(Handle *m, uint64_t B, int &rc)
 {
     rc = QSIM_OK;
     const size_t need = 4 * B;
-    if (m->tabs_used + need > m->tabs_cap) {
+    if (m->tabs_used + need > m->tabs_cap / 2) {
         if ((rc = flush_queue(m))) return nullptr;
         m->tabs_used = 0;
-        if (need > m->tabs_cap) {
+        if (need > m->tabs_cap / 2) {
             if (m->d_tabs) {
                 cudaStreamSynchronize(m->stream);
                 cudaFree(m->d_tabs);
             }
             m->d_tabs = nullptr;
             m->tabs_cap = 0;
-            const size_t cap = std::max<size_t>(need * 64, (size_t)1 << 20);
+            // ~1000 tables per half at 2^10 trajectories (128 MiB), <= 256 MiB
+            const size_t cap = std::max<size_t>(std::min<size_t>(need * 2048, (size_t)1 << 24), 2 * need);
             if (cudaMalloc(&m->d_tabs, cap * sizeof(double2)) != cudaSuccess) {
                 cudaGetLastError();
                 rc = fail(m, QSIM_ENOMEM, "batch matrix tables");

@@ -74,6 +74,23 @@ __global__ void k_batch_mats(int kind, double a0, double a1, double a2, double a
     for (int k = 0; k < 4; ++k) out[4 * t + k] = U[k];
 }
 
+// out[t] = B_t A_t: the product of two per-trajectory gates on one qubit
+// (the planner merges runs of them into one table before a pass)
+__global__ void k_batch_mul(double2 *__restrict__ out, const double2 *__restrict__ A, double2 a0, double2 a1,
+                            double2 a2, double2 a3, const double2 *__restrict__ B, double2 b0, double2 b1, double2 b2,
+                            double2 b3, uint64_t count)
+{
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= count) return;
+    double2 X[4] = {a0, a1, a2, a3}, Y[4] = {b0, b1, b2, b3}, Z[4];
+    if (A)
+        for (int k = 0; k < 4; ++k) X[k] = A[4 * t + k];
+    if (B)
+        for (int k = 0; k < 4; ++k) Y[k] = B[4 * t + k];
+    mmul(Y, X, Z);
+    for (int k = 0; k < 4; ++k) out[4 * t + k] = Z[k];
+}
+
 // psi[i] = src[i mod 2^r] * scale over the shard (every trajectory gets the
 // same register state).
 __global__ void __launch_bounds__(256) k_batch_broadcast(double2 *__restrict__ psi, uint64_t count,
@@ -146,6 +163,16 @@ void launch_batch_mats(Handle *h, int kind, const double *ang, double sigma, uin
     k_batch_mats<<<(unsigned)((B + 127) / 128), 128, 0, h->stream>>>(kind, a[0], a[1], a[2], a[3], sigma, seed, g, B,
                                                                      out);
     prof_end(h, "k_batch_mats", B * 64);
+}
+
+void launch_batch_mul(Handle *h, double2 *out, const double2 *A, const double2 ac[4], const double2 *B,
+                      const double2 bc[4], uint64_t count)
+{
+    cudaSetDevice(h->device);
+    prof_begin(h);
+    k_batch_mul<<<(unsigned)((count + 127) / 128), 128, 0, h->stream>>>(out, A, ac[0], ac[1], ac[2], ac[3], B, bc[0],
+                                                                       bc[1], bc[2], bc[3], count);
+    prof_end(h, "k_batch_mul", count * 192);
 }
 
 void launch_batch_broadcast(Handle *h, const double2 *src, int r, double scale)

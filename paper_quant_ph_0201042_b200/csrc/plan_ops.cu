@@ -49,7 +49,8 @@ struct POp {
     int cs;                 // choice form: position selecting m1 (m0 where it is 0); -1: none
     double2 m0[4], m1[4];   // m1 == m0 when cs < 0
     uint64_t nmask, dmask;  // positions acted on non-diagonally / diagonally
-    const double2 *tab;     // batched handle: per-trajectory matrices (never merged)
+    const double2 *tab;     // batched handle: per-trajectory matrices (merged on the device only)
+    bool tab_own;           // tab is a product table this flush allocated (updated in place)
     bool dead;
 };
 
@@ -147,6 +148,34 @@ bool try_merge(POp &A, const POp &B, const std::vector<char> &in_win)
     std::memcpy(A.m1, r1, sizeof r1);
     A.dense = !(is_diagm(r0) && is_diagm(r1));
     if (cs < 0 && !A.dense) A.cs = -1;
+    set_masks(A);
+    return true;
+}
+
+// Merge B into A when either carries per-trajectory matrices (batched
+// handle): both uncontrolled on the same qubit; the product table B_t A_t is
+// formed on the device into the handle's table arena (stream order puts it
+// after the tables' producers and before the pass).  A run of k noisy gates
+// or Pauli events on one qubit becomes one table lookup per tile.
+bool try_merge_tab(Handle *h, POp &A, const POp &B)
+{
+    static const bool off = getenv("QSIM_NO_TAB_MERGE") != nullptr;
+    if (off || A.tpos < 0 || A.tpos != B.tpos || A.cmask || B.cmask || A.cs >= 0 || B.cs >= 0) return false;
+    if (!A.tab && !B.tab) return false;
+    if (!A.dense || !B.dense) return false;
+    const uint64_t count = 1ull << h->batch_b;
+    const size_t need = 4 * count;
+    double2 *out;
+    if (A.tab_own) {
+        out = const_cast<double2 *>(A.tab);   // a chain keeps one product table (element-wise in place)
+    } else {
+        if (!h->d_tabs || h->tabs_used + need > h->tabs_cap) return false;
+        out = h->d_tabs + h->tabs_used;
+        h->tabs_used += need;
+    }
+    launch_batch_mul(h, out, A.tab, A.m0, B.tab, B.m0, count);
+    A.tab = out;
+    A.tab_own = true;
     set_masks(A);
     return true;
 }
@@ -439,7 +468,7 @@ int flush_queue(Handle *h)
                 for (size_t ii = jj; ii-- > 0;) {
                     POp &A = ops[Ls[ii]];
                     if (A.dead) continue;
-                    if (A.tpos == B.tpos && try_merge(A, B, in_win)) {
+                    if (A.tpos == B.tpos && (try_merge(A, B, in_win) || try_merge_tab(h, A, B))) {
                         B.dead = true;
                         break;
                     }

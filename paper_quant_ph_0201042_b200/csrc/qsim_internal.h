@@ -349,6 +349,10 @@ int dist_sum_host(const Ranks &R, const std::vector<std::vector<double>> &parts,
 void launch_batch_mats(Handle *h, int kind, const double *ang, double sigma, uint64_t seed, uint64_t g, uint64_t B,
                        double2 *out);
 void launch_batch_broadcast(Handle *h, const double2 *src, int r, double scale);
+// out[t] = B_t A_t for trajectories t < count (2x2 complex, row-major); a null
+// table means the constant matrix ac / bc for every t (batch.cu)
+void launch_batch_mul(Handle *h, double2 *out, const double2 *A, const double2 ac[4], const double2 *B,
+                      const double2 bc[4], uint64_t count);
 void launch_batch_overlap(Handle *h, const double2 *ref, int r, double scale, double *d_out);
 // one queued gate with the unfused streaming kernels (k_gates.cu)
 void run_gate_unfused(Handle *h, const QOp &op);
