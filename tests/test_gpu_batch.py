@@ -51,8 +51,12 @@ def oracle_events_ht(n, b, k, seed, p, ntraj):
 
 
 @pytest.mark.parametrize("world", [1, 2, 4])
-def test_ht_batch_trajectories_match_oracle(mk, world):
-    n, b, k, seed, sigma, p = 10, 5, 6, 100, 2e-2, 0.03
+@pytest.mark.parametrize("sigma,p,k", [(2e-2, 0.03, 6), (0.0, 0.05, 9), (2e-2, 0.0, 12)])
+def test_ht_batch_trajectories_match_oracle(mk, world, sigma, p, k):
+    """Runs of per-trajectory gates on a qubit (noisy H's, Pauli tables,
+    constant H's between them) are merged into device-side product tables by
+    the planner: every trajectory still equals the oracle's."""
+    n, b, seed = 10, 5, 100
     h = mk(n + b, world)
     p0, ev = W.run_ht_batch(h, n, b, k, seed, sigma, p)
     S = slices(h, n + b, b)
