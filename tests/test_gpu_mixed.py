@@ -47,10 +47,10 @@ def mk():
         Q.qsim_destroy(h)
 
 
-@pytest.mark.parametrize("world", [1, 2, 4])
-@pytest.mark.parametrize("seed", list(range(1, 9)))
-def test_mixed_api_sequence_matches_oracle(mk, world, seed):
-    n, sigma, nsteps = 15, 1e-2, 40
+@pytest.mark.parametrize("world,seed,n,nsteps", [(w, s, 15, 40) for w in (1, 2, 4) for s in range(1, 9)] +
+                         [(w, s, 22, 25) for w in (1, 2) for s in (11, 12)])
+def test_mixed_api_sequence_matches_oracle(mk, world, seed, n, nsteps):
+    sigma = 1e-2
     rng = np.random.default_rng(seed)
     psi = rand_state(n, 100 + seed)
     h = mk(n, world, psi)
