@@ -1045,6 +1045,8 @@ int qsim_swap(qsim_t *h, int q1, int q2)
     return QSIM_OK;
 }
 
+static int fused_qft_gen(qsim_t *h, const Ranks &R, int lo, int m, int band, int inverse, bool honly);
+
 int qsim_hadamard(qsim_t *h, int lo, int m)
 {
     QS_CHECK_HANDLE(h);
@@ -1105,7 +1107,7 @@ static int qft_gates(qsim_t *h, const Ranks &R, int lo, int m, int band, int inv
 // the same Philox draws, in the same gate-counter order -- handed to the
 // generalised kernel.  Returns 1 (nothing done) when the register does not
 // fit the pass geometry; the caller then runs qft_gates.
-static int fused_qft_gen(qsim_t *h, const Ranks &R, int lo, int m, int band, int inverse, bool honly = false)
+static int fused_qft_gen(qsim_t *h, const Ranks &R, int lo, int m, int band, int inverse, bool honly)
 {
     static const bool off = getenv("QSIM_NO_QFT_GEN") != nullptr;
     if (off || h->world != 1 || R.size() != 1 || h->batch_b > 0 || !h->fuse || h->nl < 9 || m > h->nl || m < 4 ||
@@ -1194,7 +1196,7 @@ int qsim_qft(qsim_t *h, int lo, int m, int inverse)
     }
     if (h->sigma > 0.0) {
         // operational error: the perturbed gates as fused passes when the geometry allows
-        const int rc = fused_qft_gen(h, R, lo, m, m, inverse);
+        const int rc = fused_qft_gen(h, R, lo, m, m, inverse, false);
         if (rc != 1) return rc;
     }
     // noisy, or fusion off (the paper's one sweep per gate)
@@ -1218,7 +1220,7 @@ int qsim_aqft(qsim_t *h, int lo, int m, int b, int inverse)
     if (m == 0) return QSIM_OK;
     if (b >= m - 1) return qsim_qft(h, lo, m, inverse);
     const Ranks R = ranks_of(h);
-    const int rc = fused_qft_gen(h, R, lo, m, b, inverse);
+    const int rc = fused_qft_gen(h, R, lo, m, b, inverse, false);
     if (rc != 1) return rc;
     return qft_gates(h, R, lo, m, b, inverse, true);
 }
