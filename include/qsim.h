@@ -209,7 +209,9 @@ int qsim_hadamard_angles(qsim_t *h, int lo, int m);
  * lo+k on lo+j (k > j), closing swaps.  Without gate noise the gates are the
  * constant matrices and the whole circuit runs as fused HBM passes; with gate
  * noise every H / R_d is an angle-form gate (counter advances per H and R_d,
- * m + m(m-1)/2 in total either way).  QSIM_ERANGE if the range leaves [0, n). */
+ * m + m(m-1)/2 in total either way) -- still fused passes carrying each
+ * gate's perturbed matrix / angle on a single GPU (R38), gate by
+ * gate otherwise.  QSIM_ERANGE if the range leaves [0, n). */
 int qsim_qft(qsim_t *h, int lo, int m, int inverse);
 
 /* FFT of the sub-register [lo, lo+m) ("If we regard the
@@ -225,8 +227,10 @@ int qsim_fft(qsim_t *h, int lo, int m, int inverse);
 /* Approximate QFT (§2.3.2; Barenco et al.; R30):
  * the qsim_qft circuit with every R_d of distance d = k - j > b left out.
  * b >= m-1 is qsim_qft.  Gate noise applies as in qsim_qft; the gate counter
- * advances only for the gates that are applied.  QSIM_ERANGE if the range
- * leaves [0, n) or b < 0. */
+ * advances only for the gates that are applied.  Executed as fused HBM
+ * passes with the gates' own matrices and angles (single GPU, no trajectory
+ * batch, >= 4 and <= local-qubit wires), else gate by gate.  QSIM_ERANGE if
+ * the range leaves [0, n) or b < 0. */
 int qsim_aqft(qsim_t *h, int lo, int m, int b, int inverse);
 
 /* Sign-changing operator V_f for f = delta_{x, idx}, as
