@@ -185,14 +185,15 @@ __global__ void __launch_bounds__(kPersistThreads) k_grover_persist(double2 *__r
 
 // Register-resident variant (the default when the state fits): the 2^n
 // amplitudes live in the registers of a co-resident grid (<= 16 per thread),
-// and the per-iteration all-reduce is a flag-tagged slot exchange instead of
-// a grid barrier: every CTA publishes {sum of its amplitudes, alpha_k if it
-// owns k} into its slot of a parity double buffer and then stamps the slot
-// with the iteration tag (st.release); every CTA polls all slots (ld.acquire)
-// and sums them in the same fixed order, so all CTAs form the identical mean
-// with one L2 round trip and no atomics.  Parity buffers make a slot safe to
-// overwrite: a CTA can only publish iteration t+2 after every CTA has
-// published t+1, i.e. finished reading t.
+// and the per-iteration all-reduce is a slot exchange: every CTA publishes
+// {sum of its amplitudes, alpha_k if it owns k} into its slot of a parity
+// double buffer, arrives on a monotonic counter (red.release), one thread per
+// CTA polls the counter (ld.acquire), then every CTA reads all slots and sums
+// them in the same fixed order, so all CTAs form the identical mean.  Parity
+// buffers make a slot safe to overwrite: a CTA can only publish iteration
+// t+2 after every CTA has published t+1, i.e. finished reading t.  (Measured
+// alternative: slots in NCCL's "LL" layout -- 64-bit words of {32 data bits,
+// tag}, read by 128 pollers per CTA without the counter -- 2.7x slower.)
 template <int A>
 __global__ void __launch_bounds__(kPersistThreads, 1) k_grover_regs(double2 *__restrict__ psi, uint64_t N, uint64_t k,
                                                                    int iters, double *__restrict__ trace,
