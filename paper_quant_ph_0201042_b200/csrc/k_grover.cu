@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(kThreads) k_grover_iter(double2 *__restrict__ 
 namespace cg = cooperative_groups;
 
 constexpr int kPersistThreads = 512;
+constexpr int kRegsThreads = 256;   // k_grover_regs: fewer, fatter threads (cheaper CTA barriers / trees)
 
 __global__ void __launch_bounds__(kPersistThreads) k_grover_persist(double2 *__restrict__ psi, uint64_t N, uint64_t chunk,
                                                                     uint64_t k, int iters, double *__restrict__ trace,
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(kPersistThreads) k_grover_persist(double2 *__r
 // alternative: slots in NCCL's "LL" layout -- 64-bit words of {32 data bits,
 // tag}, read by 128 pollers per CTA without the counter -- 2.7x slower.)
 template <int A>
-__global__ void __launch_bounds__(kPersistThreads, 1) k_grover_regs(double2 *__restrict__ psi, uint64_t N, uint64_t k,
+__global__ void __launch_bounds__(kRegsThreads, 1) k_grover_regs(double2 *__restrict__ psi, uint64_t N, uint64_t k,
                                                                    int iters, double *__restrict__ trace,
                                                                    double4 *__restrict__ slots,
                                                                    unsigned *__restrict__ tags)
@@ -331,13 +332,13 @@ static bool try_regs(Handle *h, uint64_t mark, int iters, double *d_trace)
 {
     const uint64_t N = h->local_dim();
     uint64_t blocks = 1;
-    while (blocks * 2 <= (uint64_t)h->num_sms && blocks * 2 <= N / kPersistThreads) blocks *= 2;
-    const uint64_t per = N / (blocks * kPersistThreads);
-    if (per < 1 || per > 16 || N % (blocks * kPersistThreads)) return false;
+    while (blocks * 2 <= (uint64_t)h->num_sms && blocks * 2 <= N / kRegsThreads) blocks *= 2;
+    const uint64_t per = N / (blocks * kRegsThreads);
+    if (per < 1 || per > 32 || N % (blocks * kRegsThreads)) return false;
     int per_sm = 0;
     void *fn = per <= 1 ? (void *)k_grover_regs<1> : per <= 2 ? (void *)k_grover_regs<2> : per <= 4 ? (void *)k_grover_regs<4>
-             : per <= 8 ? (void *)k_grover_regs<8> : (void *)k_grover_regs<16>;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPersistThreads, 0);
+             : per <= 8 ? (void *)k_grover_regs<8> : per <= 16 ? (void *)k_grover_regs<16> : (void *)k_grover_regs<32>;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kRegsThreads, 0);
     if (per_sm < 1 || blocks > (uint64_t)per_sm * h->num_sms) return false;
     // slots: 2 x blocks double4 (parity double buffer); tags[0]: the arrival counter
     const size_t nd = 8 * blocks + blocks + 16;
@@ -348,7 +349,7 @@ static bool try_regs(Handle *h, uint64_t mark, int iters, double *d_trace)
     void *args[] = {(void *)&h->psi, (void *)&N, (void *)&mark, (void *)&iters, (void *)&d_trace, (void *)&slots,
                     (void *)&tags};
     prof_begin(h);
-    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)blocks), dim3(kPersistThreads), args, 0, h->stream);
+    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)blocks), dim3(kRegsThreads), args, 0, h->stream);
     prof_end(h, "k_grover_regs", N * 32);
     if (e != cudaSuccess) {
         cudaGetLastError();
