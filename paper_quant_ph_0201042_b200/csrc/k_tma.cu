@@ -868,9 +868,14 @@ bool build_side(const double2 *base, int nl, const std::vector<int> &pos_of_tile
     for (int d = 0; d < 5; ++d) estr[d] = 1;
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
+    // L2 promotion no wider than the box's contiguous run (a 256-byte
+    // promotion of 128-byte runs also fetches the neighbouring run)
+    const uint32_t run_bytes = box[0] * 8u;
+    const CUtensorMapL2promotion prom = run_bytes >= 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                        : run_bytes >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                           : CU_TENSOR_MAP_L2_PROMOTION_NONE;
     CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void *)base, gdim, gstride, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, prom, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
