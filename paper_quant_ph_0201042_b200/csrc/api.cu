@@ -76,9 +76,10 @@ int ensure_scratch(Handle *h)
     if (h->scratch) return QSIM_OK;
     cudaError_t e = cudaMalloc(&h->scratch, sizeof(double2) * h->local_dim());
     if (e != cudaSuccess) {
+        // recoverable: callers fall back to in-place schedules where they have one
+        // (a 2^33-amplitude state fills 128 of the B200's 180 GB: no room for a copy)
         h->scratch = nullptr;
         cudaGetLastError();
-        h->poisoned = 1;
         return fail(h, QSIM_ENOMEM, "cannot allocate the " + std::to_string(sizeof(double2) * h->local_dim()) +
                                         "-byte scratch shard");
     }
@@ -401,7 +402,10 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
     const int G = (m + amax - 1) / amax;
     std::vector<int> gsize(G, m / G);
     for (int g = 0; g < m % G; ++g) gsize[g]++;
-    const bool block_moves = qft && h0->world == 1;
+    // the block-move layout writes out of place whenever a pass moves fixed
+    // bits: without room for a scratch shard the passes run in place and the
+    // closing swaps become a relabel (as on several ranks)
+    const bool block_moves = qft && h0->world == 1 && ensure_scratch(h0) == QSIM_OK;
     if (block_moves && G > 1 && gsize[0] < amax && !even) {
         // the first block lands on the lowest positions; with >= 7 wires its
         // last register window stays clear of the 3 lowest, so the store keeps
@@ -527,8 +531,9 @@ void qs::permute_local(Handle *h, const std::vector<int> &perm)
     bool ident = true;
     for (int p = 0; p < h->nl; ++p) ident &= perm[p] == p;
     if (ident) return;
-    if (h->nl < 9) {
-        // tiny shards: a sequence of swaps (positions are few)
+    if (h->nl < 9 || ensure_scratch(h) != QSIM_OK) {
+        // tiny shards, or no room for an out-of-place pass: a sequence of
+        // in-place position swaps
         std::vector<int> cur(h->nl);   // cur[p] = where old position p's bit currently is
         for (int p = 0; p < h->nl; ++p) cur[p] = p;
         std::vector<int> at(h->nl);    // at[x] = old position whose bit sits at x
@@ -555,8 +560,6 @@ void qs::permute_local(Handle *h, const std::vector<int> &perm)
     TilePass tp = make_pass(h, tile, perm);
     tp.a = 0;
     plan_tile_maps(tp);
-    ensure_scratch(h);
-    if (h->poisoned) return;
     launch_tile_pass(h, tp, h->psi, h->scratch);
     swap_buffers(h);
 }
@@ -1348,8 +1351,8 @@ int qsim_apply_perm(qsim_t *h, const qsim_perm_t *f)
             cudaMemcpyAsync(d_table, f->table, sizeof(uint32_t) * len, cudaMemcpyHostToDevice, m->stream);
             d.d_table = d_table;
         }
-        launch_perm(m, d);
-        int rc = after_launch(m, "permutation");
+        int rc = launch_perm(m, d);
+        if (!rc) rc = after_launch(m, "permutation");
         if (d_table) { cudaStreamSynchronize(m->stream); cudaFree(d_table); }
         if (rc) return lift(h, R, rc);
     }

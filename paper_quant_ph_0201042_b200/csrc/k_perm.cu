@@ -264,7 +264,7 @@ static uint64_t invmod_host(uint64_t c, uint64_t N)
     return (uint64_t)t % N;
 }
 
-void launch_perm(Handle *h, const PermDesc &d)
+int launch_perm(Handle *h, const PermDesc &d)
 {
     cudaSetDevice(h->device);   // members of a rank group may live on different devices
     PermArgs a;
@@ -326,7 +326,7 @@ void launch_perm(Handle *h, const PermDesc &d)
         prof_end(h, "k_perm_block", h->local_dim() * 32);
     } else {
         const uint64_t count = h->local_dim();
-        ensure_scratch(h);
+        if (int rc = ensure_scratch(h)) return rc;   // no room for the out-of-place permutation
         const uint64_t cap = (uint64_t)h->num_sms * 8;
         const uint64_t want = (count + 255) / 256;
         prof_begin(h);
@@ -335,6 +335,7 @@ void launch_perm(Handle *h, const PermDesc &d)
         prof_end(h, "k_perm_generic", count * 32);
         swap_buffers(h);
     }
+    return QSIM_OK;
 }
 
 }  // namespace qs

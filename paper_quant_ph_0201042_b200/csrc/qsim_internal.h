@@ -74,7 +74,7 @@ struct PermDesc {
     const uint32_t *d_table;
     uint64_t rank_bits;    // this rank's global bits (for exponent bits that are global)
 };
-void launch_perm(Handle *h, const PermDesc &d);
+int launch_perm(Handle *h, const PermDesc &d);   // QSIM_ENOMEM: the generic path found no scratch
 // Grover: iters fused iterations; d_trace receives |a_mark|^2 per iteration.
 void launch_grover(Handle *h, uint64_t mark_local, int mark_rank, int iters, double *d_trace);
 // Shor semantic-mode register (k_shor.cu): count / write {a : x^a = v mod N}
