@@ -80,6 +80,8 @@ _sig("orc_powmod", _u64, _u64, _u64, _u64)
 _sig("orc_gcd", _u64, _u64, _u64)
 _sig("orc_apply_angles", None, _p, _i32, C.POINTER(_Noise), _i32, _p, _u64, _u64, _i32)
 _sig("orc_qft", None, _p, _i32, _i32, _i32, _i32, C.POINTER(_Noise))
+_sig("orc_set_threads", None, _i32)
+_sig("orc_get_threads", _i32)
 _sig("orc_hadamard_range", None, _p, _i32, _i32, _i32)
 _sig("orc_aqft", None, _p, _i32, _i32, _i32, _i32, _i32, C.POINTER(_Noise))
 _sig("orc_measure_range", _u64, _p, _i32, _i32, _i32, _f64, _i32)
@@ -246,6 +248,15 @@ def apply_angles(psi, noise: Noise, kind, ang, ctrl_mask, ctrl_vals, q):
     a = np.zeros(4, np.float64); a[: len(ang)] = ang
     _lib.orc_apply_angles(_state(psi), _nq(psi), C.byref(noise._c), kind, _ptr(a),
                           ctrl_mask, ctrl_vals, q)
+
+
+def set_threads(k: int) -> None:
+    """OpenMP threads of the oracle's loops (0: default); results do not depend on it."""
+    _lib.orc_set_threads(int(k))
+
+
+def get_threads() -> int:
+    return int(_lib.orc_get_threads())
 
 
 def qft(psi, lo, m, inverse=False, noise: Noise | None = None):

@@ -23,6 +23,7 @@
  * Parity status of each function is listed in DESIGN.md §4 ("pins").
  */
 #include <complex.h>
+#include <omp.h>
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -1074,3 +1075,12 @@ int orc_shor_run(uint64_t N, int m, uint64_t seed, uint64_t run, int improved, i
     free(psi);
     return 0;
 }
+
+/* Host threads the oracle's parallel loops use (results are bit-identical for
+ * any count); 0 restores the OpenMP default.  Timing only (bench.py). */
+void orc_set_threads(int k)
+{
+    omp_set_num_threads(k > 0 ? k : omp_get_num_procs());
+}
+
+int orc_get_threads(void) { return omp_get_max_threads(); }
