@@ -35,6 +35,16 @@ __global__ void __launch_bounds__(kOpsThreads, 2) k_ops_pass(const __grid_consta
     extern __shared__ double2 tile_buf[];
     const OpsPass &P = L.P;
     const uint32_t tid = threadIdx.x;
+    // the op list in shared memory: indexed constant loads of a ~24 KB
+    // parameter block miss the constant cache (~16% measured), an LDS does not
+    GOp *ops = reinterpret_cast<GOp *>(tile_buf + ((size_t)1 << P.tbits));
+    {
+        const int4 *src = reinterpret_cast<const int4 *>(L.ops);
+        int4 *dst = reinterpret_cast<int4 *>(ops);
+        const int words = P.nops * (int)(sizeof(GOp) / sizeof(int4));
+        for (int w = tid; w < words; w += blockDim.x) dst[w] = src[w];
+        __syncthreads();
+    }
     const int tb = P.tbits - RB5;
 
     const OpsSeg &s0 = P.seg[0];
@@ -67,7 +77,7 @@ __global__ void __launch_bounds__(kOpsThreads, 2) k_ops_pass(const __grid_consta
                 v[k] = psi[o];
             }
         }
-        run_segments(v, L, T, tid, tb, tile_buf);
+        run_segments(v, L, T, tid, tb, tile_buf, CtaSync(), ops);
         {
             const uint64_t base = ib | tout;
 #pragma unroll
@@ -106,11 +116,11 @@ void launch_ops_pass(Handle *h, const OpsLaunch &L)
     // 10% faster there: no stage-buffer read of the first segment)
     static const double pp_max = std::getenv("QSIM_OPS_PP_MAX") ? std::atof(std::getenv("QSIM_OPS_PP_MAX")) : 12.0;
     if (cost <= pp_max && launch_ops_pass_pp(h, L)) return;
-    const size_t smem = sizeof(double2) << P.tbits;
+    const size_t smem = (sizeof(double2) << P.tbits) + (size_t)P.nops * sizeof(GOp);
     static uint64_t attr = 0;
     if (first_use_on_device(attr)) {
         cudaFuncSetAttribute(k_ops_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(sizeof(double2) << kTileMaxBits));
+                             (int)((sizeof(double2) << kTileMaxBits) + kOpsParam * sizeof(GOp)));
     }
     const int threads = 1 << (P.tbits - RB5);
     int per_sm = 1;

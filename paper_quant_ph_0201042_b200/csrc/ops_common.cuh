@@ -239,7 +239,7 @@ struct WgSync {
 
 template <class Sync = CtaSync>
 __device__ __forceinline__ void run_segments(double2 (&v)[NS5], const OpsLaunch &L, uint64_t T, uint32_t tid, int tb,
-                                             double2 *buf, Sync sync = Sync())
+                                             double2 *buf, Sync sync = Sync(), const GOp *ops = nullptr)
 {
     const OpsPass &P = L.P;
     uint32_t traj = P.bat_rank;
@@ -274,11 +274,12 @@ __device__ __forceinline__ void run_segments(double2 (&v)[NS5], const OpsLaunch 
             }
         }
         // the next op's dispatch word is fetched while this op runs
-        uint32_t code = sg.op_begin < sg.op_end ? L.ops[sg.op_begin].code : 0u;
+        const GOp *OP = ops ? ops : L.ops;   // a shared-memory copy of the op list, or the parameters
+        uint32_t code = sg.op_begin < sg.op_end ? OP[sg.op_begin].code : 0u;
         for (int i = sg.op_begin; i < sg.op_end; ++i) {
             const uint32_t c = code;
-            if (i + 1 < sg.op_end) code = L.ops[i + 1].code;
-            apply_op(v, L.ops[i], c, T, tpart, traj);
+            if (i + 1 < sg.op_end) code = OP[i + 1].code;
+            apply_op(v, OP[i], c, T, tpart, traj);
         }
         prev_stp = stp;
 #pragma unroll

@@ -227,6 +227,7 @@ struct OpsLaunch {
     GOp ops[kOpsParam];
 };
 static_assert(sizeof(OpsLaunch) <= 32000, "kernel parameter space");
+static_assert(sizeof(GOp) % 16 == 0, "op records are copied to shared memory in 16-byte words");
 void launch_ops_pass(Handle *h, const OpsLaunch &L);
 bool launch_ops_pass_tma(Handle *h, const OpsLaunch &L);
 bool launch_ops_pass_pp(Handle *h, const OpsLaunch &L);   // k_tma.cu ping-pong; false: geometry   // k_tma.cu; false: geometry unsupported
