@@ -110,11 +110,12 @@ void launch_ops_pass(Handle *h, const OpsLaunch &L)
         cost += c;
     }
     if (cost <= tma_max && launch_ops_pass_tma(h, L)) return;
-    // moderate FP64 work: the ping-pong TMA kernel overlaps loads with both
-    // warpgroups' arithmetic (configs[3]'s 9-gate H passes: 11.9 -> 10.6 ms);
-    // heavier lists stay on two CTAs per SM (configs[4]'s 25-gate passes are
-    // 10% faster there: no stage-buffer read of the first segment)
-    static const double pp_max = std::getenv("QSIM_OPS_PP_MAX") ? std::atof(std::getenv("QSIM_OPS_PP_MAX")) : 12.0;
+    // FP64 work beyond the TMA ring's: the ping-pong TMA kernel overlaps loads
+    // with both warpgroups' arithmetic (configs[3]'s 9-gate H passes: 11.9 ->
+    // 10.6 ms; configs[4]'s 25-gate passes 7% faster than k_ops_pass once both
+    // read the op list from shared memory); tiles that are not a <= 5-D TMA
+    // box go to k_ops_pass
+    static const double pp_max = std::getenv("QSIM_OPS_PP_MAX") ? std::atof(std::getenv("QSIM_OPS_PP_MAX")) : 1e9;
     if (cost <= pp_max && launch_ops_pass_pp(h, L)) return;
     const size_t smem = (sizeof(double2) << P.tbits) + (size_t)P.nops * sizeof(GOp);
     static uint64_t attr = 0;

@@ -715,6 +715,13 @@ __global__ void __launch_bounds__(2 * ops::kOpsThreads, 1)
     const OpsPass &P = L.P;
     const uint32_t wg = threadIdx.x / kOpsThreads;
     const uint32_t tid = threadIdx.x % kOpsThreads;
+    GOp *ops = reinterpret_cast<GOp *>(full + 8);   // the op list in shared memory (see k_ops_pass)
+    {
+        const int4 *src = reinterpret_cast<const int4 *>(L.ops);
+        int4 *dst = reinterpret_cast<int4 *>(ops);
+        const int words = P.nops * (int)(sizeof(GOp) / sizeof(int4));
+        for (int w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -763,7 +770,7 @@ __global__ void __launch_bounds__(2 * ops::kOpsThreads, 1)
                 if (k & (1 << b)) o |= pin[b];
             v[k] = buf[o];
         }
-        run_segments(v, L, T, tid, tb, buf, sync);
+        run_segments(v, L, T, tid, tb, buf, sync, ops);
         // the stage is no longer read: the next load into it may leave
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         sync();
@@ -1076,10 +1083,11 @@ bool launch_ops_pass_pp(Handle *h, const OpsLaunch &L)
     TmaArgs ta;
     std::memset(&ta, 0, sizeof ta);
     if (!build_side(h->psi, h->nl, tp, fid, im, ta.in_first, ta.in_len, ta.in_rank)) return false;
-    const size_t smem = (size_t)kStages * kTileBytes + 8 * sizeof(uint64_t);
+    const size_t smem = (size_t)kStages * kTileBytes + 8 * sizeof(uint64_t) + (size_t)P.nops * sizeof(GOp);
     static uint64_t attr = 0;
     if (first_use_on_device(attr))
-        cudaFuncSetAttribute(k_ops_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_ops_pp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)((size_t)kStages * kTileBytes + 8 * sizeof(uint64_t) + kOpsParam * sizeof(GOp)));
     const uint64_t ntiles = 1ull << P.nfix;
     const unsigned grid = (unsigned)std::min<uint64_t>((ntiles + 1) / 2, (uint64_t)h->num_sms);
     prof_begin(h);
