@@ -29,6 +29,9 @@ namespace {
 
 using namespace ops;
 
+// segments whose thread parts are precomputed in shared memory (more: computed per tile)
+constexpr int kOpsPreSegs = 12;
+
 __global__ void __launch_bounds__(kOpsThreads, 2) k_ops_pass(const __grid_constant__ OpsLaunch L, double2 *psi,
                                                              uint64_t ntiles)
 {
@@ -38,14 +41,30 @@ __global__ void __launch_bounds__(kOpsThreads, 2) k_ops_pass(const __grid_consta
     // the op list in shared memory: indexed constant loads of a ~24 KB
     // parameter block miss the constant cache (~16% measured), an LDS does not
     GOp *ops = reinterpret_cast<GOp *>(tile_buf + ((size_t)1 << P.tbits));
+    // per-tile index arithmetic from tables built once: the fixed-bit part of
+    // a tile's offset byte by byte, and every segment's thread part
+    uint64_t *ibtab = reinterpret_cast<uint64_t *>(ops + P.nops);   // [4][256]
+    uint32_t *tparts = reinterpret_cast<uint32_t *>(ibtab + 4 * 256);
+    const bool pre_tp = P.nseg <= kOpsPreSegs;
+    const int tb = P.tbits - RB5;
     {
         const int4 *src = reinterpret_cast<const int4 *>(L.ops);
         int4 *dst = reinterpret_cast<int4 *>(ops);
         const int words = P.nops * (int)(sizeof(GOp) / sizeof(int4));
         for (int w = tid; w < words; w += blockDim.x) dst[w] = src[w];
+        for (int e = tid; e < 4 * 256; e += blockDim.x) {
+            const int k = e >> 8, x = e & 255;
+            uint64_t o = 0;
+            for (int j = 0; j < 8; ++j) {
+                const int f = 8 * k + j;
+                if (f < P.nfix && ((x >> j) & 1)) o |= 1ull << P.fin_pos[f];
+            }
+            ibtab[e] = o;
+        }
+        if (pre_tp)
+            for (int s = 0; s < P.nseg; ++s) tparts[(s << (kTileMaxBits - RB5)) + tid] = seg_thread_part(P.seg[s], tb, tid);
         __syncthreads();
     }
-    const int tb = P.tbits - RB5;
 
     const OpsSeg &s0 = P.seg[0];
     const OpsSeg &sL = P.seg[P.nseg - 1];
@@ -63,8 +82,8 @@ __global__ void __launch_bounds__(kOpsThreads, 2) k_ops_pass(const __grid_consta
     }
 
     for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x) {
-        uint64_t ib = 0;
-        for (int f = 0; f < P.nfix; ++f) ib |= ((T >> f) & 1u) << P.fin_pos[f];
+        const uint64_t ib = ibtab[T & 255] | ibtab[256 + ((T >> 8) & 255)] | ibtab[512 + ((T >> 16) & 255)] |
+                            ibtab[768 + ((T >> 24) & 255)];
         double2 v[NS5];
         {
             const uint64_t base = ib | tin;
@@ -77,7 +96,7 @@ __global__ void __launch_bounds__(kOpsThreads, 2) k_ops_pass(const __grid_consta
                 v[k] = psi[o];
             }
         }
-        run_segments(v, L, T, tid, tb, tile_buf, CtaSync(), ops);
+        run_segments(v, L, T, tid, tb, tile_buf, CtaSync(), ops, pre_tp ? tparts : nullptr);
         {
             const uint64_t base = ib | tout;
 #pragma unroll
@@ -117,11 +136,14 @@ void launch_ops_pass(Handle *h, const OpsLaunch &L)
     // box go to k_ops_pass
     static const double pp_max = std::getenv("QSIM_OPS_PP_MAX") ? std::atof(std::getenv("QSIM_OPS_PP_MAX")) : 1e9;
     if (cost <= pp_max && launch_ops_pass_pp(h, L)) return;
-    const size_t smem = (sizeof(double2) << P.tbits) + (size_t)P.nops * sizeof(GOp);
+    const size_t pre = (P.nseg <= kOpsPreSegs ? (size_t)P.nseg << (kTileMaxBits - RB5) : 0) * sizeof(uint32_t);
+    const size_t smem = (sizeof(double2) << P.tbits) + (size_t)P.nops * sizeof(GOp) + 4 * 256 * sizeof(uint64_t) + pre;
     static uint64_t attr = 0;
     if (first_use_on_device(attr)) {
         cudaFuncSetAttribute(k_ops_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)((sizeof(double2) << kTileMaxBits) + kOpsParam * sizeof(GOp)));
+                             (int)((sizeof(double2) << kTileMaxBits) + kOpsParam * sizeof(GOp) +
+                                   4 * 256 * sizeof(uint64_t) +
+                                   ((size_t)kOpsPreSegs << (kTileMaxBits - RB5)) * sizeof(uint32_t)));
     }
     const int threads = 1 << (P.tbits - RB5);
     int per_sm = 1;

@@ -239,7 +239,8 @@ struct WgSync {
 
 template <class Sync = CtaSync>
 __device__ __forceinline__ void run_segments(double2 (&v)[NS5], const OpsLaunch &L, uint64_t T, uint32_t tid, int tb,
-                                             double2 *buf, Sync sync = Sync(), const GOp *ops = nullptr)
+                                             double2 *buf, Sync sync = Sync(), const GOp *ops = nullptr,
+                                             const uint32_t *tparts = nullptr)
 {
     const OpsPass &P = L.P;
     uint32_t traj = P.bat_rank;
@@ -248,7 +249,8 @@ __device__ __forceinline__ void run_segments(double2 (&v)[NS5], const OpsLaunch 
     uint32_t prev_wsw[RB5] = {0, 0, 0, 0, 0};
     for (int s = 0; s < P.nseg; ++s) {
         const OpsSeg &sg = P.seg[s];
-        const uint32_t tpart = seg_thread_part(sg, tb, tid);
+        // thread part of the tile index: precomputed per segment (shared memory) or here
+        const uint32_t tpart = tparts ? tparts[(s << (kTileMaxBits - RB5)) + tid] : seg_thread_part(sg, tb, tid);
         const uint32_t stp = swz(tpart);
         uint32_t wsw[RB5];
 #pragma unroll
