@@ -379,32 +379,61 @@ int flush_queue(Handle *h)
     constexpr size_t kPassCap = 512;   // bounds the planner's work per pass
     static thread_local OpsLaunch L;   // 28 KiB, copied into the launch parameters
     while (!rem.empty()) {
-        // ---- 1. pass selection
-        std::vector<int> act;
-        std::vector<char> is_act(nl, 0), blocked(nl, 0);
-        std::vector<QOp> take, left;
-        for (const QOp &op : rem) {
-            uint64_t touch = op.cmask;
-            if (op.tpos >= 0) touch |= 1ull << op.tpos;
-            bool ok = take.size() < kPassCap;
-            for (int p = 0; p < nl && ok; ++p)
-                if (((touch >> p) & 1) && blocked[p]) ok = false;
-            if (ok && !op.diag && !is_act[op.tpos]) {
-                if ((int)act.size() < amax) {
-                    act.push_back(op.tpos);
-                    is_act[op.tpos] = 1;
+        // ---- 1. pass selection: the closure of the queue (in order, up to
+        // commutation: a gate that cannot join blocks its positions) under an
+        // active set built greedily, or under each window of amax consecutive
+        // positions; the candidate applying the most register work wins.  A
+        // window keeps a brickwork's light cone together (the greedy set
+        // drifts into every other qubit, one layer per pass) and makes the
+        // tile a TMA box.
+        struct Sel {
+            std::vector<char> take;
+            std::vector<int> act;
+            double w = 0.0;
+        };
+        auto closure = [&](uint64_t allowed) {   // allowed: active-position mask (~0: any)
+            Sel s;
+            s.take.assign(rem.size(), 0);
+            uint64_t is_act = 0, blocked = 0;
+            size_t ntake = 0;
+            for (size_t i = 0; i < rem.size(); ++i) {
+                const QOp &op = rem[i];
+                uint64_t touch = op.cmask;
+                if (op.tpos >= 0) touch |= 1ull << op.tpos;
+                bool ok = ntake < kPassCap && !(touch & blocked);
+                if (ok && !op.diag && !((is_act >> op.tpos) & 1)) {
+                    if ((int)s.act.size() < amax && ((allowed >> op.tpos) & 1)) {
+                        s.act.push_back(op.tpos);
+                        is_act |= 1ull << op.tpos;
+                    } else {
+                        ok = false;
+                    }
+                }
+                if (ok) {
+                    s.take[i] = 1;
+                    ++ntake;
+                    s.w += op.diag ? 0.5 : 1.0;
                 } else {
-                    ok = false;
+                    blocked |= touch;
                 }
             }
-            if (ok) {
-                take.push_back(op);
-            } else {
-                left.push_back(op);
-                for (int p = 0; p < nl; ++p)
-                    if ((touch >> p) & 1) blocked[p] = 1;
+            return s;
+        };
+        static const bool greedy_only = std::getenv("QSIM_PASS_GREEDY") != nullptr;
+        Sel best = closure(~0ull);
+        if (!greedy_only && nl > amax) {
+            uint64_t batch_mask = 0;
+            for (int p = 0; p < nl; ++p)
+                if (is_batch[p]) batch_mask |= 1ull << p;
+            for (int p0 = 0; p0 + amax <= nl; ++p0) {
+                const uint64_t win = (((1ull << amax) - 1) << p0) & ~batch_mask;
+                Sel s = closure(win);
+                if (s.w > best.w) best = std::move(s);
             }
         }
+        std::vector<int> act = best.act;
+        std::vector<QOp> take, left;
+        for (size_t i = 0; i < rem.size(); ++i) (best.take[i] ? take : left).push_back(rem[i]);
         rem.swap(left);
         // A pass of one sparse gate (controlled, or a phase on half the
         // amplitudes) reads and writes every amplitude; the unfused kernel
@@ -623,11 +652,16 @@ int flush_queue(Handle *h)
                     ++cnt[L.ops[i].kind & 7];
                     thr += L.ops[i].tm != 0;
                 }
+                std::vector<int> tp(P.in_pos, P.in_pos + P.tbits);
+                std::sort(tp.begin(), tp.end());
+                std::string tps;
+                for (int x : tp) tps += std::to_string(x) + ",";
                 std::fprintf(stderr,
                              "[qsim plan] nl=%d tile=%d nseg=%d nops=%d dense=%d cdense=%d dense2=%d diagw=%d "
-                             "diagt=%d diagf=%d phase=%d denset=%d thread-ctrl=%d\n",
+                             "diagt=%d diagf=%d phase=%d denset=%d thread-ctrl=%d positions=%s\n",
                              nl, tbits, P.nseg, P.nops, cnt[GOP_DENSE], cnt[GOP_CDENSE], cnt[GOP_DENSE2],
-                             cnt[GOP_DIAGW], cnt[GOP_DIAGT], cnt[GOP_DIAGF], cnt[GOP_PHASE], cnt[GOP_DENSET], thr);
+                             cnt[GOP_DIAGW], cnt[GOP_DIAGT], cnt[GOP_DIAGF], cnt[GOP_PHASE], cnt[GOP_DENSET], thr,
+                             tps.c_str());
             }
             launch_ops_pass(h, L);
             if (int rc = launch_check(h, "fused gate pass")) return rc;
