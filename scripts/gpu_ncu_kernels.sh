@@ -12,7 +12,7 @@ cap() {  # name kernel-regex skip cmd...
   ncu -i gpurun_out/prof_$name.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/prof_${name}_src.csv 2>&1
   rm -f gpurun_out/prof_$name.ncu-rep
 }
-cap ops_pass k_ops_pass 3 python tools/run_cfg.py 4m
+cap ops_pass k_ops_pass 0 python tools/run_cfg.py 4m
 cap ops_pp k_ops_pp 0 python tools/run_cfg.py 4m
 cap qft_gen k_qft_gen 0 python tools/run_cfg.py 3n
 cap perm_ring k_perm_ring 0 python tools/run_cfg.py 3
