@@ -428,7 +428,9 @@ int flush_queue(Handle *h)
             for (int p0 = 0; p0 + amax <= nl; ++p0) {
                 const uint64_t win = (((1ull << amax) - 1) << p0) & ~batch_mask;
                 Sel s = closure(win);
-                if (s.w > best.w) best = std::move(s);
+                // a window's tile is a TMA box (k_ops_pp, ~7% faster per pass):
+                // it wins ties with the greedy set and a 5% margin
+                if (s.w * 1.05 > best.w) best = std::move(s);
             }
         }
         std::vector<int> act = best.act;
