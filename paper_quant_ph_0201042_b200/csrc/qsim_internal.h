@@ -228,6 +228,8 @@ struct OpsLaunch {
 };
 static_assert(sizeof(OpsLaunch) <= 32000, "kernel parameter space");
 static_assert(sizeof(GOp) % 16 == 0, "op records are copied to shared memory in 16-byte words");
+// k_ops_pp keeps 3 x 64 KiB stages and the op list in one CTA's shared memory (227 KiB opt-in)
+static_assert(3 * (16 << kTileMaxBits) + 64 + kOpsParam * sizeof(GOp) <= 232448, "k_ops_pp shared memory");
 void launch_ops_pass(Handle *h, const OpsLaunch &L);
 bool launch_ops_pass_tma(Handle *h, const OpsLaunch &L);
 bool launch_ops_pass_pp(Handle *h, const OpsLaunch &L);   // k_tma.cu ping-pong; false: geometry   // k_tma.cu; false: geometry unsupported
