@@ -394,10 +394,15 @@ constexpr int kGenInfeasible = 1000;   // dry run: a pass the generalised kernel
 int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCircuit *gc = nullptr,
                 bool dry = false, bool even = false)
 {
-    // default 7: a 2^12 tile then carries >= 5 passive bits, i.e. 512-byte runs, which
-    // the TMA streams at ~96% of HBM peak (10 wires -> 64-byte runs, ~70%)
-    static const int amax_env = getenv("QSIM_QFT_AMAX") ? atoi(getenv("QSIM_QFT_AMAX")) : 7;
-    const int amax = amax_env < 1 ? 1 : (amax_env > 10 ? 10 : amax_env);
+    // default 8: a 2^12 tile then carries >= 4 passive bits (>= 256-byte runs); measured
+    // (tools/probe_amax.py) against 7 (>= 512-byte runs) and 9 (128-byte runs): 8 needs
+    // fewer passes for most register sizes (n = 29: 4 instead of 5, a 22-wire range 3
+    // instead of 4) and is as fast per pass -- the n = 28 QFT runs 8,7,7,6 in 5.45 ms
+    // (7,7,7,7: 5.49 ms); 10 wires would leave 64-byte runs (~70% of peak)
+    // (the generalised kernel, FP64-heavier per wire, stays at 7: its 8-wire passes ran slower)
+    static const int amax_env = getenv("QSIM_QFT_AMAX") ? atoi(getenv("QSIM_QFT_AMAX")) : 0;
+    const int amax_def = amax_env > 0 ? amax_env : (gc ? 7 : 8);
+    const int amax = amax_def < 1 ? 1 : (amax_def > 10 ? 10 : amax_def);
     Handle *h0 = R[0];
     const int G = (m + amax - 1) / amax;
     std::vector<int> gsize(G, m / G);
