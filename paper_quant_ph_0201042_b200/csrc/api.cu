@@ -411,7 +411,22 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
     // bits: without room for a scratch shard the passes run in place and the
     // closing swaps become a relabel (as on several ranks)
     const bool block_moves = qft && h0->world == 1 && ensure_scratch(h0) == QSIM_OK;
-    if (block_moves && G > 1 && gsize[0] < amax && !even) {
+    if (block_moves && G > 2 && amax == 8 && !gc && !even) {
+        // measured per-pass efficiency (tools/probe_blocks.sh): 8- and 6-wire
+        // passes stream best, 7 a little worse, <= 5 and a last block of 8
+        // worse: 8,...,8 then the remainder r of the last two blocks as (8, r-8)
+        // when r-8 >= 6, else split evenly -- n = 28: 8,8,6,6 (5.43 ms vs
+        // 5.45 for 8,7,7,6), n = 29: 8,8,7,6, n = 30: 8,8,8,6
+        for (int g = 0; g < G - 2; ++g) gsize[g] = 8;
+        const int r = m - 8 * (G - 2);
+        if (r - 8 >= 6) {
+            gsize[G - 2] = 8;
+            gsize[G - 1] = r - 8;
+        } else {
+            gsize[G - 2] = (r + 1) / 2;
+            gsize[G - 1] = r / 2;
+        }
+    } else if (block_moves && G > 1 && gsize[0] < amax && !even) {
         // the first block lands on the lowest positions; with >= 7 wires its
         // last register window stays clear of the 3 lowest, so the store keeps
         // 128-byte thread runs and the pass fits the specialised kernel
@@ -419,6 +434,20 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
         gsize[0] = amax;
         const int rest = m - amax, G1 = G - 1;
         for (int g = 1; g < G; ++g) gsize[g] = rest / G1 + (g - 1 < rest % G1 ? 1 : 0);
+    }
+    if (const char *bl = getenv("QSIM_QFT_BLOCKS")) {   // measurement knob: explicit block sizes (tools/probe_blocks.sh)
+        std::vector<int> v;
+        int s = 0;
+        for (const char *c = bl; *c;) {
+            const int x = atoi(c);
+            v.push_back(x);
+            s += x;
+            while (*c && *c != ',') ++c;
+            if (*c) ++c;
+        }
+        bool ok = s == m && !v.empty();
+        for (int x : v) ok &= x >= 1 && x <= 10;
+        if (ok) gsize = v;
     }
     if (block_moves) {
         if (int rc = dist_canonicalize(R)) return rc;
@@ -430,7 +459,7 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
     std::vector<int> wp(m);                // current position of wire w (same on every rank)
     for (int w = 0; w < m; ++w) wp[w] = h0->pos[lo + w];
     int a0 = 0;
-    for (int g = 0; g < G; ++g) {
+    for (int g = 0; g < (int)gsize.size(); ++g) {
         const int a = gsize[g];
         std::vector<int> act;
         for (int u = 0; u < a; ++u) act.push_back(lo + a0 + u);
