@@ -424,6 +424,34 @@ double qsim_shor_prob_succ(uint64_t N, uint64_t phi);
  * counter = (i lo, i hi, j, tag); out[0] = x0 | x1 << 32, out[1] = x2 | x3 << 32. */
 void qsim_philox_draw(uint64_t seed, uint32_t tag, uint64_t i, uint32_t j, uint64_t out[2]);
 
+/* count consecutive draws: out[2k], out[2k+1] = qsim_philox_draw(seed, tag,
+ * i0 + k, j) for k < count (caller-owned buffer of 2 * count words). */
+void qsim_philox_draws(uint64_t seed, uint32_t tag, uint64_t i0, uint64_t count, uint32_t j, uint64_t *out);
+
+/* ---------------------------------------------------------------- gate lists */
+
+/* One queued gate: type QSIM_GT_MATRIX applies U to qubit q (controlled by
+ * ctrl_mask / ctrl_vals when ctrl_mask != 0) exactly as qsim_apply_1q /
+ * qsim_apply_ctrl; type QSIM_GT_ANGLES applies the angle-form gate `akind`
+ * (QSIM_GATE_*) with angles ang[] as qsim_apply_angles (gate noise and the
+ * gate counter included). */
+enum { QSIM_GT_MATRIX = 0, QSIM_GT_ANGLES = 1 };
+typedef struct {
+    int type;
+    int q;
+    int akind;
+    int pad_;
+    uint64_t ctrl_mask, ctrl_vals;
+    double ang[4];
+    qsim_c128 U[4];
+} qsim_gate_t;
+
+/* Apply gates[0 .. count) in order, as the corresponding single calls would
+ * (one C-ABI crossing for a whole circuit).  Stops at the first invalid gate:
+ * its error code is returned, *done (if not NULL) = the number applied before
+ * it. */
+int qsim_apply_gates(qsim_t *h, const qsim_gate_t *gates, int count, int *done);
+
 #ifdef __cplusplus
 }
 #endif

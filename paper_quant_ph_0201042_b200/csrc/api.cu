@@ -620,6 +620,16 @@ void qsim_philox_draw(uint64_t seed, uint32_t tag, uint64_t i, uint32_t j, uint6
     out[1] = d.b;
 }
 
+void qsim_philox_draws(uint64_t seed, uint32_t tag, uint64_t i0, uint64_t count, uint32_t j, uint64_t *out)
+{
+    if (!out) return;
+    for (uint64_t k = 0; k < count; ++k) {
+        const u64x2 d = draw(seed, tag, i0 + k, j);
+        out[2 * k] = d.a;
+        out[2 * k + 1] = d.b;
+    }
+}
+
 static int create_common(int n, int world, int rank, int device, qsim_t **out)
 {
     *out = nullptr;
@@ -1046,6 +1056,26 @@ int qsim_apply_angles(qsim_t *h, int kind, const double *ang, uint64_t cmask, ui
     h->gcount++;
     const Ranks R = ranks_of(h);
     return lift(h, R, apply_gate(R, cmask, cvals, q, U));
+}
+
+int qsim_apply_gates(qsim_t *h, const qsim_gate_t *gates, int count, int *done)
+{
+    QS_CHECK_HANDLE(h);
+    if (done) *done = 0;
+    if (count < 0 || (count > 0 && !gates)) return fail(h, QSIM_EINVAL, "gate list");
+    for (int i = 0; i < count; ++i) {
+        const qsim_gate_t &g = gates[i];
+        int rc;
+        if (g.type == QSIM_GT_MATRIX)
+            rc = g.ctrl_mask ? qsim_apply_ctrl(h, g.ctrl_mask, g.ctrl_vals, g.q, g.U) : qsim_apply_1q(h, g.q, g.U);
+        else if (g.type == QSIM_GT_ANGLES)
+            rc = qsim_apply_angles(h, g.akind, g.ang, g.ctrl_mask, g.ctrl_vals, g.q);
+        else
+            rc = fail(h, QSIM_EINVAL, "unknown gate type in the list");
+        if (rc) return rc;
+        if (done) *done = i + 1;
+    }
+    return QSIM_OK;
 }
 
 int qsim_set_gate_noise(qsim_t *h, uint64_t seed, double sigma)

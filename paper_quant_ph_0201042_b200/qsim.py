@@ -97,6 +97,7 @@ _sig("qsim_swap", _i32, _H, _i32, _i32)
 _sig("qsim_hadamard", _i32, _H, _i32, _i32)
 _sig("qsim_qft", _i32, _H, _i32, _i32, _i32)
 _sig("qsim_fft", _i32, _H, _i32, _i32, _i32)
+_sig("qsim_philox_draws", None, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint32, C.POINTER(C.c_uint64))
 _sig("qsim_aqft", _i32, _H, _i32, _i32, _i32, _i32)
 _sig("qsim_hadamard_angles", _i32, _H, _i32, _i32)
 _sig("qsim_measure_range", _i32, _H, _i32, _i32, _f64, _i32, C.POINTER(_u64))
@@ -276,6 +277,47 @@ def qsim_hadamard_angles(h, lo: int, m: int) -> None:
     """H = U_R(pi/4) U_P1(pi) on every qubit of [lo, lo+m), counted and noisy
     like qsim_apply_angles (fused passes where possible)."""
     _chk(h, lib.qsim_hadamard_angles(h, lo, m))
+
+
+QSIM_GT_MATRIX, QSIM_GT_ANGLES = 0, 1
+
+
+class qsim_gate_t(C.Structure):
+    _fields_ = [("type", C.c_int32), ("q", C.c_int32), ("akind", C.c_int32), ("pad_", C.c_int32),
+                ("ctrl_mask", C.c_uint64), ("ctrl_vals", C.c_uint64), ("ang", C.c_double * 4),
+                ("U", C.c_double * 8)]
+
+
+lib.qsim_apply_gates.restype = C.c_int32
+lib.qsim_apply_gates.argtypes = [_H, C.POINTER(qsim_gate_t), C.c_int32, C.POINTER(C.c_int32)]
+
+
+def qsim_philox_draws(seed: int, tag: int, i0: int, count: int, j: int = 0) -> np.ndarray:
+    """(count, 2) uint64 array of consecutive draws (i = i0 .. i0+count-1)."""
+    out = np.zeros((count, 2), np.uint64)
+    lib.qsim_philox_draws(seed, tag, i0, count, j, out.ctypes.data_as(C.POINTER(C.c_uint64)))
+    return out
+
+
+def qsim_apply_gates(h, gates) -> None:
+    """gates: sequence of ("matrix", q, U, ctrl_mask, ctrl_vals) or
+    ("angles", q, akind, ang, ctrl_mask, ctrl_vals); one C-ABI call."""
+    arr = (qsim_gate_t * max(len(gates), 1))()
+    for i, g in enumerate(gates):
+        x = arr[i]
+        if g[0] == "matrix":
+            _, q, U, cm, cv = g
+            u = np.asarray(U, dtype=np.complex128).reshape(4)
+            x.type, x.q, x.ctrl_mask, x.ctrl_vals = QSIM_GT_MATRIX, q, cm, cv
+            for k in range(4):
+                x.U[2 * k], x.U[2 * k + 1] = u[k].real, u[k].imag
+        else:
+            _, q, akind, ang, cm, cv = g
+            x.type, x.q, x.akind, x.ctrl_mask, x.ctrl_vals = QSIM_GT_ANGLES, q, akind, cm, cv
+            for k, a in enumerate(ang):
+                x.ang[k] = a
+    done = C.c_int32(0)
+    _chk(h, lib.qsim_apply_gates(h, arr, len(gates), C.byref(done)))
 
 
 def qsim_aqft(h, lo: int, m: int, b: int, inverse: bool = False) -> None:

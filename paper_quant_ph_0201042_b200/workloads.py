@@ -34,22 +34,31 @@ NOT = [[0, 1], [1, 0]]
 
 
 def run_cfg0(h, n: int = 10, seed: int = 1, ngates: int = 200):
-    """configs[0]: random circuit from |0..0> (R21).  Returns the gate list."""
+    """configs[0]: random circuit from |0..0> (R21).  Returns the gate list.
+    The draws come in three batched calls and the circuit goes to the library
+    as one gate list (one C-ABI crossing); the gates are those of R21."""
     Q.qsim_set_basis(h, 0)
-    gates = []
+    dg = Q.qsim_philox_draws(seed, Q.QSIM_TAG_GATE, 0, ngates, 0)
+    dh0 = Q.qsim_philox_draws(seed, Q.QSIM_TAG_HAAR, 0, ngates, 0)
+    dh1 = Q.qsim_philox_draws(seed, Q.QSIM_TAG_HAAR, 0, ngates, 1)
+    dp = Q.qsim_philox_draws(seed, Q.QSIM_TAG_PAIR, 0, ngates, 0)
+    gates, glist = [], []
     for g in range(ngates):
-        a, b = Q.qsim_philox_draw(seed, Q.QSIM_TAG_GATE, g, 0)
+        a, b = int(dg[g, 0]), int(dg[g, 1])
         if u01(a) < 0.7:
             q = uint_below(b, n)
-            Q.qsim_apply_angles(h, Q.QSIM_GATE_HAAR, haar_angles(seed, g), 0, 0, q)
+            a0, b0, a1, b1 = int(dh0[g, 0]), int(dh0[g, 1]), int(dh1[g, 0]), int(dh1[g, 1])
+            ang = [TWO_PI * u01(b0), TWO_PI * u01(a1), math.acos(math.sqrt(u01(a0))), TWO_PI * u01(b1)]
+            glist.append(("angles", q, Q.QSIM_GATE_HAAR, ang, 0, 0))
             gates.append(("haar", q, -1))
         else:
-            a2, b2 = Q.qsim_philox_draw(seed, Q.QSIM_TAG_PAIR, g, 0)
+            a2, b2 = int(dp[g, 0]), int(dp[g, 1])
             c = uint_below(a2, n)
             t = uint_below(b2, n - 1)
             t += t >= c
-            Q.qsim_apply_ctrl(h, 1 << c, 1 << c, t, NOT)
+            glist.append(("matrix", t, NOT, 1 << c, 1 << c))
             gates.append(("cnot", t, c))
+    Q.qsim_apply_gates(h, glist)
     return gates
 
 

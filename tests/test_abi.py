@@ -56,3 +56,13 @@ def test_create_without_gpu_fails_loudly():
         Q.qsim_create(10)
     assert e.value.code == Q.QSIM_ENODEV
     assert Q.qsim_memory_bytes(30) == 1 << 34
+
+
+def test_batched_philox_draws_equal_single_draws():
+    """qsim_philox_draws (the batched draw) = qsim_philox_draw per counter; no GPU needed."""
+    import numpy as np
+    from paper_quant_ph_0201042_b200 import qsim as Q
+    d = Q.qsim_philox_draws(7, 2, 1000, 64, 1)
+    for k in range(64):
+        assert tuple(int(x) for x in d[k]) == Q.qsim_philox_draw(7, 2, 1000 + k, 1)
+    assert d.dtype == np.uint64

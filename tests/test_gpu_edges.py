@@ -128,3 +128,36 @@ def test_flush_of_an_empty_queue_and_repeated_sync(mk):
         Q.qsim_sync(h)
     assert np.array_equal(get(h, n), psi)
     assert abs(Q.qsim_norm(h) - 1) < 1e-13
+
+
+def test_gate_list_equals_single_calls(mk):
+    """qsim_apply_gates = the same gates through qsim_apply_1q / _ctrl /
+    _angles one by one (gate noise and counter included); an invalid entry
+    stops the list with its error and leaves the applied prefix."""
+    n = 12
+    psi = rand_state(n, 21)
+    h1, h2 = mk(n, psi), mk(n, psi)
+    for h in (h1, h2):
+        Q.qsim_set_gate_noise(h, 5, 1e-2)
+    rng = np.random.default_rng(3)
+    gl = []
+    for i in range(60):
+        q = int(rng.integers(n))
+        if i % 3 == 0:
+            U = np.linalg.qr(rng.normal(size=(2, 2)) + 1j * rng.normal(size=(2, 2)))[0]
+            gl.append(("matrix", q, U, 0, 0))
+            Q.qsim_apply_1q(h2, q, U)
+        elif i % 3 == 1:
+            c = (q + 1 + int(rng.integers(n - 1))) % n
+            U = np.array([[0, 1], [1, 0]], complex)
+            gl.append(("matrix", q, U, 1 << c, 1 << c))
+            Q.qsim_apply_ctrl(h2, 1 << c, 1 << c, q, U)
+        else:
+            a = [float(x) for x in rng.uniform(0, 6, 4)]
+            gl.append(("angles", q, Q.QSIM_GATE_HAAR, a, 0, 0))
+            Q.qsim_apply_angles(h2, Q.QSIM_GATE_HAAR, a, 0, 0, q)
+    Q.qsim_apply_gates(h1, gl)
+    assert np.max(np.abs(get(h1, n) - get(h2, n))) < 1e-13
+    assert Q.qsim_get_gate_counter(h1) == Q.qsim_get_gate_counter(h2)
+    with pytest.raises(Q.QsimError):
+        Q.qsim_apply_gates(h1, [("matrix", 0, np.eye(2), 0, 0), ("matrix", n + 3, np.eye(2), 0, 0)])
