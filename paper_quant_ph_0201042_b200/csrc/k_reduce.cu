@@ -90,6 +90,32 @@ __global__ void __launch_bounds__(kThreads) k_probs_contig(const double2 *__rest
     (void)nl;
 }
 
+// Marginals with one warp per value y (rest = 2^(nl-m) amplitudes per y, up
+// to 2^14): grid-stride over y, lanes stride the y's amplitudes (16-byte
+// loads, 512 contiguous bytes per warp load when the range sits above a
+// contiguous low run), fixed xor tree; no per-y block and no finishing pass.
+__global__ void __launch_bounds__(256) k_probs_warp(const double2 *__restrict__ psi, int pl, int m, uint64_t rest,
+                                                    uint64_t ny, double *__restrict__ out)
+{
+    const uint64_t lowmask = (1ull << pl) - 1;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t y = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); y < ny; y += warps) {
+        double acc0 = 0.0, acc1 = 0.0;
+        uint64_t r = lane;
+        for (; r + 32 < rest; r += 64) {
+            const uint64_t i0 = ((r >> pl) << (pl + m)) | (y << pl) | (r & lowmask);
+            const uint64_t r1 = r + 32;
+            const uint64_t i1 = ((r1 >> pl) << (pl + m)) | (y << pl) | (r1 & lowmask);
+            acc0 += abs2(psi[i0]);
+            acc1 += abs2(psi[i1]);
+        }
+        if (r < rest) acc0 += abs2(psi[((r >> pl) << (pl + m)) | (y << pl) | (r & lowmask)]);
+        const double s = warp_sum(acc0 + acc1);
+        if (lane == 0) out[y] = s;
+    }
+}
+
 // per-y tree over its chunks
 __global__ void k_probs_finish(const double *__restrict__ part, uint64_t ny, uint64_t nchunk,
                                double *__restrict__ out)
@@ -257,6 +283,16 @@ void launch_probs_contig(Handle *h, int pl, int m, double *d_out)
     cudaSetDevice(h->device);   // members of a rank group may live on different devices
     const uint64_t ny = 1ull << m;
     const uint64_t rest = h->local_dim() >> m;
+    if (ny >= (uint64_t)h->num_sms * 64 && rest >= 64 && rest <= (1ull << 14)) {
+        // many small marginal bins: a warp per bin (a block per bin spent its
+        // time in scheduling: 5.97 TB/s on configs[3]'s 2^20 bins of 1024)
+        const uint64_t want = (ny + 7) / 8;
+        const uint64_t cap = (uint64_t)h->num_sms * 16;
+        prof_begin(h);
+        k_probs_warp<<<(unsigned)(want < cap ? want : cap), 256, 0, h->stream>>>(h->psi, pl, m, rest, ny, d_out);
+        prof_end(h, "k_probs_warp", h->local_dim() * 16);
+        return;
+    }
     // chunks so that the grid has >= ~2 waves of blocks
     uint64_t nchunk = 1;
     while (ny * nchunk < (uint64_t)h->num_sms * 16 && rest / (nchunk * 2) >= kThreads && nchunk < 64) nchunk *= 2;
