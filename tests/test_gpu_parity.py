@@ -149,7 +149,10 @@ def test_hadamard_range(reg, n, lo, m):
 
 @pytest.mark.parametrize("inverse", [False, True])
 @pytest.mark.parametrize("n,lo,m", [(9, 0, 9), (12, 0, 12), (16, 0, 16), (21, 0, 21), (13, 0, 10),
-                                    (13, 3, 10), (18, 2, 11), (17, 7, 10), (20, 0, 14), (6, 0, 6)])
+                                    (13, 3, 10), (18, 2, 11), (17, 7, 10), (20, 0, 14), (6, 0, 6),
+                                    # block partitions: 8,8,1+.. splits -- (8, r-8) and even splits of r
+                                    (17, 0, 17), (19, 0, 19), (22, 0, 22), (23, 0, 23), (24, 1, 22),
+                                    (24, 0, 24), (22, 3, 18)])
 def test_qft_matches_oracle_circuit(reg, n, lo, m, inverse):
     psi = rand_state(n, 7 * n + lo)
     h = reg(n, psi)
