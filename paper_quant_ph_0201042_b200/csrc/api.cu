@@ -410,7 +410,8 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
     // the block-move layout writes out of place whenever a pass moves fixed
     // bits: without room for a scratch shard the passes run in place and the
     // closing swaps become a relabel (as on several ranks)
-    const bool block_moves = qft && h0->world == 1 && ensure_scratch(h0) == QSIM_OK;
+    static const bool no_moves = getenv("QSIM_NO_BLOCK_MOVES") != nullptr;   // measurement knob
+    const bool block_moves = qft && h0->world == 1 && !no_moves && ensure_scratch(h0) == QSIM_OK;
     if (block_moves && G > 2 && amax == 8 && !gc && !even) {
         // measured per-pass efficiency (tools/probe_blocks.sh): 8- and 6-wire
         // passes stream best, 7 a little worse, <= 5 and a last block of 8
