@@ -16,3 +16,5 @@ cap ops_pass k_ops_pass 0 python tools/run_cfg.py 4m
 cap ops_pp k_ops_pp 0 python tools/run_cfg.py 4m
 cap qft_gen k_qft_gen 0 python tools/run_cfg.py 3n
 cap perm_ring k_perm_ring 0 python tools/run_cfg.py 3
+cap grover_regs k_grover_regs 0 python tools/run_cfg.py 1
+cap probs_warp k_probs_warp 0 python tools/run_cfg.py 3

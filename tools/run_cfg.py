@@ -1,4 +1,4 @@
-"""Run one config once (for ncu captures): python tools/run_cfg.py 3|3n|4|4m|4s"""
+"""Run one config once (for ncu captures): python tools/run_cfg.py 1|3|3n|4|4m|4s"""
 import os
 import sys
 
@@ -7,7 +7,10 @@ from paper_quant_ph_0201042_b200 import qsim as Q  # noqa: E402
 from paper_quant_ph_0201042_b200 import workloads as W  # noqa: E402
 
 w = sys.argv[1]
-if w == "3":
+if w == "1":
+    h = Q.qsim_create(20)
+    W.run_cfg1(h, 20, 2)
+elif w == "3":
     h = Q.qsim_create(30)
     W.run_cfg3(h, 20, 10, 1007, 4, 0.0)
 elif w == "3n":
