@@ -227,15 +227,18 @@ __global__ void __launch_bounds__(kRegsThreads, 1) k_grover_regs(double2 *__rest
         acc = warp_sum2(acc);
         ak = warp_sum2(ak);
         const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+        __shared__ double2 sak[32];
         if (l == 0) {
             sh[w] = acc;
+            sak[w] = ak;
         }
-        __shared__ double2 sak[32];
-        if (l == 0) sak[w] = ak;
         __syncthreads();
-        const unsigned p = (unsigned)(it + 1) & 1u;
         if (w == 0) {
-            // CTA partial: lanes < #warps hold the warp sums, fixed shuffle tree
+            // warp 0 does the rest: CTA partial (fixed shuffle tree), publish,
+            // arrive on the counter and wait, then gather every CTA's slot
+            // (lane l: slots l, l+32, ... in that order, then the fixed xor
+            // tree) -- one CTA barrier per exchange besides the partials'
+            const unsigned p = (unsigned)(it + 1) & 1u;
             const int nw = (int)(blockDim.x >> 5);
             double2 t = l < nw ? sh[l] : make_double2(0.0, 0.0);
             double2 a = l < nw ? sak[l] : make_double2(0.0, 0.0);
@@ -243,8 +246,6 @@ __global__ void __launch_bounds__(kRegsThreads, 1) k_grover_regs(double2 *__rest
             a = warp_sum2(a);
             if (l == 0) {
                 slots[(size_t)p * nb + blockIdx.x] = make_double4(t.x, t.y, a.x, a.y);
-                // arrive (release: the slot is visible before the count), then
-                // wait until every CTA of this round has arrived
                 const unsigned target = nb * (unsigned)(it + 2);
                 asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(tags) : "memory");
                 unsigned got;
@@ -252,29 +253,19 @@ __global__ void __launch_bounds__(kRegsThreads, 1) k_grover_regs(double2 *__rest
                     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(got) : "l"(tags) : "memory");
                 } while (got < target);
             }
-        }
-        __syncthreads();
-        // gather: thread b < nb reads slot b (one round trip), fixed-order trees
-        double4 q = make_double4(0.0, 0.0, 0.0, 0.0);
-        if (threadIdx.x < nb) {
-            const double2 *sp = reinterpret_cast<const double2 *>(slots + (size_t)p * nb + threadIdx.x);
-            const double2 q0 = __ldcg(sp), q1 = __ldcg(sp + 1);
-            q = make_double4(q0.x, q0.y, q1.x, q1.y);
-        }
-        const double2 s1 = warp_sum2(make_double2(q.x, q.y));
-        const double2 s2 = warp_sum2(make_double2(q.z, q.w));
-        if (l == 0) {
-            sh[w] = s1;
-            sak[w] = s2;
-        }
-        __syncthreads();
-        if (w == 0) {
-            const int ng = (int)((nb + 31) >> 5);
-            double2 t = l < ng ? sh[l] : make_double2(0.0, 0.0);
-            double2 a = l < ng ? sak[l] : make_double2(0.0, 0.0);
-            t = warp_sum2(t);
-            a = warp_sum2(a);
-            if (l == 0) s_tot = make_double4(t.x, t.y, a.x, a.y);
+            __syncwarp();
+            double4 q = make_double4(0.0, 0.0, 0.0, 0.0);
+            for (unsigned b = l; b < nb; b += 32) {
+                const double2 *sp = reinterpret_cast<const double2 *>(slots + (size_t)p * nb + b);
+                const double2 q0 = __ldcg(sp), q1 = __ldcg(sp + 1);
+                q.x += q0.x;
+                q.y += q0.y;
+                q.z += q1.x;
+                q.w += q1.y;
+            }
+            const double2 s1 = warp_sum2(make_double2(q.x, q.y));
+            const double2 s2 = warp_sum2(make_double2(q.z, q.w));
+            if (l == 0) s_tot = make_double4(s1.x, s1.y, s2.x, s2.y);
         }
         __syncthreads();
     };
