@@ -116,7 +116,10 @@ __global__ void __launch_bounds__(kThreads) k_grover_iter(double2 *__restrict__ 
 namespace cg = cooperative_groups;
 
 constexpr int kPersistThreads = 512;
-constexpr int kRegsThreads = 256;   // k_grover_regs: fewer, fatter threads (cheaper CTA barriers / trees)
+constexpr int kRegsThreads = 256;
+#ifndef GROVER_BACKOFF_NS
+#define GROVER_BACKOFF_NS 32
+#endif   // k_grover_regs: fewer, fatter threads (cheaper CTA barriers / trees)
 
 __global__ void __launch_bounds__(kPersistThreads) k_grover_persist(double2 *__restrict__ psi, uint64_t N, uint64_t chunk,
                                                                     uint64_t k, int iters, double *__restrict__ trace,
@@ -249,9 +252,11 @@ __global__ void __launch_bounds__(kRegsThreads, 1) k_grover_regs(double2 *__rest
                 const unsigned target = nb * (unsigned)(it + 2);
                 asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(tags) : "memory");
                 unsigned got;
-                do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(got) : "l"(tags) : "memory");
+                while (got < target) {
+                    __nanosleep(GROVER_BACKOFF_NS);
                     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(got) : "l"(tags) : "memory");
-                } while (got < target);
+                }
             }
             __syncwarp();
             double4 q = make_double4(0.0, 0.0, 0.0, 0.0);
