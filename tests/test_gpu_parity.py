@@ -347,6 +347,18 @@ def test_table_permutation_bit_exact(reg):
     assert np.array_equal(get(h, n), ref)
 
 
+@pytest.mark.parametrize("n,lo,m", [(24, 4, 16), (24, 0, 16), (24, 8, 16), (22, 2, 14), (26, 6, 18)])
+def test_marginals_many_bins_match_oracle(reg, n, lo, m):
+    """Marginals over many small bins (the warp-per-bin kernel), with the
+    remaining positions above, below and on both sides of the range."""
+    psi = rand_state(n, 100 + lo + m)
+    h = reg(n, psi)
+    got = Q.qsim_probs(h, lo, m)
+    ref = O.probs(psi, lo, m)
+    assert np.max(np.abs(got - ref)) < 1e-15
+    assert abs(got.sum() - 1) < 1e-12
+
+
 def test_norm_probs_measure(reg):
     n = 16
     psi = rand_state(n, 21) * 0.9
