@@ -21,7 +21,8 @@
  *     calls that return data to the host (norm, probs, get_state, measure,
  *     sync, inject_errors' event list) synchronise that stream.
  *   - A handle is not thread-safe: one mutator at a time.
- *   - Multi-GPU: one process per GPU (qsim_create_dist).  The state is sharded
+ *   - Multi-GPU: qsim_create(n, ngpus) / qsim_create_group (one process
+ *     drives every GPU) or one process per GPU (qsim_create_dist).  The state is sharded
  *     on its top log2(world) physical bits; the library tracks a logical ->
  *     physical qubit map internally, exchanges shards with NCCL send/recv when
  *     a gate needs a global qubit local, and restores the canonical layout
@@ -52,7 +53,8 @@ enum {
     QSIM_ENOTBIJ = -5,    /* permutation is not a bijection */
     QSIM_ESTATE = -6,     /* handle poisoned by an earlier asynchronous error */
     QSIM_ENCCL = -7,      /* NCCL error (handle poisoned) */
-    QSIM_ENODEV = -8      /* no CUDA device / not an sm_100 device */
+    QSIM_ENODEV = -8,     /* no CUDA device / not an sm_100 device */
+    QSIM_ENONUNITARY = -9 /* strict mode (qsim_set_strict): the matrix is not unitary */
 };
 
 /* Angle-form gate kinds (§3.2; R12-R14).
@@ -72,9 +74,15 @@ enum {
 
 /* ---------------------------------------------------------------- lifecycle */
 
-/* Allocate an n-qubit register (2^(n+4) bytes of HBM) on the
- * current CUDA device, initialised to |0...0>.  ngpus must be 1 (use
- * qsim_create_dist for multi-GPU).  Errors: QSIM_ERANGE if n < 1 or n > 40;
+/* Allocate an n-qubit register (2^(n+4) bytes of HBM),
+ * initialised to |0...0>.  ngpus = 1: on the current CUDA device.  ngpus > 1
+ * (a power of two): sharded over CUDA devices 0..ngpus-1 on its top
+ * log2(ngpus) qubits, all driven by this process -- the same handle as
+ * qsim_create_group(n, ngpus, {0, 1, ..., ngpus-1}); when fewer devices are
+ * visible, rank r goes to device r mod (device count).  The paper's pairing
+ * of rows R_j / R_{2^P + j} across processors (§2.2.1) is
+ * what the shard exchanges implement.  Errors: QSIM_ERANGE if n < 1, n > 40
+ * or 2^n < 2 ngpus; QSIM_EINVAL if ngpus is not a power of two in [1, 64];
  * QSIM_ENOMEM (message names the byte count); QSIM_ENODEV.  *out receives
  * the handle (NULL on error; qsim_last_error(NULL) then has the message). */
 int qsim_create(int n, int ngpus, qsim_t **out);
@@ -117,6 +125,12 @@ int qsim_sync(qsim_t *h);
 /* The cudaStream_t (as void*) every kernel of h is launched on, so callers
  * can record CUDA events on it (plumbing for timing; do not destroy it). */
 void *qsim_get_stream(qsim_t *h);
+
+/* Strict mode (default off): qsim_apply_1q / qsim_apply_ctrl (and matrix
+ * entries of qsim_apply_gates) return QSIM_ENONUNITARY, with no effect, when
+ * max |(U U^dagger - I)_rc| > 1e-12 -- the paper's gates are unitary
+ * (§2.2.1).  Off, any 2x2 matrix is applied as given. */
+int qsim_set_strict(qsim_t *h, int enable);
 
 /* Gate fusion (default on for shards of >= 2^9 amplitudes): single-qubit
  * and controlled gates are queued and applied as fused tile passes (one HBM
@@ -238,11 +252,23 @@ int qsim_aqft(qsim_t *h, int lo, int m, int b, int inverse);
  * idx >= 2^n. */
 int qsim_phase_flip(qsim_t *h, uint64_t idx);
 
+/* Diffusion D = -H_m V_{f0} H_m = 2|s><s| - I on the sub-register [lo, lo+m)
+ * (§5.3; |s> = H_m|0>, the sign kept literally): for
+ * every value of the other qubits, alpha_y <- 2 mean_y(alpha) - alpha_y.  The
+ * whole register (lo = 0, m = n) runs in the mean form (one read pass for the
+ * fixed-order sum, one update pass; shards summed on the host in rank order);
+ * a sub-register runs the literal H_m, diagonal 2|0><0| - I, H_m as fused
+ * passes.  Asynchronous except for the whole-register sum.  QSIM_ERANGE if
+ * the range leaves [0, n) or m < 1. */
+int qsim_diffusion(qsim_t *h, int lo, int m);
+
 /* Grover's search on the whole register (§5.3): `iters`
  * G-iterations -H_n V_{f0} H_n V_{fk} with f_k = delta_{x, mark}, applied in
  * the equivalent form alpha_k <- -alpha_k; alpha <- 2 mean(alpha) - alpha.
  * trace (host, iters doubles, may be NULL) receives |alpha_mark|^2 after each
- * iteration.  Synchronising when trace != NULL. */
+ * iteration.  One GPU: all iterations in one cooperative kernel.  Sharded
+ * handles: qsim_phase_flip + qsim_diffusion(0, n) per iteration.
+ * Synchronising when trace != NULL. */
 int qsim_grover(qsim_t *h, uint64_t mark, int iters, double *trace);
 
 /* ---------------------------------------------------------------- permutations (§2.3.3) */
@@ -451,6 +477,28 @@ typedef struct {
  * its error code is returned, *done (if not NULL) = the number applied before
  * it. */
 int qsim_apply_gates(qsim_t *h, const qsim_gate_t *gates, int count, int *done);
+
+/* ---------------------------------------------------------------- host-only exchange planner */
+
+/* The planner behind every shard exchange (no device work; exposed for the
+ * multi-process CPU tests).  The paper's large-subblock rule (PAPER.md:264-289,
+ * §2.2.1: rows R_j and R_{2^P + j} must meet on one processor) becomes a list
+ * of steps on the physical layout of an n-qubit state over `world` ranks
+ * (world a power of two), written as int triples (kind, a, b) into
+ * steps[0 .. 3*cap):
+ *   kind 0 LSWAP (a, b): swap local positions a and b;
+ *   kind 1 XCHG  (g, -): swap rank-bit position g with the top local position
+ *                        (rank r trades half its shard with rank r ^ 2^(g - nl));
+ *   kind 2 A2A   (k, -): swap the k rank-bit positions with the top k local
+ *                        positions in one all-to-all.
+ * pos_io (n ints: logical qubit -> physical position, caller-owned) is
+ * updated as the steps move the data.  qsim_plan_make_local plans for the
+ * nneed logical qubits in need (caller-owned) to become local;
+ * qsim_plan_canonical_globals for the rank bits to hold qubits 0..log2(world)-1
+ * again.  Return the number of steps (only the first cap are written), or
+ * QSIM_EINVAL / QSIM_ERANGE. */
+int qsim_plan_make_local(int n, int world, int *pos_io, const int *need, int nneed, int *steps, int cap);
+int qsim_plan_canonical_globals(int n, int world, int *pos_io, int *steps, int cap);
 
 #ifdef __cplusplus
 }

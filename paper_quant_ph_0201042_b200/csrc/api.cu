@@ -326,6 +326,28 @@ int check_qubit(Handle *h, int q)
     return QSIM_OK;
 }
 
+// strict mode (qsim_set_strict): max |(U U^dagger - I)_rc| <= 1e-12, the
+// paper's gates being unitary
+int check_unitary(Handle *h, const double2 U[4])
+{
+    if (!h->strict) return QSIM_OK;
+    double e = 0.0;
+    for (int r = 0; r < 2; ++r)
+        for (int c = 0; c < 2; ++c) {
+            // sum_k U[r][k] conj(U[c][k])
+            double re = 0.0, im = 0.0;
+            for (int k = 0; k < 2; ++k) {
+                const double2 a = U[2 * r + k], b = U[2 * c + k];
+                re += a.x * b.x + a.y * b.y;
+                im += a.y * b.x - a.x * b.y;
+            }
+            if (r == c) re -= 1.0;
+            e = std::max(e, std::hypot(re, im));
+        }
+    if (!(e <= 1e-12)) return fail(h, QSIM_ENONUNITARY, "matrix is not unitary: max |U U^dagger - I| = " + std::to_string(e));
+    return QSIM_OK;
+}
+
 int check_ctrl(Handle *h, uint64_t cmask, uint64_t cvals, int q)
 {
     if (h->n < 64 && (cmask >> h->n)) return fail(h, QSIM_ERANGE, "control mask has qubits >= n");
@@ -550,8 +572,9 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
             if (wp[w] < nl) wp[w] = perm[wp[w]];
         a0 += a;
     }
-    if (qft && !block_moves) {
-        // closing swaps as a relabelling of the logical -> physical map
+    if (qft && !block_moves && !dry) {
+        // closing swaps as a relabelling of the logical -> physical map (not in a
+        // dry run: fused_qft_gen calls it once or twice before the real pass)
         for (Handle *h : R)
             for (int t = 0; t < m / 2; ++t) std::swap(h->pos[lo + t], h->pos[lo + m - 1 - t]);
     }
@@ -688,12 +711,20 @@ static int create_common(int n, int world, int rank, int device, qsim_t **out)
 int qsim_create(int n, int ngpus, qsim_t **out)
 {
     if (!out) return QSIM_EINVAL;
-    if (ngpus != 1) {
-        *out = nullptr;
-        return fail(nullptr, QSIM_EINVAL,
-                    "qsim_create drives one GPU; use qsim_create_dist (one process per GPU) or qsim_create_group");
+    *out = nullptr;
+    if (ngpus < 1 || ngpus > 64 || (ngpus & (ngpus - 1)))
+        return fail(nullptr, QSIM_EINVAL, "ngpus must be a power of two in [1, 64]");
+    if (ngpus == 1) return create_common(n, 1, 0, -1, out);
+    // several GPUs driven by this process: the rank-group path (one shard per
+    // device, peer copies over NVLink), rank r on device r mod (device count)
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(nullptr, QSIM_ENODEV, "no CUDA device (libqsim has no CPU path)");
     }
-    return create_common(n, 1, 0, -1, out);
+    std::vector<int> devs(ngpus);
+    for (int r = 0; r < ngpus; ++r) devs[r] = r % ndev;
+    return qsim_create_group(n, ngpus, devs.data(), out);
 }
 
 int qsim_create_dist(int n, int world, int rank, int device, const void *nccl_id, qsim_t **out)
@@ -791,6 +822,7 @@ void qsim_destroy(qsim_t *h)
     if (h->scratch) cudaFree(h->scratch);
     if (h->d_red) cudaFree(h->d_red);
     if (h->d_probs) cudaFree(h->d_probs);
+    if (h->d_sum2) cudaFree(h->d_sum2);
     if (h->d_tabs) cudaFree(h->d_tabs);
     if (h->h_red) cudaFreeHost(h->h_red);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
@@ -978,8 +1010,16 @@ int qsim_apply_1q(qsim_t *h, int q, const qsim_c128 U[4])
     if (int rc = check_qubit(h, q)) return rc;
     double2 M[4];
     for (int k = 0; k < 4; ++k) M[k] = make_double2(U[k].re, U[k].im);
+    if (int rc = check_unitary(h, M)) return rc;
     const Ranks R = ranks_of(h);
     return lift(h, R, apply_gate(R, 0, 0, q, M));
+}
+
+int qsim_set_strict(qsim_t *h, int enable)
+{
+    QS_CHECK_HANDLE(h);
+    h->strict = enable ? 1 : 0;
+    return QSIM_OK;
 }
 
 int qsim_apply_ctrl(qsim_t *h, uint64_t cmask, uint64_t cvals, int q, const qsim_c128 U[4])
@@ -989,6 +1029,7 @@ int qsim_apply_ctrl(qsim_t *h, uint64_t cmask, uint64_t cvals, int q, const qsim
     if (int rc = check_ctrl(h, cmask, cvals, q)) return rc;
     double2 M[4];
     for (int k = 0; k < 4; ++k) M[k] = make_double2(U[k].re, U[k].im);
+    if (int rc = check_unitary(h, M)) return rc;
     const Ranks R = ranks_of(h);
     return lift(h, R, apply_gate(R, cmask, cvals, q, M));
 }
@@ -1181,7 +1222,8 @@ static int fused_qft_gen(qsim_t *h, const Ranks &R, int lo, int m, int band, int
     if (off || h->world != 1 || R.size() != 1 || h->batch_b > 0 || !h->fuse || h->nl < 9 || m > h->nl || m < 4 ||
         m > kGenEarly)
         return 1;
-    // geometry first (no state change besides the canonical relabel fused_range does anyway)
+    // geometry first: a dry run changes nothing but the canonicalisation / flush
+    // fused_range does anyway (its closing-swap relabel is skipped when dry)
     GenCircuit gc;
     gc.m = m;
     bool even = false;
@@ -1312,14 +1354,81 @@ int qsim_phase_flip(qsim_t *h, uint64_t idx)
     return QSIM_OK;
 }
 
+// D = 2|s><s| - I on the whole register in the mean form alpha <- 2 mean -
+// alpha: one read-only pass for the sum (fixed tree per shard, shards summed
+// on the host in rank order), one update pass.  The sum and the update are
+// layout-independent, so no exchange or canonicalisation is needed.
+static int diffusion_mean(qsim_t *h, const Ranks &R)
+{
+    std::vector<std::vector<double>> parts(R.size(), std::vector<double>(2, 0.0));
+    for (size_t i = 0; i < R.size(); ++i) {
+        Handle *m = R[i];
+        cudaSetDevice(m->device);
+        if (int rc = flush_queue(m)) return rc;
+        if (!m->d_sum2 && check_cuda(m, cudaMalloc(&m->d_sum2, 2 * sizeof(double)), "diffusion buffer")) return QSIM_ECUDA;
+        ensure_hred(m, 2);
+        launch_amp_sum(m, m->d_sum2);
+        if (int rc = after_launch(m, "diffusion sum")) return rc;
+        if (int rc = check_cuda(m, cudaMemcpyAsync(m->h_red, m->d_sum2, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                                                   m->stream), "diffusion"))
+            return rc;
+    }
+    for (size_t i = 0; i < R.size(); ++i) {
+        Handle *m = R[i];
+        cudaSetDevice(m->device);
+        if (int rc = check_cuda(m, cudaStreamSynchronize(m->stream), "diffusion")) return rc;
+        parts[i][0] = m->h_red[0];
+        parts[i][1] = m->h_red[1];
+    }
+    double S[2];
+    if (int rc = dist_sum_host(R, parts, S, 2)) return rc;
+    const double inv = std::ldexp(1.0, -h->n);
+    const double2 c = make_double2(2.0 * S[0] * inv, 2.0 * S[1] * inv);
+    for (Handle *m : R) {
+        cudaSetDevice(m->device);
+        launch_reflect(m, c);
+        if (int rc = after_launch(m, "diffusion")) return rc;
+    }
+    return QSIM_OK;
+}
+
+int qsim_diffusion(qsim_t *h, int lo, int m)
+{
+    QS_CHECK_HANDLE(h);
+    if (lo < 0 || m < 1 || lo + m > h->n) return fail(h, QSIM_ERANGE, "range outside [0, n) or m < 1");
+    const Ranks R = ranks_of(h);
+    if (lo == 0 && m == h->n && !h->batch_b) return lift(h, R, diffusion_mean(h, R));
+    // a sub-register: the paper's literal -H_m V_{f0} H_m, with
+    // -V_{f0} = 2|0><0| - I as two diagonal gates: a global -1 and a flip of
+    // the range value 0 (controls on lo..lo+m-2 at 0, target lo+m-1)
+    if (int rc = qsim_hadamard(h, lo, m)) return rc;
+    const double2 minus[4] = {make_double2(-1, 0), make_double2(0, 0), make_double2(0, 0), make_double2(-1, 0)};
+    const double2 flip0[4] = {make_double2(-1, 0), make_double2(0, 0), make_double2(0, 0), make_double2(1, 0)};
+    uint64_t cm = 0;
+    for (int q = lo; q < lo + m - 1; ++q) cm |= 1ull << q;
+    if (int rc = lift(h, R, apply_gate(R, 0, 0, lo + m - 1, minus))) return rc;
+    if (int rc = lift(h, R, apply_gate(R, cm, 0, lo + m - 1, flip0))) return rc;
+    return qsim_hadamard(h, lo, m);
+}
+
 int qsim_grover(qsim_t *h, uint64_t mark, int iters, double *trace)
 {
     QS_CHECK_HANDLE(h);
     if (h->n < 64 && mark >> h->n) return fail(h, QSIM_ERANGE, "mark >= 2^n");
     if (iters < 0) return fail(h, QSIM_EINVAL, "iters < 0");
-    if (h->world > 1) return fail(h, QSIM_EINVAL, "qsim_grover runs on a single-GPU handle");
     if (h->batch_b) return fail(h, QSIM_EINVAL, "qsim_grover on a batched handle (use gates)");
     const Ranks R = ranks_of(h);
+    if (h->world > 1) {
+        // sharded: per iteration the phase flip on the owner rank, the mean-form
+        // diffusion with the fixed-order cross-rank sum, and the trace read
+        for (int t = 0; t < iters; ++t) {
+            if (int rc = qsim_phase_flip(h, mark)) return rc;
+            if (int rc = lift(h, R, diffusion_mean(h, R))) return rc;
+            if (trace)
+                if (int rc = qsim_prob_index(h, mark, trace + t)) return rc;
+        }
+        return QSIM_OK;
+    }
     if (int rc = dist_canonicalize(R)) return rc;
     double *d_trace = nullptr;
     if (trace && iters > 0) {

@@ -249,11 +249,13 @@ __global__ void __launch_bounds__(kRegsThreads, 1) k_grover_regs(double2 *__rest
             a = warp_sum2(a);
             if (l == 0) {
                 slots[(size_t)p * nb + blockIdx.x] = make_double4(t.x, t.y, a.x, a.y);
+                // monotonic counter compared wrap-safe: it wraps after ~2^32 / nb
+                // iterations, but no CTA runs more than one exchange ahead
                 const unsigned target = nb * (unsigned)(it + 2);
                 asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(tags) : "memory");
                 unsigned got;
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(got) : "l"(tags) : "memory");
-                while (got < target) {
+                while ((int)(got - target) < 0) {
                     __nanosleep(GROVER_BACKOFF_NS);
                     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(got) : "l"(tags) : "memory");
                 }

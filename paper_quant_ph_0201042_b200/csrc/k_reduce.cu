@@ -162,6 +162,38 @@ __global__ void __launch_bounds__(kThreads) k_chunk_inner(const double2 *__restr
     }
 }
 
+// Sum of the amplitudes themselves over chunks (the mean of Grover's diffusion
+// 2|s><s| - I): block c writes re to out_re[c], im to
+// out_im[c] (same fixed tree as the norm).
+__global__ void __launch_bounds__(kThreads) k_chunk_sum(const double2 *__restrict__ a, uint64_t chunk,
+                                                        double *__restrict__ out_re, double *__restrict__ out_im)
+{
+    __shared__ double sh[32];
+    const uint64_t base = (uint64_t)blockIdx.x * chunk;
+    double re = 0.0, im = 0.0;
+    for (uint64_t i = threadIdx.x; i < chunk; i += blockDim.x) {
+        const double2 x = a[base + i];
+        re += x.x;
+        im += x.y;
+    }
+    const double sr = block_sum(re, sh);
+    const double si = block_sum(im, sh);
+    if (threadIdx.x == 0) {
+        out_re[blockIdx.x] = sr;
+        out_im[blockIdx.x] = si;
+    }
+}
+
+// alpha_i <- c - alpha_i for every amplitude (c = 2 mean: 2|s><s| - I).
+__global__ void __launch_bounds__(kThreads) k_reflect(double2 *__restrict__ psi, uint64_t count, double2 c)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+        const double2 v = psi[i];
+        psi[i] = make_double2(c.x - v.x, c.y - v.y);
+    }
+}
+
 // Projection of a measured sub-register (R31): amplitudes whose masked bits
 // equal val are scaled by s, every other one (all of them if zero_all) is 0.
 __global__ void __launch_bounds__(kThreads) k_collapse(double2 *__restrict__ psi, uint64_t count, uint64_t mask,
@@ -262,6 +294,31 @@ void launch_inner(Handle *h, const double2 *a, const double2 *b, double *d_out)
     prof_end(h, "k_chunk_inner", h->local_dim() * 32);
     tree_sum_ws(h, re, nb, tmp, d_out);
     tree_sum_ws(h, im, nb, tmp, d_out + 1);
+}
+
+void launch_amp_sum(Handle *h, double *d_out)
+{
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
+    const int bb = h->nl < 12 ? h->nl : 12;
+    const uint64_t nb = h->local_dim() >> bb;
+    ensure_red(h, 2 * nb + (nb >> 9) + 16);
+    double *re = h->d_red + 8, *im = re + nb, *tmp = im + nb;
+    prof_begin(h);
+    k_chunk_sum<<<(unsigned)nb, kThreads, 0, h->stream>>>(h->psi, 1ull << bb, re, im);
+    prof_end(h, "k_chunk_sum", h->local_dim() * 16);
+    tree_sum_ws(h, re, nb, tmp, d_out);
+    tree_sum_ws(h, im, nb, tmp, d_out + 1);
+}
+
+void launch_reflect(Handle *h, double2 c)
+{
+    cudaSetDevice(h->device);   // members of a rank group may live on different devices
+    const uint64_t count = h->local_dim();
+    const uint64_t want = (count + kThreads - 1) / kThreads;
+    const uint64_t cap = (uint64_t)h->num_sms * 8;
+    prof_begin(h);
+    k_reflect<<<(unsigned)(want < cap ? want : cap), kThreads, 0, h->stream>>>(h->psi, count, c);
+    prof_end(h, "k_reflect", count * 32);
 }
 
 void launch_collapse(Handle *h, uint64_t mask, uint64_t val, double s, int zero_all)

@@ -58,6 +58,11 @@ void launch_norm(Handle *h, double *d_out);
 // (re, im) on the device; fixed tree order.  d_out must not be in the
 // reduction workspace.
 void launch_inner(Handle *h, const double2 *a, const double2 *b, double *d_out);
+// sum of the amplitudes over one shard -> d_out[0..1] (re, im) on the device;
+// fixed tree order.  d_out must not be in the reduction workspace.
+void launch_amp_sum(Handle *h, double *d_out);
+// psi[i] <- c - psi[i] (Grover's diffusion with c = 2 mean).
+void launch_reflect(Handle *h, double2 c);
 // psi[i] *= s where (i & mask) == val, 0 elsewhere (everywhere if zero_all).
 void launch_collapse(Handle *h, uint64_t mask, uint64_t val, double s, int zero_all);
 // Partial sums of |a|^2 over consecutive blocks of 2^blk_bits amplitudes.
@@ -261,6 +266,8 @@ struct Handle {
     size_t probs_cap = 0;
     double *h_red = nullptr;     // pinned
     size_t hred_cap = 0;
+    double *d_sum2 = nullptr;    // 2 doubles: amplitude-sum result (diffusion), outside d_red
+    int strict = 0;              // qsim_set_strict: reject non-unitary matrices (QSIM_ENONUNITARY)
     // angle noise (R15)
     uint64_t noise_seed = 0;
     double sigma = 0.0;

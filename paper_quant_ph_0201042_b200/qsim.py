@@ -26,6 +26,7 @@ lib = C.CDLL(LIB_PATH)
 
 QSIM_OK, QSIM_EINVAL, QSIM_ERANGE, QSIM_ENOMEM = 0, -1, -2, -3
 QSIM_ECUDA, QSIM_ENOTBIJ, QSIM_ESTATE, QSIM_ENCCL, QSIM_ENODEV = -4, -5, -6, -7, -8
+QSIM_ENONUNITARY = -9
 QSIM_GATE_RP, QSIM_GATE_P1, QSIM_GATE_HAAR = 0, 1, 2
 QSIM_PERM_TABLE, QSIM_PERM_MODMUL, QSIM_PERM_MODEXP = 0, 1, 2
 QSIM_TAG_GATE, QSIM_TAG_HAAR, QSIM_TAG_PAIR, QSIM_TAG_OPNOISE = 1, 2, 3, 4
@@ -33,7 +34,7 @@ QSIM_TAG_MARK, QSIM_TAG_BASE, QSIM_TAG_GAUSS, QSIM_TAG_PAULI, QSIM_TAG_MEASURE, 
 
 _ERRNAMES = {
     -1: "QSIM_EINVAL", -2: "QSIM_ERANGE", -3: "QSIM_ENOMEM", -4: "QSIM_ECUDA",
-    -5: "QSIM_ENOTBIJ", -6: "QSIM_ESTATE", -7: "QSIM_ENCCL", -8: "QSIM_ENODEV",
+    -5: "QSIM_ENOTBIJ", -6: "QSIM_ESTATE", -7: "QSIM_ENCCL", -8: "QSIM_ENODEV", -9: "QSIM_ENONUNITARY",
 }
 
 
@@ -107,6 +108,8 @@ _sig("qsim_batch_set_state", _i32, _H, _p)
 _sig("qsim_batch_overlap", _i32, _H, _p, _p)
 _sig("qsim_phase_flip", _i32, _H, _u64)
 _sig("qsim_grover", _i32, _H, _u64, _i32, _p)
+_sig("qsim_diffusion", _i32, _H, _i32, _i32)
+_sig("qsim_set_strict", _i32, _H, _i32)
 _sig("qsim_apply_perm", _i32, _H, C.POINTER(qsim_perm_t))
 _sig("qsim_inject_errors", _i32, _H, _u64, C.POINTER(qsim_noise_t), _p, _i32, C.POINTER(_i32))
 _sig("qsim_norm", _i32, _H, C.POINTER(_f64))
@@ -332,6 +335,14 @@ def qsim_grover(h, mark: int, iters: int, trace: bool = True):
     out = np.zeros(max(iters, 1), np.float64) if trace else None
     _chk(h, lib.qsim_grover(h, mark, iters, out.ctypes.data if trace else None))
     return out[:iters] if trace else None
+
+
+def qsim_diffusion(h, lo: int, m: int) -> None:
+    _chk(h, lib.qsim_diffusion(h, lo, m))
+
+
+def qsim_set_strict(h, enable: bool) -> None:
+    _chk(h, lib.qsim_set_strict(h, int(bool(enable))))
 
 
 def qsim_apply_perm(h, kind: int, lo: int, m: int, *, elo: int = 0, em: int = 0, ctrl_mask: int = 0,

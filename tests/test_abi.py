@@ -25,6 +25,27 @@ def test_header_declares_the_north_star_calls():
         assert must in names
 
 
+def test_header_declares_the_round2_boundary_calls():
+    """multi-device qsim_create, qsim_diffusion, the strict
+    unitarity mode and the host planner are part of the header."""
+    names = declared_functions()
+    for must in ["qsim_diffusion", "qsim_set_strict", "qsim_grover", "qsim_phase_flip", "qsim_measure",
+                 "qsim_plan_make_local", "qsim_plan_canonical_globals", "qsim_create_group", "qsim_create_dist"]:
+        assert must in names
+    src = open(HEADER).read()
+    assert "QSIM_ENONUNITARY" in src
+
+
+def test_library_exports_nothing_undeclared():
+    """Every exported qsim_* symbol is declared in include/qsim.h."""
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True, text=True).stdout
+    exported = {ln.split()[-1] for ln in out.splitlines() if ln.split() and ln.split()[-1].startswith("qsim_")
+                and " T " in ln}
+    assert exported, out[:200]
+    assert exported <= set(declared_functions()), sorted(exported - set(declared_functions()))
+
+
 def test_library_exports_every_declared_symbol():
     assert os.path.exists(LIB), "build libqsim.so first (__graft_entry__.build())"
     lib = ctypes.CDLL(LIB)

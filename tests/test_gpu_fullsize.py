@@ -1,0 +1,134 @@
+"""Element-wise parity at the benchmarked sizes.
+
+* configs[2] at n = 28: the whole 2^28-amplitude vector through the exact pass
+  plan bench.py times, against the oracle's gate-by-gate QFT circuit
+   on the same seeded Gaussian input (~25 s of oracle time);
+* configs[4] at n = 24 (20 layers, sigma = 1e-3, p = 1e-4 and a forcing
+  p = 0.02): every amplitude and the event list, with the gate-list kernels
+  k_ops_pp / k_ops_pass asserted from the library's own launch record;
+* configs[3] with sigma = 1e-3 through the fused k_qft_gen passes: ne = 20
+  exponent qubits (the full register, so the noisy H_20 and inverse QFT run
+  the full-size pass plans) with a 6-qubit work register (N = 57) at n = 26,
+  and the full n = 30 configuration when the host has the RAM for it.
+
+Tolerances: BASELINE.json north_star (max |d alpha| <= 1e-10, |norm - 1| <=
+1e-12, bit-exact event lists); marginals to 1e-12.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+Q = pytest.importorskip("paper_quant_ph_0201042_b200.qsim")
+from paper_quant_ph_0201042_b200 import workloads as W  # noqa: E402
+
+TOL = 1e-10
+
+
+def host_ram_gib():
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) / 2**20
+    except OSError:
+        pass
+    return 0.0
+
+
+def kernels_of(h):
+    prof = Q.qsim_profile_json(h)
+    prof.pop("_launches", None)
+    return {k: v["launches"] for k, v in prof.items()}
+
+
+def test_cfg2_full_size_whole_vector():
+    n = 28
+    h = Q.qsim_create(n)
+    try:
+        Q.qsim_init_gaussian(h, 3)
+        Q.qsim_profile(h, True)
+        Q.qsim_qft(h, 0, n, False)            # the step bench.py times
+        ks = kernels_of(h)
+        Q.qsim_profile(h, False)
+        got = Q.qsim_get_state(h, 0, 1 << n)
+        norm = Q.qsim_norm(h)
+    finally:
+        Q.qsim_destroy(h)
+    print("cfg2 n=28 kernels:", ks)
+    # every pass of the bench plan is a fused QFT kernel launch
+    assert sum(v for k, v in ks.items() if k.startswith("k_qft")) >= 3
+    ref = O.cfg2(n=n, seed=3)
+    err = float(np.max(np.abs(got - ref)))
+    l2 = float(np.linalg.norm(got - ref))
+    print(f"cfg2 n=28: max |d alpha| = {err:.3e}, L2 = {l2:.3e}")
+    assert err < TOL
+    assert abs(norm - 1) < 1e-12
+
+
+@pytest.mark.parametrize("p", [1e-4, 0.02])
+def test_cfg4_n24_whole_vector(p):
+    n = 24
+    h = Q.qsim_create(n)
+    try:
+        Q.qsim_profile(h, True)
+        ev = W.run_cfg4(h, n=n, layers=20, seed=5, sigma=1e-3, p=p)
+        Q.qsim_sync(h)
+        ks = kernels_of(h)
+        Q.qsim_profile(h, False)
+        got = Q.qsim_get_state(h, 0, 1 << n)
+        norm = Q.qsim_norm(h)
+    finally:
+        Q.qsim_destroy(h)
+    print("cfg4 n=24 kernels:", ks)
+    assert ks.get("k_ops_pp", 0) > 0, ks
+    ref, rev = O.cfg4(n=n, layers=20, seed=5, sigma=1e-3, p=p)
+    assert [tuple(e) for e in ev] == [tuple(e) for e in rev]
+    if p > 1e-3:
+        assert len(rev) > 10
+    err = float(np.max(np.abs(got - ref)))
+    print(f"cfg4 n=24 p={p}: max |d alpha| = {err:.3e}, events {len(rev)}")
+    assert err < TOL
+    assert abs(norm - 1) < 1e-12
+
+
+def test_cfg3_noisy_full_exponent_register():
+    ne, nw, N = 20, 6, 57
+    a = O.shor_base(4, N)
+    h = Q.qsim_create(ne + nw)
+    try:
+        Q.qsim_profile(h, True)
+        P = W.run_cfg3(h, ne=ne, nw=nw, N=N, seed=4, sigma=1e-3, a=a)
+        ks = kernels_of(h)
+        Q.qsim_profile(h, False)
+        got = Q.qsim_get_state(h, 0, 1 << (ne + nw))
+    finally:
+        Q.qsim_destroy(h)
+    print("cfg3 ne=20 nw=6 kernels:", ks)
+    assert ks.get("k_qft_gen", 0) >= 4, ks    # noisy H_20 and noisy inverse QFT as fused passes
+    pr, psi = O.cfg3(ne=ne, nw=nw, N=N, seed=4, sigma=1e-3, a=a, want_state=True)
+    assert np.max(np.abs(P - pr)) < 1e-12
+    err = float(np.max(np.abs(got - psi)))
+    print(f"cfg3 noisy n=26: max |d alpha| = {err:.3e}")
+    assert err < TOL
+
+
+@pytest.mark.parametrize("sigma", [1e-3, 1e-4])
+def test_cfg3_full_config_noisy(sigma):
+    """configs[3] itself (n = 30, N = 1007, a = 558) with operational error;
+    the oracle needs ~2 x 16 GiB of host RAM."""
+    if host_ram_gib() < 56:
+        pytest.skip(f"host RAM {host_ram_gib():.0f} GiB < 56 GiB for the n = 30 oracle")
+    h = Q.qsim_create(30)
+    try:
+        P = W.run_cfg3(h, ne=20, nw=10, N=1007, seed=4, sigma=sigma)
+    finally:
+        Q.qsim_destroy(h)
+    pr = O.cfg3(ne=20, nw=10, N=1007, seed=4, sigma=sigma)
+    err = float(np.max(np.abs(P - pr)))
+    print(f"cfg3 n=30 sigma={sigma}: max |dP| = {err:.3e}")
+    assert err < 1e-12
+    assert abs(P.sum() - 1) < 1e-12
