@@ -201,8 +201,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int A, bool INV, bool HONLY>
 __global__ void __launch_bounds__(kThreads, 1)
     k_qft_tma(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
-              const __grid_constant__ TilePass tp, const __grid_constant__ TmaArgs ta, uint64_t ntiles)
+              const __grid_constant__ TilePass tp, const __grid_constant__ TmaArgs ta, uint64_t ntiles, int gbits)
 {
+    // this CTA's j-th tile: groups of 2^gbits consecutive tiles (adjacent
+    // runs of the lowest fixed positions), groups strided over the grid
+    const uint64_t gmask = (1ull << gbits) - 1;
+    auto tile_of = [&](uint64_t jj) -> uint64_t {
+        return ((blockIdx.x + (jj >> gbits) * (uint64_t)gridDim.x) << gbits) | (jj & gmask);
+    };
     static_assert(kRegBits == 4 && kTmaTileBits == 12 && A >= 4 && A <= 10, "window layout");
     constexpr int NST = (A + 3) / 4;   // register windows
     constexpr double SG = INV ? -1.0 : 1.0;
@@ -225,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tid == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&in_map) : "memory");
         for (uint64_t q = 0; q < kStages - 1; ++q) {
-            const uint64_t T = blockIdx.x + q * gridDim.x;
+            const uint64_t T = tile_of(q);
             if (T >= ntiles) break;
             int c[5];
             coords(ta.in_first, ta.in_len, T, c);
@@ -263,8 +269,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t yt = 0;
     for (int e = 0; e < tp.n_et; ++e) yt += (uint64_t)((tpart[0] >> tp.et_bit[e]) & 1u) << tp.et_w[e];
 
-    uint64_t j = 0;
-    for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x, ++j) {
+    for (uint64_t j = 0;; ++j) {
+        const uint64_t T = tile_of(j);
+        if (T >= ntiles) break;
         const int st = (int)(j % kStages);
         double2 *buf = bufs + (size_t)st * (1u << kTmaTileBits);
         mbar_wait(&full[st], (uint32_t)((j / kStages) & 1));
@@ -369,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             coords(ta.out_first, ta.out_len, T, c);
             tma_store(&out_map, c, buf);
             bulk_wait_read<1>();
-            const uint64_t Tn = T + (uint64_t)(kStages - 1) * gridDim.x;
+            const uint64_t Tn = tile_of(j + kStages - 1);
             if (Tn < ntiles) {
                 const int sn = (int)((j + kStages - 1) % kStages);
                 coords(ta.in_first, ta.in_len, Tn, c);
@@ -878,9 +885,14 @@ bool build_side(const double2 *base, int nl, const std::vector<int> &pos_of_tile
     // L2 promotion no wider than the box's contiguous run (a 256-byte
     // promotion of 128-byte runs also fetches the neighbouring run)
     const uint32_t run_bytes = box[0] * 8u;
-    const CUtensorMapL2promotion prom = run_bytes >= 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
-                                        : run_bytes >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
-                                                           : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    CUtensorMapL2promotion prom = run_bytes >= 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                  : run_bytes >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                     : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    static const int prom_env = getenv("QSIM_L2PROM") ? atoi(getenv("QSIM_L2PROM")) : -1;   // measurement knob
+    if (prom_env >= 0)
+        prom = prom_env >= 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+               : prom_env >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+               : prom_env >= 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
     CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void *)base, gdim, gstride, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, prom, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
@@ -912,9 +924,13 @@ void launch_fixed(Handle *h, const CUtensorMap &im, const CUtensorMap &om, const
         cudaFuncSetAttribute(k_qft_tma<A, INV, HONLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
     const uint64_t ntiles = 1ull << tp.nfix;
-    const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)h->num_sms);
+    // tiles per CTA group (QSIM_TILE_GROUP: measurement knob); groups keep the grid size
+    static const int genv = getenv("QSIM_TILE_GROUP") ? atoi(getenv("QSIM_TILE_GROUP")) : 0;
+    int gbits = genv;
+    while (gbits > 0 && (ntiles >> gbits) < (uint64_t)h->num_sms) --gbits;
+    const unsigned grid = (unsigned)std::min<uint64_t>(ntiles >> gbits, (uint64_t)h->num_sms);
     prof_begin(h);
-    k_qft_tma<A, INV, HONLY><<<grid, kThreads, smem, h->stream>>>(im, om, tp, ta, ntiles);
+    k_qft_tma<A, INV, HONLY><<<grid, kThreads, smem, h->stream>>>(im, om, tp, ta, ntiles, gbits);
     prof_end(h, "k_qft_tma", (1ull << (tp.tbits + tp.nfix)) * 32);
 }
 
