@@ -458,6 +458,20 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
         const int rest = m - amax, G1 = G - 1;
         for (int g = 1; g < G; ++g) gsize[g] = rest / G1 + (g - 1 < rest % G1 ? 1 : 0);
     }
+    // 2^13-amplitude tiles (k_qft13): one more passive bit per pass, so blocks
+    // of 9-10 wires keep 128-256-byte runs and the register needs
+    // ceil(m / 10) passes (n = 28: 10, 9, 9 -- three passes instead of four;
+    // measured per pass in profiles/r2_qft_passes.md).  The first block may
+    // take 10 wires: with block moves it writes one contiguous run per tile.
+    static const bool no13 = getenv("QSIM_NO_QFT13") != nullptr;   // measurement knob
+    const bool use13 = !gc && !no13 && h0->nl >= kTile13Bits + 2 && m >= 10;
+    if (use13 && !even) {
+        const int G13 = (m + 9) / 10;
+        gsize.assign(G13, 0);
+        gsize[0] = std::min(10, m - 5 * (G13 - 1));
+        const int rest = m - gsize[0], G1 = G13 - 1;
+        for (int g = 1; g < G13; ++g) gsize[g] = rest / G1 + (g - 1 < rest % G1 ? 1 : 0);
+    }
     if (const char *bl = getenv("QSIM_QFT_BLOCKS")) {   // measurement knob: explicit block sizes (tools/probe_blocks.sh)
         std::vector<int> v;
         int s = 0;
@@ -489,6 +503,76 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
         if (h0->world > 1) {
             if (int rc = dist_make_local(R, act)) return rc;
             for (int w = 0; w < m; ++w) wp[w] = h0->pos[lo + w];
+        }
+        // output permutation of the local positions (block moves)
+        std::vector<int> perm13(nl);
+        for (int p = 0; p < nl; ++p) perm13[p] = p;
+        if (block_moves) {
+            for (int w = a0 + a; w < m; ++w) perm13[wp[w]] = wp[w] + a;
+            for (int u = 0; u < a; ++u) perm13[wp[a0 + u]] = s0 + a0 + u;
+        }
+        if (use13 && a >= 5 && a <= 10 && !dry) {
+            // the 13-bit pass: active wires + the lowest 13 - a other positions
+            std::vector<int> tpos;
+            std::vector<char> in13(nl, 0);
+            for (int u = 0; u < a; ++u) { tpos.push_back(wp[a0 + u]); in13[wp[a0 + u]] = 1; }
+            for (int p = 0; p < nl && (int)tpos.size() < kTile13Bits; ++p)
+                if (!in13[p]) { tpos.push_back(p); in13[p] = 1; }
+            bool moved13 = false;
+            for (int p = 0; p < nl; ++p) moved13 |= !in13[p] && perm13[p] != p;
+            bool ok13 = true;
+            for (Handle *h : R) {
+                Qft13Desc d;
+                std::memset(&d, 0, sizeof d);
+                d.a = a;
+                for (int b = 0; b < kTile13Bits; ++b) {
+                    d.in_pos[b] = tpos[b];
+                    d.out_pos[b] = perm13[tpos[b]];
+                }
+                for (int p = 0; p < nl; ++p)
+                    if (!in13[p]) {
+                        d.fin_pos[d.nfix] = p;
+                        d.fout_pos[d.nfix] = perm13[p];
+                        d.nfix++;
+                    }
+                d.W = a0 + a;
+                d.inverse = inverse;
+                d.hadamard_only = !qft;
+                d.scale = std::ldexp(1.0, -(a / 2));
+                if (a & 1) d.scale *= M_SQRT1_2;
+                if (qft) {
+                    for (int i = 0; i < a0; ++i) {
+                        const int p = wp[i];
+                        if (p >= nl) { d.y_const += (uint64_t)((h->rank >> (p - nl)) & 1) << i; continue; }
+                        int b = -1;
+                        for (int t = 0; t < kTile13Bits; ++t) if (d.in_pos[t] == p) b = t;
+                        if (b >= 0) { d.et_bit[d.n_et] = b; d.et_w[d.n_et] = i; d.n_et++; }
+                        else {
+                            int f = -1;
+                            for (int t = 0; t < d.nfix; ++t) if (d.fin_pos[t] == p) f = t;
+                            d.ef_bit[d.n_ef] = f; d.ef_w[d.n_ef] = i; d.n_ef++;
+                        }
+                    }
+                }
+                double2 *out = h->psi;
+                if (moved13) {
+                    if (ensure_scratch(h)) return QSIM_ENOMEM;
+                    out = h->scratch;
+                }
+                if (!launch_qft13(h, d, h->psi, out)) {
+                    if (h != R[0]) return fail(h, QSIM_ECUDA, "13-bit QFT pass geometry differs between ranks");
+                    ok13 = false;
+                    break;
+                }
+                if (moved13) swap_buffers(h);
+                if (int rc = after_launch(h, "fused tile pass (13)")) return rc;
+            }
+            if (ok13) {
+                for (int w = 0; w < m; ++w)
+                    if (wp[w] < nl) wp[w] = perm13[wp[w]];
+                a0 += a;
+                continue;
+            }
         }
         // tile: active wires (tile bits 0..a-1) + passive low positions
         std::vector<int> tile_pos;

@@ -29,6 +29,7 @@
 #include "ops_common.cuh"
 #include "tile_common.cuh"
 #include "mbar.cuh"
+#include "tma_host.h"
 
 namespace qs {
 
@@ -805,6 +806,8 @@ __global__ void __launch_bounds__(2 * ops::kOpsThreads, 1)
 }
 
 // ------------------------------------------------------------------ host
+}  // namespace
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -897,6 +900,8 @@ bool build_side(const double2 *base, int nl, const std::vector<int> &pos_of_tile
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, prom, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
+
+namespace {
 
 template <int NM>
 void launch_tma_nm(Handle *h, const CUtensorMap &im, const CUtensorMap &om, const TilePass &tp, const TmaArgs &ta)

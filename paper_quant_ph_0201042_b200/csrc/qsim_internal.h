@@ -157,6 +157,24 @@ struct QftGen {
 };
 // true: launched; false: the pass geometry does not fit the kernel (nothing launched)
 bool launch_qft_gen_tma(Handle *h, const TilePass &tp, const QftGen &g, const double2 *in, double2 *out);
+
+// A fused QFT / H pass on 2^13-amplitude tiles (k_qft13.cu): tile bits 0..a-1
+// are the active wires in H order, a..12 passive positions; same twiddle
+// fields as TilePass.  Fixed positions fin_pos[] must be ascending (tile-id
+// bit f <-> the f-th lowest fixed position).  false: geometry unsupported.
+constexpr int kTile13Bits = 13;
+struct Qft13Desc {
+    int a;
+    int in_pos[kTile13Bits], out_pos[kTile13Bits];
+    int nfix;
+    int fin_pos[kMaxFixedBits], fout_pos[kMaxFixedBits];
+    int n_et, et_bit[kTile13Bits], et_w[kTile13Bits];
+    int n_ef, ef_bit[kMaxFixedBits], ef_w[kMaxFixedBits];
+    uint64_t y_const;
+    int W, inverse, hadamard_only;
+    double scale;
+};
+bool launch_qft13(Handle *h, const Qft13Desc &d, const double2 *in, double2 *out);
 bool qft_gen_feasible(Handle *h, const TilePass &tp);
 
 // Fused gate-list passes (k_ops.cu): ops of one pass, applied per tile.

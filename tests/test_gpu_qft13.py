@@ -1,0 +1,114 @@
+"""The 2^13-amplitude-tile QFT / H pass (k_qft13, round 2) against the oracle's
+gate-by-gate circuit and H_n: every
+block size it takes (5..10 wires), forward and inverse, sub-ranges, the block
+partitions of the default plan and explicit ones (QSIM_QFT_BLOCKS), in-place
+(Hadamard, sharded) and block-move (single-GPU QFT) layouts, and the kernel
+record proving the pass ran."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+Q = pytest.importorskip("paper_quant_ph_0201042_b200.qsim")
+
+TOL = 1e-10
+
+
+def rand_state(n, seed):
+    rng = np.random.default_rng(seed)
+    v = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    return v / np.linalg.norm(v)
+
+
+def run(n, op, lo, m, inverse=False, world=1, blocks=None):
+    psi = rand_state(n, 3 * n + lo + 7 * m)
+    if blocks:
+        os.environ["QSIM_QFT_BLOCKS"] = blocks
+    try:
+        h = Q.qsim_create(n, world)
+        Q.qsim_set_state(h, 0, psi)
+        Q.qsim_profile(h, True)
+        if op == "qft":
+            Q.qsim_qft(h, lo, m, inverse)
+        elif op == "fft":
+            Q.qsim_fft(h, lo, m, inverse)
+        else:
+            Q.qsim_hadamard(h, lo, m)
+        prof = Q.qsim_profile_json(h)
+        Q.qsim_profile(h, False)
+        got = Q.qsim_get_state(h, 0, 1 << n)
+        norm = Q.qsim_norm(h)
+        Q.qsim_destroy(h)
+    finally:
+        os.environ.pop("QSIM_QFT_BLOCKS", None)
+    ref = psi.copy()
+    if op == "had":
+        O.hadamard_range(ref, lo, m)
+    else:
+        O.qft(ref, lo, m, inverse)
+    return got, ref, norm, prof
+
+
+@pytest.mark.parametrize("inverse", [False, True])
+@pytest.mark.parametrize("n,lo,m", [(15, 0, 15), (16, 0, 16), (18, 0, 18), (20, 0, 20), (21, 0, 21),
+                                    (22, 0, 22), (23, 0, 23), (24, 0, 24), (20, 2, 15), (19, 4, 10),
+                                    (22, 1, 20), (17, 0, 11)])
+def test_qft13_default_plan(n, lo, m, inverse):
+    got, ref, norm, prof = run(n, "qft", lo, m, inverse)
+    assert "k_qft13" in prof, prof.keys()
+    assert np.max(np.abs(got - ref)) < TOL
+    assert abs(norm - 1) < 1e-12
+
+
+@pytest.mark.parametrize("blocks", ["10,10", "5,10,5", "6,7,7", "9,5,6", "8,6,6", "10,5,5", "7,6,7"])
+def test_qft13_block_partitions(blocks):
+    n = 20
+    got, ref, _, prof = run(n, "qft", 0, n, False, blocks=blocks)
+    assert "k_qft13" in prof
+    assert np.max(np.abs(got - ref)) < TOL
+
+
+@pytest.mark.parametrize("n,lo,m", [(16, 0, 16), (20, 0, 20), (21, 3, 12), (24, 0, 24), (18, 5, 13)])
+def test_hadamard13(n, lo, m):
+    got, ref, _, prof = run(n, "had", lo, m)
+    assert "k_qft13" in prof
+    assert np.max(np.abs(got - ref)) < TOL
+
+
+@pytest.mark.parametrize("n,lo,m,inverse", [(20, 0, 20, False), (19, 2, 14, True)])
+def test_fft13(n, lo, m, inverse):
+    got, ref, _, prof = run(n, "fft", lo, m, inverse)
+    assert "k_qft13" in prof
+    assert np.max(np.abs(got - ref)) < TOL
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("op", ["qft", "had"])
+def test_qft13_sharded(world, op):
+    n = 19
+    got, ref, _, prof = run(n, op, 0, n, False, world=world)
+    assert np.max(np.abs(got - ref)) < TOL
+
+
+def test_qft13_off_matches_on():
+    """QSIM_NO_QFT13 (the 12-bit kernels) and the 13-bit plan agree."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = (
+        "import sys, numpy as np; sys.path.insert(0, sys.argv[1]);"
+        "from paper_quant_ph_0201042_b200 import qsim as Q;"
+        "h = Q.qsim_create(22); Q.qsim_init_gaussian(h, 3); Q.qsim_qft(h, 0, 22, False);"
+        "np.save(sys.argv[2], Q.qsim_get_state(h, 0, 1 << 22))")
+    outs = []
+    for env in ({}, {"QSIM_NO_QFT13": "1"}):
+        path = f"/tmp/qft13_{len(env)}.npy"
+        r = subprocess.run([sys.executable, "-c", script, root, path], env=dict(os.environ, **env),
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        outs.append(np.load(path))
+    assert np.max(np.abs(outs[0] - outs[1])) < 1e-13
