@@ -5,12 +5,13 @@ seeded complex-Gaussian input) through libqsim's C-ABI.
 Metric (BASELINE.json): "state-vector GB/s per gate (% HBM peak) & circuit
 time".  One step = the whole QFT circuit (28 H + 378 controlled R_d + 14
 SWAP) on the 4 GiB state resident in HBM.  value = the
-effective per-gate state-vector bandwidth: the sum over the circuit's gates of
-the bytes each gate must move in the paper's one-sweep-per-gate model
-(dense/H: 2^(n+5) B, controlled R_d: 2^(n+3) B, SWAP: 2^(n+4) B) divided by
-the circuit time.  Because gates are fused into a few HBM passes this can
-exceed the HBM peak; the `roofline` object reports the dominant kernel's real
-fraction of the measured HBM peak.
+per-gate state-vector bandwidth in the paper's one-sweep-per-gate model: the
+bytes each gate of the circuit must move when applied alone (dense/H:
+2^(n+5) B, controlled R_d: 2^(n+3) B, SWAP: 2^(n+4) B; 1036 GiB at n = 28)
+divided by the circuit time -- the unit says "effective" because fused passes
+move far fewer bytes.  The bytes the passes really move and their fraction of
+the measured HBM peak are in `roofline` (dominant kernel) and
+config["hbm_gbs_achieved"] (whole circuit).
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N (one process per GPU;
@@ -18,6 +19,7 @@ the state is sharded on its top log2 N qubits, exchanges over NCCL).
 """
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -31,6 +33,7 @@ sys.path.insert(0, ROOT)
 N_QUBITS = 28
 SEED = 3
 METRIC = "state-vector GB/s per gate (QFT circuit; % HBM peak in roofline) & circuit time"
+UNIT = "GB/s effective (one-sweep-per-gate bytes / circuit time)"
 WORKLOAD = "configs[2]: QFT circuit, n=28 complex128 (4 GiB), seeded complex-Gaussian input"
 
 
@@ -102,20 +105,21 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(n_sample=24):
-    """The oracle as it stands (plain C + OpenMP) on the host cores: the
-    same QFT circuit on a smaller seeded Gaussian state, timed around the
-    circuit only; reported in the same per-gate GB/s unit."""
+def cpu_baseline(n_full=N_QUBITS):
+    """The oracle as it stands (plain C + OpenMP) on the host cores, on the
+    bench's own configuration: the whole configs[2] QFT circuit at n = 28 on
+    the same seeded Gaussian state (one run, ~25 s on 16 cores), timed around
+    the circuit only; reported in the same per-gate unit."""
     import oracle as O
-    import numpy as np  # noqa: F401
-    psi = O.gaussian_state(n_sample, SEED)
+    psi = O.gaussian_state(n_full, SEED)
     t0 = time.perf_counter()
-    O.qft(psi, 0, n_sample, False)
+    O.qft(psi, 0, n_full, False)
     dt = time.perf_counter() - t0
-    gb, ng = gate_bytes(n_sample)
+    del psi
+    gb, ng = gate_bytes(n_full)
     cores = O.get_threads()
     # one thread, the paper's 1-processor column (SURVEY.md 8(d)), on a smaller sample
-    n1 = max(4, n_sample - 2)
+    n1 = 22
     psi1 = O.gaussian_state(n1, SEED)
     O.set_threads(1)
     t1 = time.perf_counter()
@@ -123,47 +127,65 @@ def cpu_baseline(n_sample=24):
     dt1 = time.perf_counter() - t1
     O.set_threads(0)
     gb1, ng1 = gate_bytes(n1)
-    return {"value": gb / dt / 1e9, "unit": "GB/s", "cores": cores, "kind": "oracle",
-            "sample": f"oracle QFT circuit on n={n_sample} (one run, {ng} gates, {dt:.2f} s); "
-                      f"same metric definition as the GPU line",
-            "seconds": dt,
-            "single_thread": {"value": gb1 / dt1 / 1e9, "unit": "GB/s", "cores": 1, "seconds": dt1,
+    return {"value": gb / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"the full configs[2] circuit: oracle QFT on the n={n_full} seeded Gaussian state "
+                      f"({ng} gates, one run, {dt:.1f} s)",
+            "seconds": dt, "same_config": n_full == N_QUBITS,
+            "single_thread": {"value": gb1 / dt1 / 1e9, "unit": UNIT, "cores": 1, "seconds": dt1,
                               "sample": f"oracle QFT circuit on n={n1} ({ng1} gates) on one host thread"}}
 
 
+def qft_row_gates(n, j):
+    """Row j of the QFT circuit (PAPER.md:447-457): H(j), then R_{k-j}
+    controlled by k on j for k > j; returns (kind, control, angle) tuples."""
+    return [("h", -1, 0.0)] + [("r", k, math.pi / (1 << (k - j))) for k in range(j + 1, n)]
+
+
 def run_reference(args):
+    """The reference arm: the oracle on the host cores on our own config
+    (configs[2], n = 28, the same seeded Gaussian state).  The whole circuit
+    takes ~25 s, so each step is a bounded sample of it: one row of the QFT
+    circuit (H(j) and its controlled R_d), rows taken in
+    turn from j = 0; the per-gate unit makes rows comparable."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    steps, warm = args.steps, args.warmup
+    import numpy as np
     import oracle as O
-    n_sample = args.ref_n
-    gb, ng = gate_bytes(n_sample)
-    times = []
-    for i in range(warm + steps):
-        psi = O.gaussian_state(n_sample, SEED)
+    n = args.ref_n
+    psi = O.gaussian_state(n, SEED)
+    Hm = np.array([[1, 1], [1, -1]], complex) / math.sqrt(2)
+    times, gbs = [], []
+    for i in range(args.warmup + args.steps):
+        j = i % n
+        gates = qft_row_gates(n, j)
         t0 = time.perf_counter()
-        O.qft(psi, 0, n_sample, False)
+        for kind, c, ang in gates:
+            if kind == "h":
+                O.apply_1q(psi, j, Hm)
+            else:
+                O.apply_ctrl(psi, 1 << c, 1 << c, j, np.diag([1.0, complex(math.cos(ang), math.sin(ang))]))
         dt = time.perf_counter() - t0
-        if i >= warm:
+        if i >= args.warmup:
             times.append(dt)
+            gbs.append(((1 << (n + 5)) + (len(gates) - 1) * (1 << (n + 3))) / 1e9)
     t = statistics.mean(times)
-    value = gb / t / 1e9
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    # same metric / unit / config as our arm; each step is a bounded sample
-    # of the workload (the same circuit at n = n_sample), in the same per-gate unit
+    value = sum(gbs) / sum(times)
+    cores = O.get_threads()
     gb_full, ng_full = gate_bytes(N_QUBITS)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
-        "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded complex Gaussian, DESIGN.md R19)",
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded complex Gaussian, DESIGN.md R19)",
         "config": {"workload": WORKLOAD, "n": N_QUBITS, "gates": ng_full, "gate_bytes": gb_full,
                    "state_bytes": 16 << N_QUBITS, "parallelism": "cpu-oracle",
-                   "sample": f"each step: the same QFT circuit on a seeded Gaussian n={n_sample} state "
-                             f"({ng} gates) run by the CPU oracle (plain C + OpenMP)"},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "oracle",
-                         "sample": f"oracle QFT circuit, n={n_sample}, {steps} timed runs"},
-        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                   "sample": f"each step: one row of the QFT circuit (H(j) + its controlled R_d) on the n={n} "
+                             f"seeded Gaussian state, rows j = 0, 1, ... in turn, by the CPU oracle "
+                             f"(plain C + OpenMP)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"oracle QFT-circuit rows at n={n}, {args.steps} timed steps"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -176,10 +198,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_QUBITS)
-    ap.add_argument("--ref-n", type=int, default=22)
-    ap.add_argument("--cpu-n", type=int, default=24)
+    ap.add_argument("--ref-n", type=int, default=N_QUBITS)
+    ap.add_argument("--cpu-n", type=int, default=N_QUBITS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--profile-only", action="store_true", help="warm-up + steps only (for ncu)")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -260,6 +282,10 @@ def main():
 
     # dominant kernel roofline (algorithmic bytes per launch / mean launch time)
     ours = {k: v for k, v in prof.items() if not k.startswith("nccl_")}
+    # the whole circuit's real HBM traffic: the algorithmic bytes of every launch
+    pass_bytes = sum(v["bytes"] for v in ours.values()) / args.steps
+    hbm_ach = pass_bytes / (ms * 1e-3) / 1e9 / world
+    passes = sum(v["launches"] for k, v in ours.items() if k.startswith("k_qft")) / args.steps
     comm = {k: v for k, v in prof.items() if k.startswith("nccl_")}
     dom = max(ours.items(), key=lambda kv: kv[1]["ms"]) if ours else None
     roof = None
@@ -293,29 +319,38 @@ def main():
                       "share_of_step": cms / (ms * args.steps),
                       "ops": {k: v["launches"] for k, v in comm.items()}}
 
-    # ---------------- end to end: host buffers through the C-ABI
+    # ---------------- end to end: host buffers through the C-ABI.  Single GPU:
+    # qsim_qft_host_stream pipelines the steps (copy in of step i+1 and copy
+    # out of step i-1 overlap the transform of step i); every step still moves
+    # its whole input in and its whole result out over PCIe inside the timed call.
     shard = 1 << (n - (world.bit_length() - 1))
     host_in = torch.empty(shard, dtype=torch.complex128, pin_memory=True).numpy()
     host_out = torch.empty(shard, dtype=torch.complex128, pin_memory=True).numpy()
     Q.qsim_get_state(h, rank * shard, shard, host_in)
     barrier()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    for _ in range(args.e2e_steps):
-        Q.qsim_set_state(h, rank * shard, host_in)
-        step()
-        Q.qsim_get_state(h, rank * shard, shard, host_out)
-    f1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = f0.elapsed_time(f1) / args.e2e_steps
+    if world == 1:
+        Q.qsim_qft_host_stream(h, 0, n, False, host_in, host_out, 1, 0, 0)   # warm the stages
+        t0 = time.perf_counter()
+        Q.qsim_qft_host_stream(h, 0, n, False, host_in, host_out, args.e2e_steps, 0, 0)
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
+        e2e_how = "qsim_qft_host_stream (pipelined host->device, transform, device->host)"
+    else:
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            Q.qsim_set_state(h, rank * shard, host_in)
+            step()
+            Q.qsim_get_state(h, rank * shard, shard, host_out)
+        torch.cuda.synchronize()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
+        e2e_how = "qsim_set_state + qsim_qft + qsim_get_state per step (serial)"
     if world > 1:
         t = torch.tensor([e2e_ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e = {"value": gb / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
-           "h2d_bytes_per_step": shard * 16 * world, "d2h_bytes_per_step": shard * 16 * world}
+    e2e = {"value": gb / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
+           "h2d_bytes_per_step": shard * 16 * world, "d2h_bytes_per_step": shard * 16 * world,
+           "how": e2e_how, "steps": args.e2e_steps}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -324,14 +359,15 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC,
-            "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded complex Gaussian, DESIGN.md R19)",
             "config": {"workload": WORKLOAD, "n": n, "gates": ngates, "gate_bytes": gb,
                        "state_bytes": 16 << n, "parallelism": f"sv-shard{world}",
                        "l2": "inputs larger than L2 (4 GiB state vs 126 MB L2)",
                        "circuit_ms": ms, "effective_frac_of_hbm_peak": value / peak,
-                       "norm_after": norm},
+                       "hbm_gbs_achieved": hbm_ach, "hbm_frac_achieved": hbm_ach / peak,
+                       "passes_per_step": passes, "norm_after": norm},
             "roofline": roof,
             "nvlink": nvlink,
             "cpu_baseline": cpu,

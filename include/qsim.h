@@ -247,6 +247,18 @@ int qsim_fft(qsim_t *h, int lo, int m, int inverse);
  * the range leaves [0, n) or b < 0. */
 int qsim_aqft(qsim_t *h, int lo, int m, int b, int inverse);
 
+/* The QFT (as qsim_qft, noiseless) of `count` host-resident states, end to
+ * end and pipelined: state i is in[i * in_stride .. + 2^n) and its transform
+ * goes to out[i * out_stride .. + 2^n) (strides in amplitudes; 0 reuses one
+ * buffer).  State i+1 is copied to the device on one stream while state i is
+ * transformed and state i-1 copied back on another, through four device shard
+ * buffers (the state, the scratch and two stages: 4 x 2^(n+4) bytes).  Use
+ * pinned host memory for the copies to overlap.  The handle's state becomes
+ * the last result.  Synchronising.  Single-GPU handles without gate noise;
+ * QSIM_EINVAL otherwise, QSIM_ERANGE on the range, QSIM_ENOMEM. */
+int qsim_qft_host_stream(qsim_t *h, int lo, int m, int inverse, const qsim_c128 *in, uint64_t in_stride,
+                         qsim_c128 *out, uint64_t out_stride, int count);
+
 /* Sign-changing operator V_f for f = delta_{x, idx}, as
  * the phase flip alpha_idx <- -alpha_idx (R17).  QSIM_ERANGE if
  * idx >= 2^n. */

@@ -511,7 +511,12 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
             for (int w = a0 + a; w < m; ++w) perm13[wp[w]] = wp[w] + a;
             for (int u = 0; u < a; ++u) perm13[wp[a0 + u]] = s0 + a0 + u;
         }
-        if (use13 && a >= 5 && a <= 10 && !dry) {
+        // in place (no block moves), a block on the lowest positions would put
+        // them in the last register window: 512-byte runs per thread, one
+        // 16-byte store per lane per run -- that pass stays on the 12-bit kernel
+        bool low_block = false;
+        for (int u = 0; u < a; ++u) low_block |= !block_moves && wp[a0 + u] < kTile13Bits - a + 5;
+        if (use13 && a >= 5 && a <= 10 && !dry && !low_block) {
             // the 13-bit pass: active wires + the lowest 13 - a other positions
             std::vector<int> tpos;
             std::vector<char> in13(nl, 0);
@@ -907,6 +912,10 @@ void qsim_destroy(qsim_t *h)
     if (h->d_red) cudaFree(h->d_red);
     if (h->d_probs) cudaFree(h->d_probs);
     if (h->d_sum2) cudaFree(h->d_sum2);
+    for (double2 *b : h->stage)
+        if (b) cudaFree(b);
+    if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
+    if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
     if (h->d_tabs) cudaFree(h->d_tabs);
     if (h->h_red) cudaFreeHost(h->h_red);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
@@ -1395,6 +1404,106 @@ int qsim_qft(qsim_t *h, int lo, int m, int inverse)
     }
     // noisy, or fusion off (the paper's one sweep per gate)
     return qft_gates(h, R, lo, m, m, inverse, true);
+}
+
+// QFT of `count` host-resident states, pipelined: state i+1 is copied in
+// (its own stream) while state i is transformed and state i-1 copied out
+// (a third stream).  Four shard buffers (psi, scratch, two stages) rotate;
+// cross-stream order comes from events recorded on the streams that last
+// used each buffer.  Every transform is qsim_qft's own fused pass plan.
+int qsim_qft_host_stream(qsim_t *h, int lo, int m, int inverse, const qsim_c128 *in, uint64_t in_stride,
+                         qsim_c128 *out, uint64_t out_stride, int count)
+{
+    QS_CHECK_HANDLE(h);
+    if (lo < 0 || m < 1 || lo + m > h->n) return fail(h, QSIM_ERANGE, "range outside [0, n)");
+    if (count < 0 || (count > 0 && (!in || !out))) return fail(h, QSIM_EINVAL, "host buffers / count");
+    if (h->world != 1 || !h->members.empty() || h->batch_b)
+        return fail(h, QSIM_EINVAL, "qsim_qft_host_stream runs on a single-GPU handle");
+    if (h->sigma != 0.0) return fail(h, QSIM_EINVAL, "qsim_qft_host_stream: noiseless transforms only");
+    if (count == 0) return QSIM_OK;
+    const Ranks R = ranks_of(h);
+    cudaSetDevice(h->device);
+    if (int rc = flush_queue(h)) return rc;
+    if (int rc = ensure_scratch(h)) return rc;
+    for (double2 *&b : h->stage)
+        if (!b && check_cuda(h, cudaMalloc(&b, sizeof(double2) * h->local_dim()), "stream stage buffer"))
+            return QSIM_ENOMEM;
+    if (!h->s_h2d && check_cuda(h, cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking), "copy stream"))
+        return QSIM_ECUDA;
+    if (!h->s_d2h && check_cuda(h, cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking), "copy stream"))
+        return QSIM_ECUDA;
+    for (int q = 0; q < h->n; ++q) h->pos[q] = h->n - 1 - q;   // each input is given in the canonical layout
+    const size_t bytes = sizeof(double2) * h->local_dim();
+    double2 *buf[4] = {h->psi, h->scratch, h->stage[0], h->stage[1]};
+    cudaEvent_t done[4];   // last use of each buffer (any stream)
+    for (auto &e : done) {
+        cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        cudaEventRecord(e, h->stream);
+    }
+    auto idx_of = [&](const double2 *p) {
+        for (int b = 0; b < 4; ++b)
+            if (buf[b] == p) return b;
+        return -1;
+    };
+    int busy_out = -1, busy_out2 = -1;   // buffers still being copied out (states i-1, i-2)
+    int in_next = 2;                     // buffer the next input lands in
+    int rc = QSIM_OK;
+    // first input
+    cudaStreamWaitEvent(h->s_h2d, done[in_next], 0);
+    rc = check_cuda(h, cudaMemcpyAsync(buf[in_next], in, bytes, cudaMemcpyHostToDevice, h->s_h2d), "stream H2D");
+    for (int i = 0; i < count && !rc; ++i) {
+        const int cur = in_next;
+        cudaEvent_t landed;
+        cudaEventCreateWithFlags(&landed, cudaEventDisableTiming);
+        cudaEventRecord(landed, h->s_h2d);
+        cudaStreamWaitEvent(h->stream, landed, 0);
+        cudaEventDestroy(landed);
+        // the compute scratch: a buffer that is neither the input nor being copied out
+        int sc = -1;
+        for (int b = 0; b < 4 && sc < 0; ++b)
+            if (b != cur && b != busy_out && b != busy_out2) sc = b;
+        cudaStreamWaitEvent(h->stream, done[sc], 0);
+        h->psi = buf[cur];
+        h->scratch = buf[sc];
+        rc = fused_range(R, lo, m, 1, inverse);
+        if (rc) break;
+        h->gcount += (uint64_t)m + (uint64_t)m * (m - 1) / 2;
+        const int res = idx_of(h->psi), other = idx_of(h->scratch);
+        cudaEventRecord(done[other], h->stream);
+        cudaEventRecord(done[res], h->stream);
+        // the next input: a buffer not holding this result, not being copied out
+        if (i + 1 < count) {
+            in_next = -1;
+            for (int b = 0; b < 4 && in_next < 0; ++b)
+                if (b != res && b != busy_out && b != other) in_next = b;
+            if (in_next < 0) in_next = other;
+            cudaStreamWaitEvent(h->s_h2d, done[in_next], 0);
+            rc = check_cuda(h, cudaMemcpyAsync(buf[in_next], in + (size_t)(i + 1) * in_stride, bytes, cudaMemcpyHostToDevice,
+                                               h->s_h2d), "stream H2D");
+            if (rc) break;
+        }
+        // copy the result out once the transform is done
+        cudaStreamWaitEvent(h->s_d2h, done[res], 0);
+        rc = check_cuda(h, cudaMemcpyAsync(out + (size_t)i * out_stride, buf[res], bytes, cudaMemcpyDeviceToHost, h->s_d2h),
+                        "stream D2H");
+        cudaEventRecord(done[res], h->s_d2h);
+        busy_out2 = busy_out;
+        busy_out = res;
+    }
+    if (!rc) rc = check_cuda(h, cudaStreamSynchronize(h->s_h2d), "stream H2D");
+    if (!rc) rc = check_cuda(h, cudaStreamSynchronize(h->stream), "stream compute");
+    if (!rc) rc = check_cuda(h, cudaStreamSynchronize(h->s_d2h), "stream D2H");
+    for (auto &e : done) cudaEventDestroy(e);
+    // the handle keeps the last result as its state; the other buffers as scratch / stages
+    const int res = idx_of(h->psi);
+    int k = 0;
+    for (int b = 0; b < 4; ++b) {
+        if (b == res) continue;
+        if (k == 0) h->scratch = buf[b];
+        else h->stage[k - 1] = buf[b];
+        ++k;
+    }
+    return rc;
 }
 
 int qsim_fft(qsim_t *h, int lo, int m, int inverse)

@@ -285,6 +285,10 @@ struct Handle {
     double *h_red = nullptr;     // pinned
     size_t hred_cap = 0;
     double *d_sum2 = nullptr;    // 2 doubles: amplitude-sum result (diffusion), outside d_red
+    // host-stream pipeline (qsim_qft_host_stream): two extra shard buffers and
+    // the copy streams (created on first use)
+    double2 *stage[2] = {nullptr, nullptr};
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     int strict = 0;              // qsim_set_strict: reject non-unitary matrices (QSIM_ENONUNITARY)
     // angle noise (R15)
     uint64_t noise_seed = 0;

@@ -109,6 +109,7 @@ _sig("qsim_batch_overlap", _i32, _H, _p, _p)
 _sig("qsim_phase_flip", _i32, _H, _u64)
 _sig("qsim_grover", _i32, _H, _u64, _i32, _p)
 _sig("qsim_diffusion", _i32, _H, _i32, _i32)
+_sig("qsim_qft_host_stream", _i32, _H, _i32, _i32, _i32, _p, _u64, _p, _u64, _i32)
 _sig("qsim_set_strict", _i32, _H, _i32)
 _sig("qsim_apply_perm", _i32, _H, C.POINTER(qsim_perm_t))
 _sig("qsim_inject_errors", _i32, _H, _u64, C.POINTER(qsim_noise_t), _p, _i32, C.POINTER(_i32))
@@ -335,6 +336,15 @@ def qsim_grover(h, mark: int, iters: int, trace: bool = True):
     out = np.zeros(max(iters, 1), np.float64) if trace else None
     _chk(h, lib.qsim_grover(h, mark, iters, out.ctypes.data if trace else None))
     return out[:iters] if trace else None
+
+
+def qsim_qft_host_stream(h, lo: int, m: int, inverse: bool, inp: np.ndarray, out: np.ndarray, count: int,
+                         in_stride: int, out_stride: int) -> None:
+    """inp / out: complex128 host arrays (pinned for overlap) holding the states at the given strides."""
+    assert inp.dtype == np.complex128 and out.dtype == np.complex128
+    assert inp.flags.c_contiguous and out.flags.c_contiguous
+    _chk(h, lib.qsim_qft_host_stream(h, lo, m, int(bool(inverse)), inp.ctypes.data, in_stride, out.ctypes.data,
+                                     out_stride, count))
 
 
 def qsim_diffusion(h, lo: int, m: int) -> None:

@@ -200,3 +200,60 @@ def test_generalised_qft_without_block_moves():
     r = subprocess.run([sys.executable, "-c", _NO_MOVES_SCRIPT, ROOT], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("n,lo,m,inv", [(18, 0, 18, False), (17, 2, 12, True)])
+def test_qft_host_stream(n, lo, m, inv):
+    """Pipelined end-to-end QFTs of host states (qsim_qft_host_stream) equal
+    the oracle's circuit on each state; the handle keeps the last result and
+    keeps working afterwards."""
+    count = 5
+    rng = np.random.default_rng(n)
+    states = rng.normal(size=(count, 1 << n)) + 1j * rng.normal(size=(count, 1 << n))
+    states /= np.linalg.norm(states, axis=1, keepdims=True)
+    inp = np.ascontiguousarray(states)
+    out = np.zeros_like(inp)
+    h = Q.qsim_create(n)
+    try:
+        Q.qsim_qft_host_stream(h, lo, m, inv, inp, out, count, 1 << n, 1 << n)
+        last = Q.qsim_get_state(h, 0, 1 << n)
+        # the handle still works: one more transform on the resident state
+        Q.qsim_qft(h, lo, m, not inv)
+        back = Q.qsim_get_state(h, 0, 1 << n)
+        # stride 0: the same input every time, one output buffer
+        one = np.zeros(1 << n, np.complex128)
+        Q.qsim_qft_host_stream(h, lo, m, inv, inp[0].copy(), one, 3, 0, 0)
+    finally:
+        Q.qsim_destroy(h)
+    for i in range(count):
+        ref = states[i].copy()
+        O.qft(ref, lo, m, inv)
+        assert np.max(np.abs(out[i] - ref)) < TOL, i
+    assert np.max(np.abs(last - out[-1])) == 0.0
+    assert np.max(np.abs(back - states[-1])) < TOL
+    ref0 = states[0].copy()
+    O.qft(ref0, lo, m, inv)
+    assert np.max(np.abs(one - ref0)) < TOL
+
+
+def test_qft_host_stream_errors():
+    h = Q.qsim_create(10)
+    try:
+        x = np.zeros(1 << 10, np.complex128)
+        with pytest.raises(Q.QsimError) as e:
+            Q.qsim_qft_host_stream(h, 3, 9, False, x, x, 1, 0, 0)
+        assert e.value.code == Q.QSIM_ERANGE
+        Q.qsim_set_gate_noise(h, 1, 1e-3)
+        with pytest.raises(Q.QsimError) as e:
+            Q.qsim_qft_host_stream(h, 0, 10, False, x, x, 1, 0, 0)
+        assert e.value.code == Q.QSIM_EINVAL
+    finally:
+        Q.qsim_destroy(h)
+    g = Q.qsim_create(12, 2)
+    try:
+        x = np.zeros(1 << 12, np.complex128)
+        with pytest.raises(Q.QsimError) as e:
+            Q.qsim_qft_host_stream(g, 0, 12, False, x, x, 1, 0, 0)
+        assert e.value.code == Q.QSIM_EINVAL
+    finally:
+        Q.qsim_destroy(g)
