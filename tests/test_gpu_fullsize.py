@@ -88,7 +88,7 @@ def test_cfg4_n24_whole_vector(p):
     ref, rev = O.cfg4(n=n, layers=20, seed=5, sigma=1e-3, p=p)
     assert [tuple(e) for e in ev] == [tuple(e) for e in rev]
     if p > 1e-3:
-        assert len(rev) > 10
+        assert len(rev) >= 4   # ~ 20 x 24 x p = 9.6 expected
     err = float(np.max(np.abs(got - ref)))
     print(f"cfg4 n=24 p={p}: max |d alpha| = {err:.3e}, events {len(rev)}")
     assert err < TOL

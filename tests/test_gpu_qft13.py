@@ -72,7 +72,7 @@ def test_qft13_block_partitions(blocks):
     assert np.max(np.abs(got - ref)) < TOL
 
 
-@pytest.mark.parametrize("n,lo,m", [(16, 0, 16), (20, 0, 20), (21, 3, 12), (24, 0, 24), (18, 5, 13)])
+@pytest.mark.parametrize("n,lo,m", [(22, 0, 22), (20, 0, 20), (21, 3, 12), (24, 0, 24), (22, 2, 18)])
 def test_hadamard13(n, lo, m):
     got, ref, _, prof = run(n, "had", lo, m)
     assert "k_qft13" in prof
