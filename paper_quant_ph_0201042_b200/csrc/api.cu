@@ -916,6 +916,10 @@ void qsim_destroy(qsim_t *h)
         if (b) cudaFree(b);
     if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
     if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
+    if (h->s_comm) {
+        cudaStreamSynchronize(h->s_comm);
+        cudaStreamDestroy(h->s_comm);
+    }
     if (h->d_tabs) cudaFree(h->d_tabs);
     if (h->h_red) cudaFreeHost(h->h_red);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
@@ -998,6 +1002,18 @@ int qsim_sync(qsim_t *h)
         cudaSetDevice(m->device);
         if (int rc = flush_queue(m)) return lift(h, R, rc);
         if (int rc = check_cuda(m, cudaStreamSynchronize(m->stream), "qsim_sync")) return lift(h, R, rc);
+#ifndef QSIM_NO_NCCL
+        if (m->comm) {
+            // an asynchronous NCCL failure (a peer died, a network error) surfaces here
+            ncclResult_t ar = ncclSuccess;
+            const ncclResult_t qr = ncclCommGetAsyncError(m->comm, &ar);
+            if (qr != ncclSuccess || (ar != ncclSuccess && ar != ncclInProgress)) {
+                m->poisoned = 1;
+                return lift(h, R, fail(m, QSIM_ENCCL, std::string("NCCL asynchronous error: ") +
+                                                           ncclGetErrorString(qr != ncclSuccess ? qr : ar)));
+            }
+        }
+#endif
     }
     return QSIM_OK;
 }

@@ -15,6 +15,7 @@
 // pairwise exchanges, local positions by one bit-permutation pass.
 // Host-side partial results are combined in fixed rank order (allgather,
 // then summed on the host), so results are deterministic.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -139,13 +140,31 @@ static int plan_canonical_globals(int n, int nl, std::vector<int> &pos, std::vec
 // its rank bit g with rank r ^ 2^(g-nl) (whose half has the other top bit),
 // so afterwards the qubits at position g and nl-1 have traded places.
 //
-//  * multi-process world (one rank per process): ncclSend + ncclRecv of the
-//    contiguous S/2 half in one group, received into the scratch shard and
-//    copied back;
-//  * in-process group (qsim_create_group): the lower rank of each pair swaps
-//    the two halves directly with device-to-device copies (peer copies over
-//    NVLink when the members live on different GPUs), ordered against both
-//    members' streams with events.
+// Both transports move the half in chunks (QSIM_XCHG_CHUNK_KB, default
+// 64 MiB) on two streams so the steps overlap:
+//  * multi-process world (one rank per process): chunk c goes out and comes
+//    in with ncclSend + ncclRecv in one group on the handle's comm stream
+//    (into the scratch shard), and is copied into place on the compute stream
+//    as soon as its group completes -- while chunk c+1 is on the wire;
+//  * in-process group (qsim_create_group): the lower rank's stream parks its
+//    chunk in its scratch and pulls the partner's chunk (peer copies over
+//    NVLink between GPUs), the partner's stream writes the parked chunk into
+//    its own half, chunk by chunk, ordered by events.
+
+static uint64_t xchg_chunk_amps(uint64_t half)
+{
+    static const long kb = std::getenv("QSIM_XCHG_CHUNK_KB") ? std::atol(std::getenv("QSIM_XCHG_CHUNK_KB")) : 65536;
+    uint64_t c = (uint64_t)(kb > 0 ? kb : 65536) * 1024 / sizeof(double2);
+    if (c < 1) c = 1;
+    while (half / c > 64) c <<= 1;   // at most 64 chunks
+    return c < half ? c : half;
+}
+
+static int comm_stream(Handle *h)
+{
+    if (h->s_comm) return QSIM_OK;
+    return check_cuda(h, cudaStreamCreateWithFlags(&h->s_comm, cudaStreamNonBlocking), "comm stream");
+}
 
 static int exchange_nccl(Handle *h, int g)
 {
@@ -155,15 +174,31 @@ static int exchange_nccl(Handle *h, int g)
     const int b = (h->rank >> gb) & 1;
     const uint64_t half = h->local_dim() >> 1;
     if (int rc = ensure_scratch(h)) return rc;
+    if (int rc = comm_stream(h)) return rc;
     double2 *mine = h->psi + (uint64_t)(1 - b) * half;
+    const uint64_t ca = xchg_chunk_amps(half);
     prof_begin(h);
-    if (int rc = nccl_check(h, ncclGroupStart(), "ncclGroupStart")) return rc;
-    ncclSend(mine, half * 2, ncclDouble, partner, h->comm, h->stream);
-    ncclRecv(h->scratch, half * 2, ncclDouble, partner, h->comm, h->stream);
-    if (int rc = nccl_check(h, ncclGroupEnd(), "ncclGroupEnd")) return rc;
+    cudaEvent_t ready;
+    cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+    cudaEventRecord(ready, h->stream);
+    cudaStreamWaitEvent(h->s_comm, ready, 0);
+    cudaEventDestroy(ready);
+    for (uint64_t off = 0; off < half; off += ca) {
+        const uint64_t cnt = std::min<uint64_t>(ca, half - off);
+        if (int rc = nccl_check(h, ncclGroupStart(), "ncclGroupStart")) return rc;
+        ncclSend(mine + off, cnt * 2, ncclDouble, partner, h->comm, h->s_comm);
+        ncclRecv(h->scratch + off, cnt * 2, ncclDouble, partner, h->comm, h->s_comm);
+        if (int rc = nccl_check(h, ncclGroupEnd(), "ncclGroupEnd")) return rc;
+        cudaEvent_t done;
+        cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+        cudaEventRecord(done, h->s_comm);
+        cudaStreamWaitEvent(h->stream, done, 0);
+        cudaEventDestroy(done);
+        cudaError_t e = cudaMemcpyAsync(mine + off, h->scratch + off, cnt * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                        h->stream);
+        if (e != cudaSuccess) return check_cuda(h, e, "exchange copy");
+    }
     prof_end_comm(h, "nccl_pair_exchange", half * 32);
-    cudaError_t e = cudaMemcpyAsync(mine, h->scratch, half * sizeof(double2), cudaMemcpyDeviceToDevice, h->stream);
-    if (e != cudaSuccess) return check_cuda(h, e, "exchange copy");
     return QSIM_OK;
 #else
     (void)g;
@@ -176,17 +211,28 @@ static int alltoall_nccl(Handle *h, int k)
 #ifndef QSIM_NO_NCCL
     const uint64_t blk = h->local_dim() >> k;
     if (int rc = ensure_scratch(h)) return rc;
+    if (int rc = comm_stream(h)) return rc;
     prof_begin(h);
+    cudaEvent_t ready, done;
+    cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+    cudaEventRecord(ready, h->stream);
+    cudaStreamWaitEvent(h->s_comm, ready, 0);
     if (int rc = nccl_check(h, ncclGroupStart(), "ncclGroupStart")) return rc;
     for (int p = 0; p < h->world; ++p) {
         if (p == h->rank) continue;
-        ncclSend(h->psi + (uint64_t)p * blk, blk * 2, ncclDouble, p, h->comm, h->stream);
-        ncclRecv(h->scratch + (uint64_t)p * blk, blk * 2, ncclDouble, p, h->comm, h->stream);
+        ncclSend(h->psi + (uint64_t)p * blk, blk * 2, ncclDouble, p, h->comm, h->s_comm);
+        ncclRecv(h->scratch + (uint64_t)p * blk, blk * 2, ncclDouble, p, h->comm, h->s_comm);
     }
     if (int rc = nccl_check(h, ncclGroupEnd(), "ncclGroupEnd")) return rc;
-    prof_end_comm(h, "nccl_alltoall", (uint64_t)(h->world - 1) * blk * 32);
+    cudaEventRecord(done, h->s_comm);
+    // this rank's own block moves locally while the others are on the wire
     cudaError_t e = cudaMemcpyAsync(h->scratch + (uint64_t)h->rank * blk, h->psi + (uint64_t)h->rank * blk,
                                     blk * sizeof(double2), cudaMemcpyDeviceToDevice, h->stream);
+    cudaStreamWaitEvent(h->stream, done, 0);
+    cudaEventDestroy(ready);
+    cudaEventDestroy(done);
+    prof_end_comm(h, "nccl_alltoall", (uint64_t)(h->world - 1) * blk * 32);
     if (e != cudaSuccess) return check_cuda(h, e, "all-to-all copy");
     swap_buffers(h);
     return QSIM_OK;
@@ -235,26 +281,42 @@ static int alltoall_group(const Ranks &R, int k)
 
 static int exchange_pair(Handle *A, Handle *B, int g)
 {
+    (void)g;
     // A = lower rank (bit g = 0): its half with top bit 1 <-> B's half with top bit 0
     const uint64_t half = A->local_dim() >> 1;
     if (int rc = ensure_scratch(A)) return rc;
     double2 *ha = A->psi + half, *hb = B->psi;
+    const uint64_t ca = xchg_chunk_amps(half);
     // an event lives on its stream's device (the members may sit on different GPUs)
     cudaEvent_t eb, ea;
     cudaSetDevice(B->device);
     cudaEventCreateWithFlags(&eb, cudaEventDisableTiming);
     cudaEventRecord(eb, B->stream);
     cudaSetDevice(A->device);
-    cudaEventCreateWithFlags(&ea, cudaEventDisableTiming);
     cudaStreamWaitEvent(A->stream, eb, 0);
-    const size_t bytes = half * sizeof(double2);
-    cudaMemcpyAsync(A->scratch, ha, bytes, cudaMemcpyDefault, A->stream);
-    cudaMemcpyAsync(ha, hb, bytes, cudaMemcpyDefault, A->stream);
-    cudaMemcpyAsync(hb, A->scratch, bytes, cudaMemcpyDefault, A->stream);
-    cudaEventRecord(ea, A->stream);
-    cudaStreamWaitEvent(B->stream, ea, 0);
+    prof_begin(A);
+    for (uint64_t off = 0; off < half; off += ca) {
+        const size_t bytes = std::min<uint64_t>(ca, half - off) * sizeof(double2);
+        // A parks its chunk and pulls B's; B then writes the parked chunk into its half
+        cudaSetDevice(A->device);
+        cudaMemcpyAsync(A->scratch + off, ha + off, bytes, cudaMemcpyDefault, A->stream);
+        cudaMemcpyAsync(ha + off, hb + off, bytes, cudaMemcpyDefault, A->stream);
+        cudaEventCreateWithFlags(&ea, cudaEventDisableTiming);
+        cudaEventRecord(ea, A->stream);
+        cudaSetDevice(B->device);
+        cudaStreamWaitEvent(B->stream, ea, 0);
+        cudaMemcpyAsync(hb + off, A->scratch + off, bytes, cudaMemcpyDefault, B->stream);
+        cudaEventDestroy(ea);
+    }
+    // A's scratch is read by B's copies: A waits for them before reusing it
+    cudaSetDevice(B->device);
+    cudaEventRecord(eb, B->stream);
+    cudaSetDevice(A->device);
+    cudaStreamWaitEvent(A->stream, eb, 0);
+    prof_end_comm(A, "group_pair_exchange", half * 32);
+    cudaSetDevice(B->device);
     cudaEventDestroy(eb);
-    cudaEventDestroy(ea);
+    cudaSetDevice(A->device);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? QSIM_OK : check_cuda(A, e, "group exchange");
 }

@@ -105,13 +105,22 @@ __device__ __forceinline__ void cdense_rb(double2 (&v)[NS5], double2 u0, double2
 template <int B, int C>
 __device__ __forceinline__ void dense2_rb(double2 (&v)[NS5], const GOp &op)
 {
-    const double2 a0 = op.u[0], a1 = op.u[1], a2 = op.u[2], a3 = op.u[3];
-    const double2 b0 = op.u[4], b1 = op.u[5], b2 = op.u[6], b3 = op.u[7];
+    // the pairs with selector 0, then those with selector 1: one matrix live at a time
+    {
+        const double2 a0 = op.u[0], a1 = op.u[1], a2 = op.u[2], a3 = op.u[3];
 #pragma unroll
-    for (int k = 0; k < NS5; ++k) {
-        if (k & (1 << B)) continue;
-        const bool s = (k >> C) & 1;
-        pair_inplace(v[k], v[k | (1 << B)], s ? b0 : a0, s ? b1 : a1, s ? b2 : a2, s ? b3 : a3);
+        for (int k = 0; k < NS5; ++k) {
+            if ((k & (1 << B)) || ((k >> C) & 1)) continue;
+            pair_inplace(v[k], v[k | (1 << B)], a0, a1, a2, a3);
+        }
+    }
+    {
+        const double2 b0 = op.u[4], b1 = op.u[5], b2 = op.u[6], b3 = op.u[7];
+#pragma unroll
+        for (int k = 0; k < NS5; ++k) {
+            if ((k & (1 << B)) || !((k >> C) & 1)) continue;
+            pair_inplace(v[k], v[k | (1 << B)], b0, b1, b2, b3);
+        }
     }
 }
 
@@ -213,6 +222,34 @@ __device__ __forceinline__ void apply_op(double2 (&v)[NS5], const GOp &op, uint3
 #undef QS_CD
 #undef QS_D2
 
+// DENSE on window bit rb (case OPC_DENSE + rb) or DENSE2 (OPC_DENSE2 + rb * 5
+// + cs) with no control checks, trajectory table or run-time selector
+__device__ __forceinline__ void apply_dense_fast(double2 (&v)[NS5], const GOp &op, uint32_t c)
+{
+    if (c < OPC_DENSE + 5) {
+        const double2 u0 = op.u[0], u1 = op.u[1], u2 = op.u[2], u3 = op.u[3];
+        switch (c) {
+        case 0: dense_rb<0, false>(v, u0, u1, u2, u3, 0, 0); break;
+        case 1: dense_rb<1, false>(v, u0, u1, u2, u3, 0, 0); break;
+        case 2: dense_rb<2, false>(v, u0, u1, u2, u3, 0, 0); break;
+        case 3: dense_rb<3, false>(v, u0, u1, u2, u3, 0, 0); break;
+        default: dense_rb<4, false>(v, u0, u1, u2, u3, 0, 0); break;
+        }
+        return;
+    }
+    switch (c) {
+#define QS_F2(B, C) \
+    case OPC_DENSE2 + (B) * 5 + (C): dense2_rb<B, C>(v, op); break;
+        QS_F2(0, 1) QS_F2(0, 2) QS_F2(0, 3) QS_F2(0, 4)
+        QS_F2(1, 0) QS_F2(1, 2) QS_F2(1, 3) QS_F2(1, 4)
+        QS_F2(2, 0) QS_F2(2, 1) QS_F2(2, 3) QS_F2(2, 4)
+        QS_F2(3, 0) QS_F2(3, 1) QS_F2(3, 2) QS_F2(3, 4)
+        QS_F2(4, 0) QS_F2(4, 1) QS_F2(4, 2) QS_F2(4, 3)
+#undef QS_F2
+    default: break;
+    }
+}
+
 __device__ __forceinline__ uint32_t seg_thread_part(const OpsSeg &s, int tb, uint32_t tid)
 {
     uint32_t ti = 0;
@@ -281,7 +318,13 @@ __device__ __forceinline__ void run_segments(double2 (&v)[NS5], const OpsLaunch 
         for (int i = sg.op_begin; i < sg.op_end; ++i) {
             const uint32_t c = code;
             if (i + 1 < sg.op_end) code = OP[i + 1].code;
-            apply_op(v, OP[i], c, T, tpart, traj);
+            if (c < OPC_DENSE + 5 || (c >= OPC_DENSE2 && c < OPC_DIAGW)) {
+                // fast path (noisy circuits: almost every op): a dense 2x2, or a
+                // pair of them selected by a window bit, with no run-time checks
+                apply_dense_fast(v, OP[i], c);
+            } else {
+                apply_op(v, OP[i], c, T, tpart, traj);
+            }
         }
         prev_stp = stp;
 #pragma unroll

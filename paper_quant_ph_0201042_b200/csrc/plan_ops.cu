@@ -35,6 +35,8 @@
 #include <string>
 #include <vector>
 
+#include <cmath>
+
 #include "qsim_internal.h"
 
 namespace qs {
@@ -439,15 +441,21 @@ int flush_queue(Handle *h)
         rem.swap(left);
         // A pass of one sparse gate (controlled, or a phase on half the
         // amplitudes) reads and writes every amplitude; the unfused kernel
-        // touches only the amplitudes the gate changes -- worth it when the
-        // masked positions are >= 3 (runs of >= 128 B, so DRAM skips whole
-        // sectors).
+        // touches only the amplitudes the gate changes.  Measured on B200
+        // (ncu dram__bytes, profiles/r2_lowgates.md): DRAM reads move whole
+        // 128-byte lines (8 amplitudes), writes 32-byte sectors (2), so with
+        // the masked positions m the unfused kernel moves S 2^-|m >> 3| read +
+        // S 2^-|m >> 1| written against the pass's 2 S -- it wins below ~1.6 S
+        // (CR on positions (1,2): 1.08 vs 1.35 ms at n = 28; (2,3): 0.63 vs
+        // 1.36; a control on position 0 touches every sector: the pass).
         if (take.size() == 1 && !take[0].tab) {
             const QOp &q = take[0];
             uint64_t m = q.cmask;
             if (q.diag && q.tpos >= 0 && q.u[0].x == 1.0 && q.u[0].y == 0.0) m |= 1ull << q.tpos;
             if (q.diag && q.tpos < 0) m = q.cmask;
-            if (m && (m & 7ull) == 0) {
+            const double traffic = std::ldexp(1.0, -__builtin_popcountll(m >> 3)) +
+                                   std::ldexp(1.0, -__builtin_popcountll(m >> 1));
+            if (m && traffic <= 1.6) {
                 run_gate_unfused(h, q);
                 if (int rc = launch_check(h, "gate")) return rc;
                 continue;

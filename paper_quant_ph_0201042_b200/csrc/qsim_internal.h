@@ -289,6 +289,7 @@ struct Handle {
     // the copy streams (created on first use)
     double2 *stage[2] = {nullptr, nullptr};
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaStream_t s_comm = nullptr;   // shard-exchange stream (dist.cu), created on first use
     int strict = 0;              // qsim_set_strict: reject non-unitary matrices (QSIM_ENONUNITARY)
     // angle noise (R15)
     uint64_t noise_seed = 0;

@@ -152,3 +152,41 @@ def test_group_matches_single_gpu_bitwise_for_permutations(grp):
         cm = 1 << (5 - j)
         O.modmul(ref, 6, 8, cm, cm, c, 221)
     assert np.array_equal(get(h, n), ref)
+
+
+_CHUNK_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import oracle as O
+from paper_quant_ph_0201042_b200 import qsim as Q
+worst = 0.0
+for world in (2, 4, 8):
+    n = 16
+    rng = np.random.default_rng(world)
+    psi = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n); psi /= np.linalg.norm(psi)
+    h = Q.qsim_create_group(n, world)
+    Q.qsim_set_state(h, 0, psi)
+    ref = psi.copy()
+    Q.qsim_qft(h, 0, n, False); O.qft(ref, 0, n, False)
+    for _ in range(40):
+        q = int(rng.integers(n))
+        U = (rng.normal(size=(2, 2)) + 1j * rng.normal(size=(2, 2))) / 2
+        Q.qsim_apply_1q(h, q, U); O.apply_1q(ref, q, U)
+    Q.qsim_hadamard(h, 0, 5); O.hadamard_range(ref, 0, 5)
+    worst = max(worst, float(np.max(np.abs(Q.qsim_get_state(h, 0, 1 << n) - ref))))
+    Q.qsim_destroy(h)
+print("WORST", worst)
+assert worst < 1e-10, worst
+"""
+
+
+def test_group_exchanges_in_many_chunks():
+    """Shard exchanges pipelined in 4 KiB chunks (QSIM_XCHG_CHUNK_KB): the
+    chunked transport (two streams, per-chunk events) gives the oracle's state."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _CHUNK_SCRIPT, root], env=dict(os.environ, QSIM_XCHG_CHUNK_KB="4"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr

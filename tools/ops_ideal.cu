@@ -1,0 +1,138 @@
+// tools/ops_ideal.cu -- measurement only: FP64 efficiency of dense 2x2 pair
+// updates on 32 register-resident amplitudes per thread, 8 warps per SM,
+// without the gate-list interpreter (op = dense 2x2 on window bit i % 5,
+// matrices from shared memory): the ceiling the k_ops_* kernels can reach.
+// VAR 0: plain C pair update; VAR 1: 4-way split accumulation (shallower chains)
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+struct Op { double2 u[4]; };
+
+template <int B, int VAR>
+__device__ __forceinline__ void dense(double2 (&v)[32], const double2 u0, const double2 u1, const double2 u2, const double2 u3)
+{
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+        if (k & (1 << B)) continue;
+        const double2 x = v[k], y = v[k | (1 << B)];
+        if (VAR == 0) {
+            v[k] = make_double2(fma(u0.x, x.x, fma(-u0.y, x.y, fma(u1.x, y.x, -u1.y * y.y))),
+                                fma(u0.x, x.y, fma(u0.y, x.x, fma(u1.x, y.y, u1.y * y.x))));
+            v[k | (1 << B)] = make_double2(fma(u2.x, x.x, fma(-u2.y, x.y, fma(u3.x, y.x, -u3.y * y.y))),
+                                           fma(u2.x, x.y, fma(u2.y, x.x, fma(u3.x, y.y, u3.y * y.x))));
+        } else {
+            const double a = fma(u0.x, x.x, -u0.y * x.y), b = fma(u1.x, y.x, -u1.y * y.y);
+            const double c = fma(u0.x, x.y, u0.y * x.x), d = fma(u1.x, y.y, u1.y * y.x);
+            const double e = fma(u2.x, x.x, -u2.y * x.y), f = fma(u3.x, y.x, -u3.y * y.y);
+            const double g = fma(u2.x, x.y, u2.y * x.x), hh = fma(u3.x, y.y, u3.y * y.x);
+            v[k] = make_double2(a + b, c + d);
+            v[k | (1 << B)] = make_double2(e + f, g + hh);
+        }
+    }
+}
+
+// 16 amplitudes per thread, 512 threads (16 warps per SM)
+template <int B>
+__device__ __forceinline__ void dense16(double2 (&v)[16], const double2 u0, const double2 u1, const double2 u2, const double2 u3)
+{
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        if (k & (1 << B)) continue;
+        const double2 x = v[k], y = v[k | (1 << B)];
+        v[k] = make_double2(fma(u0.x, x.x, fma(-u0.y, x.y, fma(u1.x, y.x, -u1.y * y.y))),
+                            fma(u0.x, x.y, fma(u0.y, x.x, fma(u1.x, y.y, u1.y * y.x))));
+        v[k | (1 << B)] = make_double2(fma(u2.x, x.x, fma(-u2.y, x.y, fma(u3.x, y.x, -u3.y * y.y))),
+                                       fma(u2.x, x.y, fma(u2.y, x.x, fma(u3.x, y.y, u3.y * y.x))));
+    }
+}
+
+__global__ void __launch_bounds__(512, 1) k_ideal16(double2 *psi, const Op *ops_g, int nops, uint64_t ntiles)
+{
+    __shared__ Op ops[64];
+    for (int i = threadIdx.x; i < nops; i += blockDim.x) ops[i] = ops_g[i];
+    __syncthreads();
+    for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x) {
+        double2 v[16];
+        double2 *base = psi + T * 8192 + threadIdx.x;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = base[512 * k];
+        for (int i = 0; i < nops; ++i) {
+            const double2 u0 = ops[i].u[0], u1 = ops[i].u[1], u2 = ops[i].u[2], u3 = ops[i].u[3];
+            switch (i % 4) {
+            case 0: dense16<0>(v, u0, u1, u2, u3); break;
+            case 1: dense16<1>(v, u0, u1, u2, u3); break;
+            case 2: dense16<2>(v, u0, u1, u2, u3); break;
+            default: dense16<3>(v, u0, u1, u2, u3); break;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) base[512 * k] = v[k];
+    }
+}
+
+template <int VAR>
+__global__ void __launch_bounds__(256, 1) k_ideal(double2 *psi, const Op *ops_g, int nops, uint64_t ntiles)
+{
+    __shared__ Op ops[64];
+    for (int i = threadIdx.x; i < nops; i += blockDim.x) ops[i] = ops_g[i];
+    __syncthreads();
+    for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x) {
+        double2 v[32];
+        double2 *base = psi + T * 8192 + threadIdx.x;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) v[k] = base[256 * k];
+        for (int i = 0; i < nops; ++i) {
+            const double2 u0 = ops[i].u[0], u1 = ops[i].u[1], u2 = ops[i].u[2], u3 = ops[i].u[3];
+            switch (i % 5) {
+            case 0: dense<0, VAR>(v, u0, u1, u2, u3); break;
+            case 1: dense<1, VAR>(v, u0, u1, u2, u3); break;
+            case 2: dense<2, VAR>(v, u0, u1, u2, u3); break;
+            case 3: dense<3, VAR>(v, u0, u1, u2, u3); break;
+            default: dense<4, VAR>(v, u0, u1, u2, u3); break;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 32; ++k) base[256 * k] = v[k];
+    }
+}
+
+int main()
+{
+    const int n = 28, nops = 26;
+    const uint64_t N = 1ull << n;
+    double2 *psi;
+    Op *ops;
+    cudaMalloc(&psi, N * 16);
+    cudaMemset(psi, 0, N * 16);
+    cudaMalloc(&ops, 64 * sizeof(Op));
+    Op h[64];
+    for (int i = 0; i < 64; ++i)
+        for (int k = 0; k < 4; ++k) h[i].u[k] = make_double2(0.5 + 0.01 * k, 0.25 - 0.01 * i);
+    cudaMemcpy(ops, h, sizeof h, cudaMemcpyHostToDevice);
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    for (int var = 0; var < 3; ++var) {
+        auto go = [&]() {
+            if (var == 0) k_ideal<0><<<sms, 256>>>(psi, ops, nops, N >> 13);
+            else if (var == 1) k_ideal<1><<<sms, 256>>>(psi, ops, nops, N >> 13);
+            else k_ideal16<<<sms, 512>>>(psi, ops, nops, N >> 13);
+        };
+        go();
+        cudaEventRecord(a);
+        for (int r = 0; r < 3; ++r) go();
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        ms /= 3;
+        const double instr = (double)nops * 16 * (N / 2);   // FP64 instructions (16 per pair)
+        printf("{\"var\": %d, \"ms\": %.3f, \"fp64_instr_per_s\": %.4e, \"frac_of_64_per_clk_at_1965\": %.3f, \"err\": \"%s\"}\n",
+               var, ms, instr / (ms * 1e-3), instr / (ms * 1e-3) / (sms * 64.0 * 1.965e9),
+               cudaGetErrorString(cudaGetLastError()));
+    }
+    return 0;
+}
