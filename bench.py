@@ -191,6 +191,98 @@ def run_reference(args):
     return 0
 
 
+def cfg4_gate_bytes(n, layers=20):
+    """Per-gate model of configs[4]: a Haar gate 2^(n+5) B, a noisy CNOT (a
+    controlled dense 2x2, one control) 2^(n+4) B."""
+    cnots = sum(len(range(l & 1, n - 1, 2)) for l in range(layers))
+    return layers * n * (1 << (n + 5)) + cnots * (1 << (n + 4)), layers * n + cnots
+
+
+def run_config4(args):
+    """configs[4] (BASELINE.json): the noisy Haar + CNOT brickwork, n = 32,
+    20 layers, sigma = 1e-3, p = 1e-4, seed 5, on one GPU; one step = the
+    whole circuit from |0...0> (qsim_set_basis) to the read-out of the norm.
+    The gate-list passes are FP64-bound, so the roofline object is the FP64
+    pipe of the dominant kernel: algorithmic FP64 instructions per launch
+    (16 per amplitude pair of a dense 2x2, the library's count) over its launch
+    time, against 148 SMs x 64 FP64 FMA/clk x the max SM clock."""
+    import torch
+    from paper_quant_ph_0201042_b200 import qsim as Q
+    from paper_quant_ph_0201042_b200 import workloads as W
+    n = args.n if args.n != N_QUBITS else 32
+    layers = 20
+    torch.cuda.set_device(0)
+    h = Q.qsim_create(n)
+    stream = torch.cuda.ExternalStream(Q.qsim_get_stream(h))
+    events = []
+
+    def step():
+        nonlocal events
+        events = W.run_cfg4(h, n=n, layers=layers, seed=5, sigma=1e-3, p=1e-4)
+
+    for _ in range(args.warmup):
+        step()
+    Q.qsim_sync(h)
+    sampler = ClockSampler(0)
+    sampler.start()
+    time.sleep(0.3)
+    l0 = Q.qsim_launch_count(h)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    Q.qsim_sync(h)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = Q.qsim_launch_count(h) - l0
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    # end to end: the same step with its result (the norm and the event list) read back
+    t0 = time.perf_counter()
+    for _ in range(2):
+        step()
+        nrm = Q.qsim_norm(h)
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / 2
+    Q.qsim_profile(h, True)
+    step()
+    prof = Q.qsim_profile_json(h)
+    prof.pop("_launches", None)
+    Q.qsim_profile(h, False)
+    gb, ngates = cfg4_gate_bytes(n, layers)
+    value = gb / (ms * 1e-3) / 1e9
+    peak_hbm, peak_kind, sm_max = load_peaks()
+    dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    fp64_peak = 148 * 64 * sm_max * 1e6          # FP64 FMA-class instructions per second (lanes)
+    ach = dom["fp64"] / (dom["ms"] * 1e-3)
+    roof = {"bound": "fp64", "kernel": dom_name, "achieved": ach / 1e12, "peak": fp64_peak / 1e12,
+            "unit": "T FP64 instr/s", "frac": ach / fp64_peak, "traffic": None,
+            "peak_source": "148 SMs x 64 FP64 FMA/clk x sm_max_mhz (B200_PROFILING.md units; tools/microbench.cu "
+                           "measured 58.4/clk/SM)",
+            "fp64_per_launch": dom["fp64"] / dom["launches"], "ms_per_launch": dom["ms"] / dom["launches"],
+            "launches_per_step": dom["launches"], "share_of_step": dom["ms"] / ms,
+            "hbm_gbs_of_kernel": dom["bytes"] / (dom["ms"] * 1e-3) / 1e9}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Haar + noisy-CNOT brickwork, DESIGN.md R18)",
+        "config": {"workload": f"configs[4]: noisy random circuit n={n}, 20 layers, sigma=1e-3, p=1e-4, seed 5",
+                   "n": n, "gates": ngates, "gate_bytes": gb, "state_bytes": 16 << n, "parallelism": "sv-shard1",
+                   "l2": f"inputs larger than L2 ({16 << n >> 30} GiB state)", "circuit_ms": ms,
+                   "events_last_step": len(events), "norm_after": nrm},
+        "roofline": roof,
+        "cpu_baseline": None,
+        "e2e": {"value": gb / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms, "h2d_bytes_per_step":
+                ngates * 64, "d2h_bytes_per_step": 8 + 24 * len(events),
+                "how": "run_cfg4 (gate matrices to the device as call parameters) + qsim_norm read-back"},
+        "gpu_launches": launches, "clocks": clocks,
+        "kernels": prof,
+    }
+    print(json.dumps(line), flush=True)
+    Q.qsim_destroy(h)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -203,9 +295,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--profile-only", action="store_true", help="warm-up + steps only (for ncu)")
+    ap.add_argument("--config", type=int, default=2, choices=[2, 4],
+                    help="2: the headline QFT (default); 4: the noisy brickwork, FP64 roofline (one GPU)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == 4:
+        return run_config4(args)
 
     import numpy as np
     import torch

@@ -110,8 +110,9 @@ void prof_end_comm(Handle *h, const char *name, uint64_t bytes)
     if (!h->prof_on || !h->pending) return;
     cudaEvent_t b = pool_event(h);
     cudaEventRecord(b, h->stream);
-    h->prof.push_back({name, bytes, h->pending, b});
+    h->prof.push_back({name, bytes, h->pending, b, h->prof_fp64});
     h->pending = nullptr;
+    h->prof_fp64 = 0;
 }
 
 void prof_end(Handle *h, const char *name, uint64_t bytes)
@@ -962,7 +963,7 @@ const char *qsim_profile_json(qsim_t *h)
     Handle *m = ranks_of(h)[0];
     flush_queue(m);
     cudaStreamSynchronize(m->stream);
-    struct Agg { double ms = 0; uint64_t bytes = 0, n = 0; };
+    struct Agg { double ms = 0; uint64_t bytes = 0, n = 0, fp64 = 0; };
     std::vector<std::pair<std::string, Agg>> agg;
     for (const auto &r : m->prof) {
         float ms = 0.f;
@@ -973,6 +974,7 @@ const char *qsim_profile_json(qsim_t *h)
         agg[k].second.ms += ms;
         agg[k].second.bytes += r.bytes;
         agg[k].second.n += 1;
+        agg[k].second.fp64 += r.fp64;
     }
     std::string js = "{\"_launches\": [";
     char buf[256];
@@ -984,9 +986,9 @@ const char *qsim_profile_json(qsim_t *h)
     }
     js += "]";
     for (size_t k = 0; k < agg.size(); ++k) {
-        std::snprintf(buf, sizeof buf, ", \"%s\": {\"launches\": %llu, \"ms\": %.6f, \"bytes\": %llu}",
+        std::snprintf(buf, sizeof buf, ", \"%s\": {\"launches\": %llu, \"ms\": %.6f, \"bytes\": %llu, \"fp64\": %llu}",
                       agg[k].first.c_str(), (unsigned long long)agg[k].second.n, agg[k].second.ms,
-                      (unsigned long long)agg[k].second.bytes);
+                      (unsigned long long)agg[k].second.bytes, (unsigned long long)agg[k].second.fp64);
         js += buf;
     }
     js += "}";

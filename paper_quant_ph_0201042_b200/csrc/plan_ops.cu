@@ -447,7 +447,8 @@ int flush_queue(Handle *h)
         // the masked positions m the unfused kernel moves S 2^-|m >> 3| read +
         // S 2^-|m >> 1| written against the pass's 2 S -- it wins below ~1.6 S
         // (CR on positions (1,2): 1.08 vs 1.35 ms at n = 28; (2,3): 0.63 vs
-        // 1.36; a control on position 0 touches every sector: the pass).
+        // 1.36; position 0 in the mask touches every line and half the sectors or
+        // more: the pass, measured no slower).
         if (take.size() == 1 && !take[0].tab) {
             const QOp &q = take[0];
             uint64_t m = q.cmask;
@@ -455,7 +456,7 @@ int flush_queue(Handle *h)
             if (q.diag && q.tpos < 0) m = q.cmask;
             const double traffic = std::ldexp(1.0, -__builtin_popcountll(m >> 3)) +
                                    std::ldexp(1.0, -__builtin_popcountll(m >> 1));
-            if (m && traffic <= 1.6) {
+            if (m && !(m & 1) && traffic <= 1.6) {
                 run_gate_unfused(h, q);
                 if (int rc = launch_check(h, "gate")) return rc;
                 continue;
@@ -673,6 +674,7 @@ int flush_queue(Handle *h)
                              cnt[GOP_DIAGW], cnt[GOP_DIAGT], cnt[GOP_DIAGF], cnt[GOP_PHASE], cnt[GOP_DENSET], thr,
                              tps.c_str());
             }
+            prof_set_fp64(h, ops_fp64(L));
             launch_ops_pass(h, L);
             if (int rc = launch_check(h, "fused gate pass")) return rc;
             pi = pe;
@@ -680,6 +682,26 @@ int flush_queue(Handle *h)
     }
     h->tabs_used = 0;   // every queued table is consumed by the launches above (stream order)
     return QSIM_OK;
+}
+
+uint64_t ops_fp64(const OpsLaunch &L)
+{
+    const OpsPass &P = L.P;
+    const double amps = std::ldexp(1.0, P.tbits + P.nfix);
+    double per_amp = 0.0;
+    for (int i = 0; i < P.nops; ++i) {
+        const GOp &g = L.ops[i];
+        double c;
+        switch (g.kind) {
+        case GOP_DENSE: case GOP_DENSE2: case GOP_DENSET: c = 8.0; break;
+        case GOP_CDENSE: c = 4.0; break;
+        case GOP_DIAGW: c = (g.u[0].x == 1.0 && g.u[0].y == 0.0) ? 2.0 : 4.0; break;
+        default: c = 4.0; break;
+        }
+        c = std::ldexp(c, -__builtin_popcountll(g.fm) - __builtin_popcount(g.tm) - __builtin_popcount(g.wm));
+        per_amp += c;
+    }
+    return (uint64_t)(per_amp * amps);
 }
 
 }  // namespace qs

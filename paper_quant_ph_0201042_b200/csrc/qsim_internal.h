@@ -305,7 +305,8 @@ struct Handle {
     int num_sms = 148;
     // profiling
     int prof_on = 0;
-    struct ProfRec { const char *name; uint64_t bytes; cudaEvent_t a, b; };
+    struct ProfRec { const char *name; uint64_t bytes; cudaEvent_t a, b; uint64_t fp64; };
+    uint64_t prof_fp64 = 0;   // algorithmic FP64 instructions of the next launch (prof_set_fp64)
     std::vector<ProfRec> prof;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
@@ -348,6 +349,14 @@ inline bool first_use_on_device(uint64_t &mask)
 // enabled; prof_end also counts the launch.
 void prof_begin(Handle *h);
 void prof_end(Handle *h, const char *name, uint64_t bytes);
+// the algorithmic FP64 instructions (FMA / MUL / ADD, one per lane) of the
+// next launch, for FP64-bound kernels' roofline (qsim_profile_json "fp64")
+inline void prof_set_fp64(Handle *h, uint64_t n) { h->prof_fp64 = n; }
+struct OpsLaunch;
+// FP64 instructions of a gate-list pass: 16 per amplitude pair of a dense
+// 2x2 (8 per amplitude), 4 per amplitude a phase multiplies, scaled by the
+// fraction of amplitudes each op's controls select
+uint64_t ops_fp64(const OpsLaunch &L);
 void prof_end_comm(Handle *h, const char *name, uint64_t bytes);   // exchanges: bytes sent + received
 
 // error helpers
