@@ -217,8 +217,11 @@ def run_config4(args):
     events = []
 
     def step():
+        # the whole circuit, executed: gates still queued at the end (the last
+        # layer's) would otherwise be dropped by the next step's qsim_set_basis
         nonlocal events
         events = W.run_cfg4(h, n=n, layers=layers, seed=5, sigma=1e-3, p=1e-4)
+        Q.qsim_sync(h)
 
     for _ in range(args.warmup):
         step()

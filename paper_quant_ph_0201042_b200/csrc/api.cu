@@ -110,18 +110,19 @@ void prof_end_comm(Handle *h, const char *name, uint64_t bytes)
     if (!h->prof_on || !h->pending) return;
     cudaEvent_t b = pool_event(h);
     cudaEventRecord(b, h->stream);
-    h->prof.push_back({name, bytes, h->pending, b, h->prof_fp64});
+    h->prof.push_back({name, bytes, h->pending, b, 0});
     h->pending = nullptr;
-    h->prof_fp64 = 0;
 }
 
 void prof_end(Handle *h, const char *name, uint64_t bytes)
 {
     h->launches++;
+    const uint64_t fp64 = h->prof_fp64;
+    h->prof_fp64 = 0;
     if (!h->prof_on || !h->pending) return;
     cudaEvent_t b = pool_event(h);
     cudaEventRecord(b, h->stream);
-    h->prof.push_back({name, bytes, h->pending, b});
+    h->prof.push_back({name, bytes, h->pending, b, fp64});
     h->pending = nullptr;
 }
 
