@@ -322,12 +322,16 @@ def main():
     from paper_quant_ph_0201042_b200 import workloads as W
 
     n = args.n
+    # --gpus N without torchrun: one process drives N ranks (qsim_create(n, N),
+    # the in-process rank group; ranks share devices when fewer are visible)
+    group = world == 1 and args.gpus > 1
+    ranks = args.gpus if group else world
     if world > 1:
         uid = [Q.qsim_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         h = Q.qsim_create_dist(n, world, rank, local, uid[0])
     else:
-        h = Q.qsim_create(n)
+        h = Q.qsim_create(n, ranks)
     stream = torch.cuda.ExternalStream(Q.qsim_get_stream(h))
 
     def barrier():
@@ -387,12 +391,13 @@ def main():
     peak, peak_kind, _ = load_peaks()
 
     # dominant kernel roofline (algorithmic bytes per launch / mean launch time)
-    ours = {k: v for k, v in prof.items() if not k.startswith("nccl_")}
+    is_comm = lambda k: k.startswith("nccl_") or k.startswith("group_")
+    ours = {k: v for k, v in prof.items() if not is_comm(k)}
     # the whole circuit's real HBM traffic: the algorithmic bytes of every launch
     pass_bytes = sum(v["bytes"] for v in ours.values()) / args.steps
-    hbm_ach = pass_bytes / (ms * 1e-3) / 1e9 / world
+    hbm_ach = pass_bytes / (ms * 1e-3) / 1e9   # per GPU: the profile covers rank 0 (its shard)
     passes = sum(v["launches"] for k, v in ours.items() if k.startswith("k_qft")) / args.steps
-    comm = {k: v for k, v in prof.items() if k.startswith("nccl_")}
+    comm = {k: v for k, v in prof.items() if is_comm(k)}
     dom = max(ours.items(), key=lambda kv: kv[1]["ms"]) if ours else None
     roof = None
     if dom:
@@ -429,13 +434,13 @@ def main():
     # qsim_qft_host_stream pipelines the steps (copy in of step i+1 and copy
     # out of step i-1 overlap the transform of step i); every step still moves
     # its whole input in and its whole result out over PCIe inside the timed call.
-    shard = 1 << (n - (world.bit_length() - 1))
+    shard = 1 << (n - (world.bit_length() - 1))   # this process's slice (the whole state for a group)
     host_in = torch.empty(shard, dtype=torch.complex128, pin_memory=True).numpy()
     host_out = torch.empty(shard, dtype=torch.complex128, pin_memory=True).numpy()
     Q.qsim_get_state(h, rank * shard, shard, host_in)
     barrier()
     torch.cuda.synchronize()
-    if world == 1:
+    if world == 1 and not group:
         Q.qsim_qft_host_stream(h, 0, n, False, host_in, host_out, 1, 0, 0)   # warm the stages
         t0 = time.perf_counter()
         Q.qsim_qft_host_stream(h, 0, n, False, host_in, host_out, args.e2e_steps, 0, 0)
@@ -459,17 +464,20 @@ def main():
            "how": e2e_how, "steps": args.e2e_steps}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not group and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.cpu_n)
 
     if rank == 0:
         line = {
             "metric": METRIC,
-            "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "value": value, "unit": UNIT, "n_gpus": ranks, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded complex Gaussian, DESIGN.md R19)",
             "config": {"workload": WORKLOAD, "n": n, "gates": ngates, "gate_bytes": gb,
-                       "state_bytes": 16 << n, "parallelism": f"sv-shard{world}",
+                       "state_bytes": 16 << n,
+                       "parallelism": (f"sv-shard{ranks} (one process, rank group over "
+                                       f"{torch.cuda.device_count()} visible device(s))" if group
+                                       else f"sv-shard{world}"),
                        "l2": "inputs larger than L2 (4 GiB state vs 126 MB L2)",
                        "circuit_ms": ms, "effective_frac_of_hbm_peak": value / peak,
                        "hbm_gbs_achieved": hbm_ach, "hbm_frac_achieved": hbm_ach / peak,

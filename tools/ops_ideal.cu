@@ -97,6 +97,62 @@ __global__ void __launch_bounds__(256, 1) k_ideal(double2 *psi, const Op *ops_g,
     }
 }
 
+
+// DENSE2-like op: two matrices selected by window bit C
+template <int B, int C>
+__device__ __forceinline__ void dense2(double2 (&v)[32], const double2 *u)
+{
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+        if (k & (1 << B)) continue;
+        const double2 *m = ((k >> C) & 1) ? u + 4 : u;
+        const double2 u0 = m[0], u1 = m[1], u2 = m[2], u3 = m[3];
+        const double2 x = v[k], y = v[k | (1 << B)];
+        v[k] = make_double2(fma(u0.x, x.x, fma(-u0.y, x.y, fma(u1.x, y.x, -u1.y * y.y))),
+                            fma(u0.x, x.y, fma(u0.y, x.x, fma(u1.x, y.y, u1.y * y.x))));
+        v[k | (1 << B)] = make_double2(fma(u2.x, x.x, fma(-u2.y, x.y, fma(u3.x, y.x, -u3.y * y.y))),
+                                       fma(u2.x, x.y, fma(u2.y, x.x, fma(u3.x, y.y, u3.y * y.x))));
+    }
+}
+
+struct Op8 { double2 u[8]; };
+
+// TR: a shared-memory transpose (write all 32, barrier, read back permuted) every 7 ops
+template <bool TR>
+__global__ void __launch_bounds__(256, 1) k_ideal2(double2 *psi, const Op8 *ops_g, int nops, uint64_t ntiles)
+{
+    extern __shared__ double2 sh[];
+    Op8 *ops = reinterpret_cast<Op8 *>(sh + 8192);
+    for (int i = threadIdx.x; i < nops; i += blockDim.x) ops[i] = ops_g[i];
+    __syncthreads();
+    for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x) {
+        double2 v[32];
+        double2 *base = psi + T * 8192 + threadIdx.x;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) v[k] = base[256 * k];
+        for (int i = 0; i < nops; ++i) {
+            const double2 *u = ops[i].u;
+            switch (i % 5) {
+            case 0: dense2<0, 1>(v, u); break;
+            case 1: dense2<1, 2>(v, u); break;
+            case 2: dense2<2, 3>(v, u); break;
+            case 3: dense2<3, 4>(v, u); break;
+            default: dense2<4, 0>(v, u); break;
+            }
+            if (TR && (i % 7) == 6) {
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < 32; ++k) sh[(threadIdx.x * 32 + k) ^ (threadIdx.x & 7)] = v[k];
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < 32; ++k) v[k] = sh[(threadIdx.x * 32 + k) ^ (threadIdx.x & 7)];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 32; ++k) base[256 * k] = v[k];
+    }
+}
+
 int main()
 {
     const int n = 28, nops = 26;
@@ -133,6 +189,35 @@ int main()
         printf("{\"var\": %d, \"ms\": %.3f, \"fp64_instr_per_s\": %.4e, \"frac_of_64_per_clk_at_1965\": %.3f, \"err\": \"%s\"}\n",
                var, ms, instr / (ms * 1e-3), instr / (ms * 1e-3) / (sms * 64.0 * 1.965e9),
                cudaGetErrorString(cudaGetLastError()));
+    }
+    {
+        Op8 *ops8;
+        cudaMalloc(&ops8, 64 * sizeof(Op8));
+        Op8 h8[64];
+        for (int i = 0; i < 64; ++i)
+            for (int k = 0; k < 8; ++k) h8[i].u[k] = make_double2(0.5 + 0.01 * k, 0.25 - 0.01 * i);
+        cudaMemcpy(ops8, h8, sizeof h8, cudaMemcpyHostToDevice);
+        const size_t sm = 8192 * 16 + 64 * sizeof(Op8);
+        cudaFuncSetAttribute(k_ideal2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(k_ideal2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        for (int tr = 0; tr < 2; ++tr) {
+            auto go = [&]() {
+                if (tr) k_ideal2<true><<<sms, 256, sm>>>(psi, ops8, nops, N >> 13);
+                else k_ideal2<false><<<sms, 256, sm>>>(psi, ops8, nops, N >> 13);
+            };
+            go();
+            cudaEventRecord(a);
+            for (int r = 0; r < 3; ++r) go();
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms;
+            cudaEventElapsedTime(&ms, a, b);
+            ms /= 3;
+            const double instr = (double)nops * 16 * (N / 2);
+            printf("{\"var\": \"dense2%s\", \"ms\": %.3f, \"frac_of_64_per_clk_at_1965\": %.3f, \"err\": \"%s\"}\n",
+                   tr ? "+transpose" : "", ms, instr / (ms * 1e-3) / (sms * 64.0 * 1.965e9),
+                   cudaGetErrorString(cudaGetLastError()));
+        }
     }
     return 0;
 }
