@@ -424,7 +424,10 @@ def main():
         cms = sum(v["ms"] for v in comm.values())
         if cms > 0:
             ach = cb / 2 / (cms * 1e-3) / 1e9
+            shared = group and torch.cuda.device_count() < ranks
             nvlink = {"bound": "nvlink", "achieved": ach, "peak": 770.0, "unit": "GB/s per direction",
+                      "note": ("ranks share one device: device-local copies, not NVLink" if shared else
+                               "rank 0's exchanges"),
                       "frac": ach / 770.0, "peak_source": "B200_PROFILING.md measured peer copy (900 nominal)",
                       "bytes_per_step": cb / args.steps, "ms_per_step": cms / args.steps,
                       "share_of_step": cms / (ms * args.steps),

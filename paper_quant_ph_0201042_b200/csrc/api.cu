@@ -1274,7 +1274,7 @@ int qsim_hadamard(qsim_t *h, int lo, int m)
     if (lo < 0 || m < 0 || lo + m > h->n) return fail(h, QSIM_ERANGE, "range outside [0, n)");
     if (m == 0) return QSIM_OK;
     const Ranks R = ranks_of(h);
-    if (h->nl >= 9 && m <= h->nl) return lift(h, R, fused_range(R, lo, m, 0, 0));
+    if (h->nl >= 9 && (m <= h->nl || h->nl >= 12)) return lift(h, R, fused_range(R, lo, m, 0, 0));
     const double r = M_SQRT1_2;
     double2 H[4] = {make_double2(r, 0), make_double2(r, 0), make_double2(r, 0), make_double2(-r, 0)};
     for (int q = lo; q < lo + m; ++q)
@@ -1411,7 +1411,7 @@ int qsim_qft(qsim_t *h, int lo, int m, int inverse)
     if (lo < 0 || m < 0 || lo + m > h->n) return fail(h, QSIM_ERANGE, "range outside [0, n)");
     if (m == 0) return QSIM_OK;
     const Ranks R = ranks_of(h);
-    if (h->sigma == 0.0 && h->fuse && h->nl >= 9 && m <= h->nl) {
+    if (h->sigma == 0.0 && h->fuse && h->nl >= 9 && (m <= h->nl || h->nl >= 12)) {
         // noiseless: fused passes (constant gates, R25)
         h->gcount += (uint64_t)m + (uint64_t)m * (m - 1) / 2;
         return lift(h, R, fused_range(R, lo, m, 1, inverse));
@@ -1531,7 +1531,7 @@ int qsim_fft(qsim_t *h, int lo, int m, int inverse)
     if (lo < 0 || m < 0 || lo + m > h->n) return fail(h, QSIM_ERANGE, "range outside [0, n)");
     if (m == 0) return QSIM_OK;
     const Ranks R = ranks_of(h);
-    if (h->nl >= 9 && m <= h->nl) return lift(h, R, fused_range(R, lo, m, 1, inverse));
+    if (h->nl >= 9 && (m <= h->nl || h->nl >= 12)) return lift(h, R, fused_range(R, lo, m, 1, inverse));
     return qft_gates(h, R, lo, m, m, inverse, false);   // tiny registers: constant gates, not counted
 }
 
