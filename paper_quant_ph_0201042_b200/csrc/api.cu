@@ -415,6 +415,119 @@ struct GenCircuit {
 
 constexpr int kGenInfeasible = 1000;   // dry run: a pass the generalised kernel cannot take
 
+// One fused QFT / H block of an in-process rank group whose wires gw (block
+// indices, 1 or 2 of them) sit on rank bits: k_qft13 in rank-group mode on
+// every member -- each takes the tiles whose split bits equal its own rank
+// bits, lands the tile's rows from the 2^ng shards that hold them (peer
+// memory over NVLink between GPUs) and stores every amplitude back in place
+// into the shard its global bits name.  The paper's pairing rule (rows R_j
+// and R_{2^P+j} meet on one processor) is met inside the
+// tile instead of by moving half of each shard first.  Returns 1 (nothing
+// launched) when the geometry does not fit.
+int rank_group_pass(const Ranks &R, const std::vector<int> &wp, int a0, int a, const std::vector<int> &gw, int qft,
+                    int inverse)
+{
+    Handle *h0 = R[0];
+    const int nl = h0->nl, ng = (int)gw.size();
+    // tile: block wires (tile bits 0..a-1) + the lowest 13 - a local positions
+    std::vector<int> tpos;
+    std::vector<char> in_t(nl, 0);
+    for (int u = 0; u < a; ++u) {
+        const int p = wp[a0 + u];
+        tpos.push_back(p);
+        if (p < nl) in_t[p] = 1;
+    }
+    for (int p = 0; p < nl && (int)tpos.size() < kTile13Bits; ++p)
+        if (!in_t[p]) { tpos.push_back(p); in_t[p] = 1; }
+    if ((int)tpos.size() != kTile13Bits) return 1;
+    std::vector<int> gbits(gw);
+    std::sort(gbits.begin(), gbits.end(), [&](int x, int y) { return wp[a0 + x] < wp[a0 + y]; });
+    std::vector<Qft13Desc> ds(R.size());
+    for (size_t r = 0; r < R.size(); ++r) {
+        Handle *h = R[r];
+        Qft13Desc &d = ds[r];
+        std::memset(&d, 0, sizeof d);
+        d.a = a;
+        for (int b = 0; b < kTile13Bits; ++b) {
+            d.in_pos[b] = tpos[b];
+            d.out_pos[b] = tpos[b] < nl ? tpos[b] : -1;
+        }
+        for (int p = 0; p < nl; ++p)
+            if (!in_t[p]) {
+                d.fin_pos[d.nfix] = p;
+                d.fout_pos[d.nfix] = p;
+                d.nfix++;
+            }
+        if (d.nfix < ng) return 1;
+        d.W = a0 + a;
+        d.inverse = inverse;
+        d.hadamard_only = !qft;
+        d.scale = std::ldexp(1.0, -(a / 2));
+        if (a & 1) d.scale *= M_SQRT1_2;
+        if (qft) {
+            for (int i = 0; i < a0; ++i) {
+                const int p = wp[i];
+                if (p >= nl) { d.y_const += (uint64_t)((h->rank >> (p - nl)) & 1) << i; continue; }
+                int b = -1;
+                for (int t = 0; t < kTile13Bits; ++t) if (d.in_pos[t] == p) b = t;
+                if (b >= 0) { d.et_bit[d.n_et] = b; d.et_w[d.n_et] = i; d.n_et++; }
+                else {
+                    int f = -1;
+                    for (int t = 0; t < d.nfix; ++t) if (d.fin_pos[t] == p) f = t;
+                    d.ef_bit[d.n_ef] = f; d.ef_w[d.n_ef] = i; d.n_ef++;
+                }
+            }
+        }
+        d.ng = ng;
+        for (int i = 0; i < ng; ++i) {
+            d.gbit[i] = gbits[i];
+            d.split_fix[i] = d.nfix - ng + i;
+            const int rb = wp[a0 + gbits[i]] - nl;
+            d.split_val |= (uint64_t)((h->rank >> rb) & 1) << i;
+        }
+        for (int c = 0; c < (1 << ng); ++c) {
+            int rr = h->rank;
+            for (int i = 0; i < ng; ++i) {
+                const int rb = wp[a0 + gbits[i]] - nl;
+                rr = (rr & ~(1 << rb)) | (((c >> i) & 1) << rb);
+            }
+            d.gbase[c] = R[rr]->psi;
+        }
+    }
+    // every member's earlier work on its shard is done before anyone reads it
+    const size_t P = R.size();
+    std::vector<cudaEvent_t> ev(P);
+    auto all_wait = [&]() {
+        for (size_t i = 0; i < P; ++i) {
+            cudaSetDevice(R[i]->device);
+            cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+            cudaEventRecord(ev[i], R[i]->stream);
+        }
+        for (size_t i = 0; i < P; ++i) {
+            cudaSetDevice(R[i]->device);
+            for (size_t j = 0; j < P; ++j) cudaStreamWaitEvent(R[i]->stream, ev[j], 0);
+        }
+        for (size_t i = 0; i < P; ++i) {
+            cudaSetDevice(R[i]->device);
+            cudaEventDestroy(ev[i]);
+        }
+    };
+    for (Handle *h : R) {
+        cudaSetDevice(h->device);
+        if (int rc = flush_queue(h)) return rc;
+    }
+    all_wait();
+    for (size_t r = 0; r < P; ++r) {
+        if (!launch_qft13(R[r], ds[r], R[r]->psi, R[r]->psi)) {
+            if (r == 0) return 1;
+            return fail(R[r], QSIM_ECUDA, "rank-group pass geometry differs between members");
+        }
+        if (int rc = after_launch(R[r], "rank-group pass")) return rc;
+    }
+    all_wait();   // a member's later work waits for every member that wrote into its shard
+    return QSIM_OK;
+}
+
 int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCircuit *gc = nullptr,
                 bool dry = false, bool even = false)
 {
@@ -503,6 +616,23 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
         std::vector<int> act;
         for (int u = 0; u < a; ++u) act.push_back(lo + a0 + u);
         if (h0->world > 1) {
+            // in-process rank groups: a block with one or two wires on rank bits
+            // runs as one rank-group pass over peer memory (the exchange fused
+            // into the pass, nothing moves beforehand); otherwise the block's
+            // wires are made local by shard exchanges first
+            static const bool no_rg = getenv("QSIM_NO_RANK_GROUP_PASS") != nullptr;   // measurement knob
+            std::vector<int> gw;
+            for (int u = 0; u < a; ++u)
+                if (wp[a0 + u] >= h0->nl) gw.push_back(u);
+            if (!no_rg && use13 && !dry && R.size() > 1 && !gw.empty() && gw.size() <= 2 && a >= 5 && a <= 10 &&
+                a - (int)gw.size() <= h0->nl) {
+                const int rc = rank_group_pass(R, wp, a0, a, gw, qft, inverse);
+                if (rc == QSIM_OK) {
+                    a0 += a;
+                    continue;
+                }
+                if (rc != 1) return rc;   // 1: geometry not supported, fall through
+            }
             if (int rc = dist_make_local(R, act)) return rc;
             for (int w = 0; w < m; ++w) wp[w] = h0->pos[lo + w];
         }

@@ -62,8 +62,19 @@ struct Q13 {
     int n_et, et_bit[kTB], et_w[kTB];         // early wires on tile bits
     int n_ef;                                 // early wires on tile-id bits (as erun)
     uint64_t y_const;
-    int qe0, qe1;                             // ext-id bits of the quarter index (landing ranks 11, 12)
+    int qe0, qe1;                             // ext-id bits of the quarter index (landing ranks 11, 12; -1: global)
     int in_first[5], in_len[5];               // tensor-map dim -> ext-id bit run
+    // rank-group pass (the exchange fused into the pass, peer memory): ng
+    // tile bits sit on rank bits -- the highest-ranked tile bits, i.e. the
+    // quarter bits -- so the tile's rows live in 2^ng shards; quarter q comes
+    // from shard (q >> (2 - ng)) through its own tensor map, every element is
+    // stored into the shard its global bits name, and this rank takes the
+    // tiles whose split bits equal its own rank bits
+    int ng;
+    int split_bit[2];                         // tile-id bits fixed per rank (ascending)
+    uint64_t split_val;
+    int gthr[2], gwin[2];                     // map-1 thread bit / window bit of global tile bit i (-1: not)
+    double2 *outb[4];                         // shard of global-bit combination c
 };
 
 __device__ __forceinline__ void tma_load5(void *dst, const CUtensorMap *map, const int (&c)[5], uint64_t *bar)
@@ -139,8 +150,9 @@ __device__ __forceinline__ double2 root13(uint64_t t, int W, const double2 *coar
 
 template <int A, bool INV, bool HONLY>
 __global__ void __launch_bounds__(kThr, 1)
-    k_qft13(const __grid_constant__ CUtensorMap in_map, double2 *__restrict__ out, const __grid_constant__ Q13 P,
-            uint64_t ntiles)
+    k_qft13(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap in_map1,
+            const __grid_constant__ CUtensorMap in_map2, const __grid_constant__ CUtensorMap in_map3,
+            double2 *__restrict__ out, const __grid_constant__ Q13 P, uint64_t ntiles)
 {
     static_assert(A >= kWB && A <= 10, "two 5-bit windows");
     constexpr int W1 = A - kWB;               // first wire of window 1
@@ -164,17 +176,27 @@ __global__ void __launch_bounds__(kThr, 1)
     __syncthreads();
 
     // quarter load s (s = 4 j + q: tile j of this CTA, quarter q) into slot s % 7
+    // this rank's t-th tile -> the full tile id (the split bits carry the rank's bits)
+    auto full_tile = [&](uint64_t t) -> uint64_t {
+        for (int i = 0; i < P.ng; ++i) t = ins_bit(t, P.split_bit[i], (P.split_val >> i) & 1);
+        return t;
+    };
     auto issue = [&](uint64_t s) {
-        const uint64_t T = blockIdx.x + (s >> 2) * (uint64_t)gridDim.x;
-        if (T >= ntiles) return;
+        const uint64_t t = blockIdx.x + (s >> 2) * (uint64_t)gridDim.x;
+        if (t >= ntiles) return;
+        const uint64_t T = full_tile(t);
         const uint64_t q = s & 3;
-        const uint64_t X = ins_bit(ins_bit(T, P.qe0, q & 1), P.qe1, q >> 1);
+        uint64_t X = T;
+        if (P.qe0 >= 0) X = ins_bit(X, P.qe0, q & 1);
+        if (P.qe1 >= 0) X = ins_bit(X, P.qe1, q >> 1);
         int c[5];
 #pragma unroll
         for (int d = 0; d < 5; ++d) c[d] = P.in_len[d] ? (int)((X >> P.in_first[d]) & ((1ull << P.in_len[d]) - 1)) : 0;
         const int sl = (int)(s % kSlots);
         mbar_expect_tx(&bar[sl], kSlotBytes);
-        tma_load5(slots + (size_t)sl * kSlotAmps, &in_map, c, &bar[sl]);
+        const int m = P.ng == 0 ? 0 : (int)(q >> (2 - P.ng));
+        const CUtensorMap *mp = m == 0 ? &in_map : m == 1 ? &in_map1 : m == 2 ? &in_map2 : &in_map3;
+        tma_load5(slots + (size_t)sl * kSlotAmps, mp, c, &bar[sl]);
     };
     if (tid == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&in_map) : "memory");
@@ -190,15 +212,19 @@ __global__ void __launch_bounds__(kThr, 1)
         tp0 |= bit << P.order0[t];
         tp1 |= bit << P.order1[t];
         lin |= bit << P.in_rank[P.order0[t]];
-        tout |= (uint64_t)bit << P.out_pos[P.order1[t]];
+        if (P.out_pos[P.order1[t]] >= 0) tout |= (uint64_t)bit << P.out_pos[P.order1[t]];
     }
     uint32_t pin[kWB];
     uint64_t pout[kWB];
 #pragma unroll
     for (int b = 0; b < kWB; ++b) {
         pin[b] = 1u << P.in_rank[b];
-        pout[b] = 1ull << P.out_pos[W1 + b];
+        pout[b] = P.out_pos[W1 + b] >= 0 ? 1ull << P.out_pos[W1 + b] : 0ull;   // -1: a global bit
     }
+    // global-bit combination of this thread's part of its elements (map 1)
+    uint32_t gtid = 0;
+    for (int i = 0; i < P.ng; ++i)
+        if (P.gthr[i] >= 0) gtid |= ((tid >> P.gthr[i]) & 1u) << i;
     const uint32_t stp0 = swz13(tp0), stp1 = swz13(tp1);
     // J of the thread bits of map 0 (the window-0 bits are wires 0..4: weights 2^(A-1-b))
     constexpr uint32_t amask = (1u << A) - 1u;
@@ -215,8 +241,9 @@ __global__ void __launch_bounds__(kThr, 1)
     }
 
     for (uint64_t j = 0;; ++j) {
-        const uint64_t T = blockIdx.x + j * (uint64_t)gridDim.x;
-        if (T >= ntiles) break;
+        const uint64_t tt = blockIdx.x + j * (uint64_t)gridDim.x;
+        if (tt >= ntiles) break;
+        const uint64_t T = full_tile(tt);
         const uint32_t s0 = (uint32_t)((4 * j) % kSlots);   // slot of quarter 0; quarter q in (s0 + q) % 7
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -332,19 +359,34 @@ __global__ void __launch_bounds__(kThr, 1)
         uint64_t ib = tout;
         for (int e = 0; e < P.n_orun; ++e)
             ib |= ((T >> P.orun_src[e]) & ((1ull << P.orun_len[e]) - 1)) << P.orun_dst[e];
+        if (P.ng == 0) {
 #pragma unroll
-        for (int k = 0; k < kNS; ++k) {
-            uint64_t o = ib;
+            for (int k = 0; k < kNS; ++k) {
+                uint64_t o = ib;
 #pragma unroll
-            for (int b = 0; b < kWB; ++b)
-                if (k & (1 << b)) o |= pout[b];
-            __stcs(out + o, v[k]);
+                for (int b = 0; b < kWB; ++b)
+                    if (k & (1 << b)) o |= pout[b];
+                __stcs(out + o, v[k]);
+            }
+        } else {
+            // rank-group pass: each element goes to the shard its global bits name
+#pragma unroll
+            for (int k = 0; k < kNS; ++k) {
+                uint64_t o = ib;
+#pragma unroll
+                for (int b = 0; b < kWB; ++b)
+                    if (k & (1 << b)) o |= pout[b];
+                uint32_t g = gtid;
+                for (int i = 0; i < P.ng; ++i)
+                    if (P.gwin[i] >= 0) g |= (uint32_t)((k >> P.gwin[i]) & 1) << i;
+                __stcs(P.outb[g] + o, v[k]);
+            }
         }
     }
 }
 
 template <int A, bool INV, bool HONLY>
-void launch13(Handle *h, const CUtensorMap &im, double2 *out, const Q13 &P, uint64_t ntiles)
+void launch13(Handle *h, const CUtensorMap (&im)[4], double2 *out, const Q13 &P, uint64_t ntiles)
 {
     const size_t smem = (size_t)kSlots * kSlotBytes + 64 * sizeof(double2) + kSlots * sizeof(uint64_t);
     static uint64_t attr = 0;
@@ -352,12 +394,13 @@ void launch13(Handle *h, const CUtensorMap &im, double2 *out, const Q13 &P, uint
         cudaFuncSetAttribute(k_qft13<A, INV, HONLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)h->num_sms);
     prof_begin(h);
-    k_qft13<A, INV, HONLY><<<grid, kThr, smem, h->stream>>>(im, out, P, ntiles);
+    k_qft13<A, INV, HONLY><<<grid, kThr, smem, h->stream>>>(im[0], im[1], im[2], im[3], out, P, ntiles);
     prof_end(h, "k_qft13", (ntiles << kTB) * 32);
 }
 
 template <int A>
-void launch13_a(Handle *h, const CUtensorMap &im, double2 *out, const Q13 &P, uint64_t ntiles, bool inv, bool honly)
+void launch13_a(Handle *h, const CUtensorMap (&im)[4], double2 *out, const Q13 &P, uint64_t ntiles, bool inv,
+                bool honly)
 {
     if (honly) launch13<A, false, true>(h, im, out, P, ntiles);
     else if (inv) launch13<A, true, false>(h, im, out, P, ntiles);
@@ -390,14 +433,28 @@ bool launch_qft13(Handle *h, const Qft13Desc &d, const double2 *in, double2 *out
             if (byin[r] >= kWB) rest.push_back(byin[r]);
         for (int t = 0; t < kThrBits; ++t) P.order0[t] = rest[t];
     }
-    // map 1: window = tile bits a-5..a-1, thread bits by output position (coalesced stores)
+    // map 1: window = tile bits a-5..a-1, thread bits by output position
+    // (coalesced stores; global tile bits, out_pos -1, last)
     {
         std::vector<int> rest;
         for (int b = 0; b < kTB; ++b)
             if (b < d.a - kWB || b >= d.a) rest.push_back(b);
-        std::sort(rest.begin(), rest.end(), [&](int x, int y) { return d.out_pos[x] < d.out_pos[y]; });
+        auto key = [&](int b) { return d.out_pos[b] < 0 ? 1000 + b : d.out_pos[b]; };
+        std::sort(rest.begin(), rest.end(), [&](int x, int y) { return key(x) < key(y); });
         for (int t = 0; t < kThrBits; ++t) P.order1[t] = rest[t];
     }
+    // rank-group pass: the global tile bits (in_pos >= nl) are the highest-ranked
+    P.ng = d.ng;
+    for (int i = 0; i < d.ng; ++i) {
+        if (byin[kTB - d.ng + i] != d.gbit[i] || d.in_pos[d.gbit[i]] < nl) return false;
+        P.split_bit[i] = d.split_fix[i];
+        P.gthr[i] = P.gwin[i] = -1;
+        for (int t = 0; t < kThrBits; ++t)
+            if (P.order1[t] == d.gbit[i]) P.gthr[i] = t;
+        if (d.gbit[i] >= d.a - kWB && d.gbit[i] < d.a) P.gwin[i] = d.gbit[i] - (d.a - kWB);
+    }
+    P.split_val = d.split_val;
+    for (int c = 0; c < (1 << d.ng); ++c) P.outb[c] = d.gbase[c];
     // early wires: on tile bits they must be thread bits of map 0 (they are passive bits >= a)
     P.n_et = d.n_et;
     for (int e = 0; e < d.n_et; ++e) {
@@ -438,7 +495,10 @@ bool launch_qft13(Handle *h, const Qft13Desc &d, const double2 *in, double2 *out
     std::vector<int> fid(nl, -1);
     {
         std::vector<char> in_sub(nl, 0);
-        for (int p : sub_pos) in_sub[p] = 1;
+        for (int p : sub_pos) {
+            if (p >= nl) return false;
+            in_sub[p] = 1;
+        }
         int e = 0;
         P.qe0 = P.qe1 = -1;
         for (int p = 0; p < nl; ++p) {
@@ -447,16 +507,20 @@ bool launch_qft13(Handle *h, const Qft13Desc &d, const double2 *in, double2 *out
             if (p == d.in_pos[byin[kQB + 1]]) P.qe1 = e;
             fid[p] = e++;
         }
-        if (P.qe0 < 0 || P.qe1 < 0 || P.qe0 > P.qe1) return false;
+        // local quarter bits are ext-id bits; global ones (rank-group pass) pick the shard
+        if ((d.ng < 2 && P.qe0 < 0) || (d.ng < 1 && P.qe1 < 0) || (P.qe1 >= 0 && P.qe0 > P.qe1)) return false;
         // the tile-id bits fill the other ext bits in ascending position order,
         // which is the order of d.fin_pos (ascending)
         for (int f = 1; f < d.nfix; ++f)
             if (d.fin_pos[f] < d.fin_pos[f - 1]) return false;
     }
-    CUtensorMap im;
+    CUtensorMap im[4];
     int rank_sub[kQB];
-    if (!build_side(in, nl, sub_pos, fid, im, P.in_first, P.in_len, rank_sub)) return false;
-    const uint64_t ntiles = 1ull << d.nfix;
+    std::memset(im, 0, sizeof im);
+    for (int c = 0; c < (1 << d.ng); ++c)
+        if (!build_side(d.ng ? d.gbase[c] : in, nl, sub_pos, fid, im[c], P.in_first, P.in_len, rank_sub))
+            return false;
+    const uint64_t ntiles = 1ull << (d.nfix - d.ng);   // this rank's share of the tiles
     switch (d.a) {
     case 5: launch13_a<5>(h, im, out, P, ntiles, d.inverse, d.hadamard_only); break;
     case 6: launch13_a<6>(h, im, out, P, ntiles, d.inverse, d.hadamard_only); break;

@@ -173,6 +173,15 @@ struct Qft13Desc {
     uint64_t y_const;
     int W, inverse, hadamard_only;
     double scale;
+    // rank-group pass (api.cu fused_range, in-process groups): ng <= 2 tile
+    // bits gbit[] (ascending position) sit on rank bits (in_pos >= nl, out_pos
+    // -1); the pass runs in place on the 2^ng shards gbase[c] (c = the global
+    // bits' values) and this rank takes the tiles whose tile-id bits
+    // split_fix[] (ascending) equal split_val's bits
+    int ng;
+    int gbit[2], split_fix[2];
+    uint64_t split_val;
+    double2 *gbase[4];
 };
 bool launch_qft13(Handle *h, const Qft13Desc &d, const double2 *in, double2 *out);
 bool qft_gen_feasible(Handle *h, const TilePass &tp);

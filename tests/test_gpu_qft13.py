@@ -112,3 +112,59 @@ def test_qft13_off_matches_on():
         assert r.returncode == 0, r.stderr
         outs.append(np.load(path))
     assert np.max(np.abs(outs[0] - outs[1])) < 1e-13
+
+
+@pytest.mark.parametrize("world,n", [(2, 17), (4, 18), (2, 20), (4, 19)])
+@pytest.mark.parametrize("op,inverse", [("qft", False), ("qft", True), ("had", False), ("fft", False)])
+def test_rank_group_pass(world, n, op, inverse):
+    """Blocks whose wires sit on rank bits run as one k_qft13 rank-group pass
+    over peer memory (no shard exchange): the whole-register transform of a
+    sharded handle equals the oracle, and rank 0 records no exchange."""
+    psi = rand_state(n, 11 * n + world)
+    h = Q.qsim_create(n, world)
+    try:
+        Q.qsim_set_state(h, 0, psi)
+        Q.qsim_profile(h, True)
+        if op == "qft":
+            Q.qsim_qft(h, 0, n, inverse)
+        elif op == "fft":
+            Q.qsim_fft(h, 0, n, inverse)
+        else:
+            Q.qsim_hadamard(h, 0, n)
+        prof = Q.qsim_profile_json(h)
+        Q.qsim_profile(h, False)
+        got = Q.qsim_get_state(h, 0, 1 << n)
+    finally:
+        Q.qsim_destroy(h)
+    ref = psi.copy()
+    if op == "had":
+        O.hadamard_range(ref, 0, n)
+    else:
+        O.qft(ref, 0, n, inverse)
+    assert "k_qft13" in prof, prof.keys()
+    assert "group_pair_exchange" not in prof, prof.keys()
+    assert np.max(np.abs(got - ref)) < TOL
+
+
+def test_rank_group_pass_off_matches_on():
+    """QSIM_NO_RANK_GROUP_PASS (exchanges, then local passes) and the
+    rank-group pass give the same state (world 2 and 8: 8 ranks put three
+    wires on rank bits, the block falls back to exchanges)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = (
+        "import sys, numpy as np; sys.path.insert(0, sys.argv[1]);"
+        "from paper_quant_ph_0201042_b200 import qsim as Q;"
+        "out = [];"
+        "exec(\"for w in (2, 8):\\n h = Q.qsim_create(19, w); Q.qsim_init_gaussian(h, 3); Q.qsim_qft(h, 0, 19, False);"
+        " Q.qsim_hadamard(h, 2, 15); out.append(Q.qsim_get_state(h, 0, 1 << 19)); Q.qsim_destroy(h)\");"
+        "np.save(sys.argv[2], np.stack(out))")
+    res = []
+    for env in ({}, {"QSIM_NO_RANK_GROUP_PASS": "1"}):
+        path = f"/tmp/rgp_{len(env)}.npy"
+        r = subprocess.run([sys.executable, "-c", script, root, path], env=dict(os.environ, **env),
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        res.append(np.load(path))
+    assert np.max(np.abs(res[0] - res[1])) < 1e-13
