@@ -442,6 +442,14 @@ int rank_group_pass(const Ranks &R, const std::vector<int> &wp, int a0, int a, c
     if ((int)tpos.size() != kTile13Bits) return 1;
     std::vector<int> gbits(gw);
     std::sort(gbits.begin(), gbits.end(), [&](int x, int y) { return wp[a0 + x] < wp[a0 + y]; });
+    // one process per GPU: the peers' shards through CUDA IPC (collective; all
+    // ranks agree on availability); an in-process group addresses them directly
+    std::vector<double2 *> world_shards;
+    const bool world_mode = R.size() == 1;
+    if (world_mode) {
+        if (int rc = flush_queue(h0)) return rc;
+        if (int rc = dist_world_shards(h0, world_shards)) return rc;   // 1: no IPC, the caller exchanges
+    }
     std::vector<Qft13Desc> ds(R.size());
     for (size_t r = 0; r < R.size(); ++r) {
         Handle *h = R[r];
@@ -491,7 +499,7 @@ int rank_group_pass(const Ranks &R, const std::vector<int> &wp, int a0, int a, c
                 const int rb = wp[a0 + gbits[i]] - nl;
                 rr = (rr & ~(1 << rb)) | (((c >> i) & 1) << rb);
             }
-            d.gbase[c] = R[rr]->psi;
+            d.gbase[c] = world_shards.empty() ? R[rr]->psi : world_shards[rr];
         }
     }
     // every member's earlier work on its shard is done before anyone reads it
@@ -512,6 +520,15 @@ int rank_group_pass(const Ranks &R, const std::vector<int> &wp, int a0, int a, c
             cudaEventDestroy(ev[i]);
         }
     };
+    if (world_mode) {
+        // every rank's earlier work is done before anyone touches its shard;
+        // afterwards no rank moves on while a peer may still write into it
+        if (int rc = dist_world_barrier(h0)) return rc;
+        if (!launch_qft13(h0, ds[0], h0->psi, h0->psi))
+            return fail(h0, QSIM_ECUDA, "rank-group pass geometry rejected after the shards were mapped");
+        if (int rc = after_launch(h0, "rank-group pass")) return rc;
+        return dist_world_barrier(h0);
+    }
     for (Handle *h : R) {
         cudaSetDevice(h->device);
         if (int rc = flush_queue(h)) return rc;
@@ -624,7 +641,7 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
             std::vector<int> gw;
             for (int u = 0; u < a; ++u)
                 if (wp[a0 + u] >= h0->nl) gw.push_back(u);
-            if (!no_rg && use13 && !dry && R.size() > 1 && !gw.empty() && gw.size() <= 2 && a >= 5 && a <= 10 &&
+            if (!no_rg && use13 && !dry && !gw.empty() && gw.size() <= 2 && a >= 5 && a <= 10 &&
                 a - (int)gw.size() <= h0->nl) {
                 const int rc = rank_group_pass(R, wp, a0, a, gw, qft, inverse);
                 if (rc == QSIM_OK) {

@@ -492,6 +492,56 @@ static int remote_gate_world(Handle *h, uint64_t cmask, uint64_t cvals, int q, c
 // shard and its partner's (r ^ 2^(g-nl)) into its scratch shard; once both
 // kernels of a pair are done (cross-stream events) the ranks swap shard and
 // scratch.  No layout change, no staging copies.
+// Multi-process world, rank-group passes: every rank's current shard mapped
+// into this process (CUDA IPC, set up once; one all-gather of which of its two
+// allocations each rank is using), and a stream-ordered barrier.
+int dist_world_shards(Handle *h, std::vector<double2 *> &shards)
+{
+#ifndef QSIM_NO_NCCL
+    if (h->world < 2 || !h->comm || ipc_setup(h) != 1) return 1;
+    const int W = h->world;
+    unsigned char par = h->psi == h->own_buf[0] ? 0 : 1;
+    std::vector<unsigned char> pars(W, 0);
+    unsigned char *d = nullptr;
+    if (cudaMalloc(&d, W + 1) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(h, QSIM_ENOMEM, "rank-group pass buffer");
+    }
+    cudaMemcpyAsync(d, &par, 1, cudaMemcpyHostToDevice, h->stream);
+    int rc = nccl_check(h, ncclAllGather(d, d + 1, 1, ncclUint8, h->comm, h->stream), "ncclAllGather");
+    cudaMemcpyAsync(pars.data(), d + 1, W, cudaMemcpyDeviceToHost, h->stream);
+    cudaStreamSynchronize(h->stream);
+    cudaFree(d);
+    if (rc) return rc;
+    shards.assign(W, nullptr);
+    for (int r = 0; r < W; ++r) shards[r] = h->peer_buf[2 * r + pars[r]];
+    return QSIM_OK;
+#else
+    (void)h;
+    (void)shards;
+    return 1;
+#endif
+}
+
+int dist_world_barrier(Handle *h)
+{
+#ifndef QSIM_NO_NCCL
+    double *dz = nullptr;
+    if (cudaMalloc(&dz, sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(h, QSIM_ENOMEM, "barrier buffer");
+    }
+    cudaMemsetAsync(dz, 0, sizeof(double), h->stream);
+    int rc = nccl_check(h, ncclAllReduce(dz, dz, 1, ncclDouble, ncclSum, h->comm, h->stream), "barrier");
+    cudaStreamSynchronize(h->stream);
+    cudaFree(dz);
+    return rc;
+#else
+    (void)h;
+    return QSIM_OK;
+#endif
+}
+
 int dist_remote_gate(const Ranks &R, uint64_t cmask, uint64_t cvals, int q, const double2 U[4])
 {
 #ifndef QSIM_NO_NCCL

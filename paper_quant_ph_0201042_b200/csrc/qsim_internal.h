@@ -393,6 +393,10 @@ int dist_make_local(const Ranks &R, const std::vector<int> &need);   // make log
 bool dist_remote_gate_available(const Ranks &R);
 int dist_remote_gate(const Ranks &R, uint64_t cmask, uint64_t cvals, int q, const double2 U[4]);
 int dist_canonicalize(const Ranks &R);                               // pos[q] = n-1-q everywhere
+// multi-process world: every rank's current shard as a pointer in this
+// process (CUDA IPC; 1: not available), and a stream-ordered all-rank barrier
+int dist_world_shards(Handle *h, std::vector<double2 *> &shards);
+int dist_world_barrier(Handle *h);
 // per-rank host partials -> the sum over all ranks of the world, in rank order
 // (parts[i] belongs to R[i]); out may alias parts[0]
 int dist_sum_host(const Ranks &R, const std::vector<std::vector<double>> &parts, double *out, size_t count);
