@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqsim.so")
+# QSIM_LIB: another in-tree build of the same library (A/B measurements only)
+LIB_PATH = os.environ.get("QSIM_LIB") or os.path.join(_HERE, "libqsim.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
