@@ -153,6 +153,60 @@ __global__ void __launch_bounds__(256, 1) k_ideal2(double2 *psi, const Op8 *ops_
     }
 }
 
+
+// a dense 2x2 on lane bit L: each thread keeps its own row, the partner's
+// amplitude arrives by shuffle (4 x 32-bit per double2)
+__device__ __forceinline__ double shfl_d(double x, int m)
+{
+    int lo = __double2loint(x), hi = __double2hiint(x);
+    lo = __shfl_xor_sync(0xffffffffu, lo, m);
+    hi = __shfl_xor_sync(0xffffffffu, hi, m);
+    return __hiloint2double(hi, lo);
+}
+template <int L>
+__device__ __forceinline__ void dense_lane(double2 (&v)[32], const double2 u0, const double2 u1, const double2 u2,
+                                           const double2 u3)
+{
+    const bool hi = (threadIdx.x >> L) & 1;
+    const double2 a = hi ? u3 : u0, b = hi ? u2 : u1;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+        const double2 x = v[k];
+        const double2 y = make_double2(shfl_d(x.x, 1 << L), shfl_d(x.y, 1 << L));
+        v[k] = make_double2(fma(a.x, x.x, fma(-a.y, x.y, fma(b.x, y.x, -b.y * y.y))),
+                            fma(a.x, x.y, fma(a.y, x.x, fma(b.x, y.y, b.y * y.x))));
+    }
+}
+
+__global__ void __launch_bounds__(256, 1) k_ideal_lane(double2 *psi, const Op *ops_g, int nops, uint64_t ntiles)
+{
+    __shared__ Op ops[64];
+    for (int i = threadIdx.x; i < nops; i += blockDim.x) ops[i] = ops_g[i];
+    __syncthreads();
+    for (uint64_t T = blockIdx.x; T < ntiles; T += gridDim.x) {
+        double2 v[32];
+        double2 *base = psi + T * 8192 + threadIdx.x;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) v[k] = base[256 * k];
+        for (int i = 0; i < nops; ++i) {
+            const double2 u0 = ops[i].u[0], u1 = ops[i].u[1], u2 = ops[i].u[2], u3 = ops[i].u[3];
+            switch (i % 9) {
+            case 0: dense<0, 0>(v, u0, u1, u2, u3); break;
+            case 1: dense<1, 0>(v, u0, u1, u2, u3); break;
+            case 2: dense<2, 0>(v, u0, u1, u2, u3); break;
+            case 3: dense<3, 0>(v, u0, u1, u2, u3); break;
+            case 4: dense<4, 0>(v, u0, u1, u2, u3); break;
+            case 5: dense_lane<0>(v, u0, u1, u2, u3); break;
+            case 6: dense_lane<1>(v, u0, u1, u2, u3); break;
+            case 7: dense_lane<2>(v, u0, u1, u2, u3); break;
+            default: dense_lane<3>(v, u0, u1, u2, u3); break;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 32; ++k) base[256 * k] = v[k];
+    }
+}
+
 int main()
 {
     const int n = 28, nops = 26;
@@ -218,6 +272,19 @@ int main()
                    tr ? "+transpose" : "", ms, instr / (ms * 1e-3) / (sms * 64.0 * 1.965e9),
                    cudaGetErrorString(cudaGetLastError()));
         }
+    }
+    {
+        k_ideal_lane<<<sms, 256>>>(psi, ops, nops, N >> 13);
+        cudaEventRecord(a);
+        for (int r = 0; r < 3; ++r) k_ideal_lane<<<sms, 256>>>(psi, ops, nops, N >> 13);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        ms /= 3;
+        const double instr = (double)nops * 16 * (N / 2);
+        printf("{\"var\": \"reg+lane ops (5 of 9 in registers, 4 by shuffle)\", \"ms\": %.3f, \"frac_of_64_per_clk_at_1965\": %.3f, \"err\": \"%s\"}\n",
+               ms, instr / (ms * 1e-3) / (sms * 64.0 * 1.965e9), cudaGetErrorString(cudaGetLastError()));
     }
     return 0;
 }
