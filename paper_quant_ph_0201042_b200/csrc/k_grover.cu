@@ -198,8 +198,17 @@ __global__ void __launch_bounds__(kPersistThreads) k_grover_persist(double2 *__r
 // t+2 after every CTA has published t+1, i.e. finished reading t.  (Measured
 // alternative: slots in NCCL's "LL" layout -- 64-bit words of {32 data bits,
 // tag}, read by 128 pollers per CTA without the counter -- 2.7x slower.)
-template <int A>
-__global__ void __launch_bounds__(kRegsThreads, 1) k_grover_regs(double2 *__restrict__ psi, uint64_t N, uint64_t k,
+// CARRY: the amplitude sum is carried instead of re-reduced every
+// iteration.  D = 2|s><s| - I has |s> as an eigenvector and is symmetric, so
+// <s|D phi> = <s|phi> for every phi: the sum after an iteration is the sum
+// after the phase flip, S - 2 alpha_k, and alpha_k itself becomes
+// 2 (S - 2 alpha_k)/N + alpha_k.  Every CTA evolves (S, alpha_k) with exactly
+// the floating-point operations the owner of alpha_k applies to its register,
+// so all CTAs agree bit for bit with the state and no grid-wide exchange is
+// needed after the first sum; every amplitude is still updated in every
+// iteration.
+template <int A, bool CARRY>
+__global__ void __launch_bounds__(kRegsThreads, A <= 4 ? 4 : A <= 8 ? 2 : 1) k_grover_regs(double2 *__restrict__ psi, uint64_t N, uint64_t k,
                                                                    int iters, double *__restrict__ trace,
                                                                    double4 *__restrict__ slots,
                                                                    unsigned *__restrict__ tags)
@@ -278,21 +287,40 @@ __global__ void __launch_bounds__(kRegsThreads, 1) k_grover_regs(double2 *__rest
     };
 
     exchange(-1);
+    double4 cur = s_tot;   // (S, alpha_k) -- carried in registers when CARRY
     for (int t = 0; t < iters; ++t) {
-        const double4 T = s_tot;   // sum S and alpha_k of the previous iteration
+        const double4 T = CARRY ? cur : s_tot;   // sum S and alpha_k of the previous iteration
         // after V_{f_k} the sum is S - 2 alpha_k; 2|s><s| - I maps a -> 2 mean - a
-        const double m2x = 2.0 * (T.x - 2.0 * T.z) * inv, m2y = 2.0 * (T.y - 2.0 * T.w) * inv;
+        const double sfx = T.x - 2.0 * T.z, sfy = T.y - 2.0 * T.w;
+        const double m2x = 2.0 * sfx * inv, m2y = 2.0 * sfy * inv;
+        if (CARRY) {
+            // alpha_k lives in cur (bit-identical in every CTA), so the
+            // owner's register slot is left to the plain update and replaced
+            // by cur at the store: no per-amplitude sign select, 2 DADD per
+            // amplitude
 #pragma unroll
-        for (int j = 0; j < A; ++j) {
-            double2 a = v[j];
-            if (own_t && j == kj) { a.x = -a.x; a.y = -a.y; }   // V_{f_k}
-            v[j] = make_double2(m2x - a.x, m2y - a.y);
+            for (int j = 0; j < A; ++j) v[j] = make_double2(m2x - v[j].x, m2y - v[j].y);
+        } else {
+#pragma unroll
+            for (int j = 0; j < A; ++j) {
+                double2 a = v[j];
+                if (own_t && j == kj) { a.x = -a.x; a.y = -a.y; }   // V_{f_k}
+                v[j] = make_double2(m2x - a.x, m2y - a.y);
+            }
         }
-        exchange(t);
-        if (blockIdx.x == 0 && threadIdx.x == 0 && trace) trace[t] = fma(s_tot.z, s_tot.z, s_tot.w * s_tot.w);
+        if (CARRY) {
+            // the owner's update of alpha_k, m2 - (-alpha_k), with the same operations
+            cur = make_double4(sfx, sfy, m2x - (-T.z), m2y - (-T.w));
+            if (blockIdx.x == 0 && threadIdx.x == 0 && trace) trace[t] = fma(cur.z, cur.z, cur.w * cur.w);
+        } else {
+            exchange(t);
+            if (blockIdx.x == 0 && threadIdx.x == 0 && trace) trace[t] = fma(s_tot.z, s_tot.z, s_tot.w * s_tot.w);
+        }
     }
 #pragma unroll
-    for (int j = 0; j < A; ++j) psi[base + threadIdx.x + (uint64_t)j * blockDim.x] = v[j];
+    for (int j = 0; j < A; ++j)
+        psi[base + threadIdx.x + (uint64_t)j * blockDim.x] =
+            CARRY && iters > 0 && own_t && j == kj ? make_double2(cur.z, cur.w) : v[j];
 }
 
 }  // namespace
@@ -329,13 +357,35 @@ static bool try_persist(Handle *h, uint64_t mark, int iters, double *d_trace)
 static bool try_regs(Handle *h, uint64_t mark, int iters, double *d_trace)
 {
     const uint64_t N = h->local_dim();
+    // QSIM_GROVER_REDUCE: re-reduce the sum every iteration (measurement / cross-check knob)
+    static const bool reduce = getenv("QSIM_GROVER_REDUCE") != nullptr;
+    auto pick = [&](uint64_t per) -> void * {
+        if (reduce)
+            return per <= 1 ? (void *)k_grover_regs<1, false> : per <= 2 ? (void *)k_grover_regs<2, false>
+                 : per <= 4 ? (void *)k_grover_regs<4, false> : per <= 8 ? (void *)k_grover_regs<8, false>
+                 : per <= 16 ? (void *)k_grover_regs<16, false> : (void *)k_grover_regs<32, false>;
+        return per <= 1 ? (void *)k_grover_regs<1, true> : per <= 2 ? (void *)k_grover_regs<2, true>
+             : per <= 4 ? (void *)k_grover_regs<4, true> : per <= 8 ? (void *)k_grover_regs<8, true>
+             : per <= 16 ? (void *)k_grover_regs<16, true> : (void *)k_grover_regs<32, true>;
+    };
     uint64_t blocks = 1;
     while (blocks * 2 <= (uint64_t)h->num_sms && blocks * 2 <= N / kRegsThreads) blocks *= 2;
+    if (!reduce) {
+        // no exchange after the first sum: spread the state thin (down to 4
+        // amplitudes per thread, several CTAs per SM) so the iterations' short
+        // dependent update chains interleave across many warps -- as far as
+        // every CTA stays co-resident (the first sum is a grid-wide exchange)
+        while (N / (blocks * 2 * kRegsThreads) >= 4) {
+            int ps = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, pick(N / (blocks * 2 * kRegsThreads)), kRegsThreads, 0);
+            if ((uint64_t)ps * h->num_sms < blocks * 2) break;
+            blocks *= 2;
+        }
+    }
     const uint64_t per = N / (blocks * kRegsThreads);
     if (per < 1 || per > 32 || N % (blocks * kRegsThreads)) return false;
     int per_sm = 0;
-    void *fn = per <= 1 ? (void *)k_grover_regs<1> : per <= 2 ? (void *)k_grover_regs<2> : per <= 4 ? (void *)k_grover_regs<4>
-             : per <= 8 ? (void *)k_grover_regs<8> : per <= 16 ? (void *)k_grover_regs<16> : (void *)k_grover_regs<32>;
+    void *fn = pick(per);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kRegsThreads, 0);
     if (per_sm < 1 || blocks > (uint64_t)per_sm * h->num_sms) return false;
     // slots: 2 x blocks double4 (parity double buffer); tags[0]: the arrival counter

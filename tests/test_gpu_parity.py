@@ -553,3 +553,26 @@ def test_cfg4_mirror_returns_to_zero(reg, n):
     _cfg4_inverse(h, n, layers, seed, sigma, ev)
     assert Q.qsim_prob_index(h, 0) > 1 - 1e-10
     assert abs(Q.qsim_norm(h) - 1) < 1e-12
+
+
+def test_cfg1_carried_sum_equals_reduced_sum():
+    """k_grover_regs carries the amplitude sum through the iterations (D keeps
+    <s|.>) instead of re-reducing it every iteration; the
+    re-reducing variant (QSIM_GROVER_REDUCE) gives the same trace and state."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = (
+        "import sys, numpy as np; sys.path.insert(0, sys.argv[1]);"
+        "from paper_quant_ph_0201042_b200 import qsim as Q; from paper_quant_ph_0201042_b200 import workloads as W;"
+        "h = Q.qsim_create(20); k, tr = W.run_cfg1(h, n=20, seed=2);"
+        "np.save(sys.argv[2], np.concatenate([tr.astype(complex), Q.qsim_get_state(h, 0, 1 << 20)]))")
+    res = []
+    for env in ({}, {"QSIM_GROVER_REDUCE": "1"}):
+        path = f"/tmp/grover_{len(env)}.npy"
+        r = subprocess.run([sys.executable, "-c", script, root, path], env=dict(os.environ, **env),
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        res.append(np.load(path))
+    assert np.max(np.abs(res[0] - res[1])) < 1e-13
