@@ -596,7 +596,7 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
     // measured per pass in profiles/r2_qft_passes.md).  The first block may
     // take 10 wires: with block moves it writes one contiguous run per tile.
     static const bool no13 = getenv("QSIM_NO_QFT13") != nullptr;   // measurement knob
-    static const bool force13 = getenv("QSIM_FORCE_QFT13") != nullptr;   // measurement knob
+    const bool force13 = getenv("QSIM_FORCE_QFT13") != nullptr;   // test / measurement knob (read per call)
     // only where it saves a pass: a 12-bit pass of <= 8 wires streams faster
     // (6.2-6.5 vs 5.4-6.1 TB/s), so ceil(m/10) must beat ceil(m/8)
     // (m = 31: 8,8,8,7 on 12-bit tiles 43.6 ms vs 48.9 ms on 13-bit tiles)

@@ -24,10 +24,15 @@ def rand_state(n, seed):
     return v / np.linalg.norm(v)
 
 
-def run(n, op, lo, m, inverse=False, world=1, blocks=None):
+def run(n, op, lo, m, inverse=False, world=1, blocks=None, force=True):
+    """op on a seeded state; force: QSIM_FORCE_QFT13 (the 13-bit passes even
+    where the default plan keeps the 12-bit kernel, i.e. where they do not
+    save a pass -- this module tests the kernel at every size)."""
     psi = rand_state(n, 3 * n + lo + 7 * m)
     if blocks:
         os.environ["QSIM_QFT_BLOCKS"] = blocks
+    if force:
+        os.environ["QSIM_FORCE_QFT13"] = "1"
     try:
         h = Q.qsim_create(n, world)
         Q.qsim_set_state(h, 0, psi)
@@ -45,6 +50,7 @@ def run(n, op, lo, m, inverse=False, world=1, blocks=None):
         Q.qsim_destroy(h)
     finally:
         os.environ.pop("QSIM_QFT_BLOCKS", None)
+        os.environ.pop("QSIM_FORCE_QFT13", None)
     ref = psi.copy()
     if op == "had":
         O.hadamard_range(ref, lo, m)
@@ -62,6 +68,26 @@ def test_qft13_default_plan(n, lo, m, inverse):
     assert "k_qft13" in prof, prof.keys()
     assert np.max(np.abs(got - ref)) < TOL
     assert abs(norm - 1) < 1e-12
+
+
+@pytest.mark.parametrize("n", [15, 16, 17, 20, 21, 24, 25, 28])
+def test_default_plan_uses_qft13_where_it_saves_a_pass(n):
+    """Default plan: the 13-bit passes exactly where ceil(m/10) < ceil(m/8)
+    (a 12-bit pass of <= 8 wires streams faster)."""
+    got, ref, _, prof = run(n, "qft", 0, n, False, force=False) if n <= 24 else (None, None, None, None)
+    if n > 24:   # large: kernel record only
+        h = Q.qsim_create(n)
+        try:
+            Q.qsim_init_gaussian(h, 1)
+            Q.qsim_profile(h, True)
+            Q.qsim_qft(h, 0, n, False)
+            prof = Q.qsim_profile_json(h)
+        finally:
+            Q.qsim_destroy(h)
+    else:
+        assert np.max(np.abs(got - ref)) < TOL
+    saves = (n + 9) // 10 < (n + 7) // 8
+    assert ("k_qft13" in prof) == saves, (n, prof.keys())
 
 
 @pytest.mark.parametrize("blocks", ["10,10", "5,10,5", "6,7,7", "9,5,6", "8,6,6", "10,5,5", "7,6,7"])
