@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(kPersistThreads) k_grover_persist(double2 *__r
 // needed after the first sum; every amplitude is still updated in every
 // iteration.
 template <int A, bool CARRY>
-__global__ void __launch_bounds__(kRegsThreads, A <= 4 ? 4 : A <= 8 ? 2 : 1) k_grover_regs(double2 *__restrict__ psi, uint64_t N, uint64_t k,
+__global__ void __launch_bounds__(kRegsThreads, A <= 8 ? 2 : 1) k_grover_regs(double2 *__restrict__ psi, uint64_t N, uint64_t k,
                                                                    int iters, double *__restrict__ trace,
                                                                    double4 *__restrict__ slots,
                                                                    unsigned *__restrict__ tags)
@@ -218,9 +218,14 @@ __global__ void __launch_bounds__(kRegsThreads, A <= 4 ? 4 : A <= 8 ? 2 : 1) k_g
     const unsigned nb = gridDim.x;
     const uint64_t chunk = (uint64_t)A * blockDim.x;
     const uint64_t base = (uint64_t)blockIdx.x * chunk;
+    // slots of this thread inside the state (all A but in the last CTA)
+    const uint64_t first = base + threadIdx.x;
+    const uint64_t nv_all = first >= N ? 0 : (N - first + blockDim.x - 1) / blockDim.x;
+    const int nv = nv_all > (uint64_t)A ? A : (int)nv_all;
     double2 v[A];
 #pragma unroll
-    for (int j = 0; j < A; ++j) v[j] = psi[base + threadIdx.x + (uint64_t)j * blockDim.x];
+    for (int j = 0; j < A; ++j)   // ragged last CTA: slots past N hold 0, evolve harmlessly, are never stored
+        v[j] = j < nv ? psi[base + threadIdx.x + (uint64_t)j * blockDim.x] : make_double2(0.0, 0.0);
     // the owner of k: thread / register slot (static index via the unrolled loops)
     const bool own_k = k >= base && k < base + chunk;
     const uint32_t kl = (uint32_t)(k - base);
@@ -232,6 +237,7 @@ __global__ void __launch_bounds__(kRegsThreads, A <= 4 ? 4 : A <= 8 ? 2 : 1) k_g
         double2 acc = make_double2(0.0, 0.0), ak = make_double2(0.0, 0.0);
 #pragma unroll
         for (int j = 0; j < A; ++j) {
+            if (j >= nv) break;   // ragged: slots past N are not amplitudes
             acc.x += v[j].x;
             acc.y += v[j].y;
             if (own_t && j == kj) ak = v[j];
@@ -319,8 +325,9 @@ __global__ void __launch_bounds__(kRegsThreads, A <= 4 ? 4 : A <= 8 ? 2 : 1) k_g
     }
 #pragma unroll
     for (int j = 0; j < A; ++j)
-        psi[base + threadIdx.x + (uint64_t)j * blockDim.x] =
-            CARRY && iters > 0 && own_t && j == kj ? make_double2(cur.z, cur.w) : v[j];
+        if (j < nv)
+            psi[base + threadIdx.x + (uint64_t)j * blockDim.x] =
+                CARRY && iters > 0 && own_t && j == kj ? make_double2(cur.z, cur.w) : v[j];
 }
 
 }  // namespace
@@ -359,33 +366,35 @@ static bool try_regs(Handle *h, uint64_t mark, int iters, double *d_trace)
     const uint64_t N = h->local_dim();
     // QSIM_GROVER_REDUCE: re-reduce the sum every iteration (measurement / cross-check knob)
     static const bool reduce = getenv("QSIM_GROVER_REDUCE") != nullptr;
-    auto pick = [&](uint64_t per) -> void * {
-        if (reduce)
-            return per <= 1 ? (void *)k_grover_regs<1, false> : per <= 2 ? (void *)k_grover_regs<2, false>
-                 : per <= 4 ? (void *)k_grover_regs<4, false> : per <= 8 ? (void *)k_grover_regs<8, false>
-                 : per <= 16 ? (void *)k_grover_regs<16, false> : (void *)k_grover_regs<32, false>;
-        return per <= 1 ? (void *)k_grover_regs<1, true> : per <= 2 ? (void *)k_grover_regs<2, true>
-             : per <= 4 ? (void *)k_grover_regs<4, true> : per <= 8 ? (void *)k_grover_regs<8, true>
-             : per <= 16 ? (void *)k_grover_regs<16, true> : (void *)k_grover_regs<32, true>;
-    };
-    uint64_t blocks = 1;
-    while (blocks * 2 <= (uint64_t)h->num_sms && blocks * 2 <= N / kRegsThreads) blocks *= 2;
-    if (!reduce) {
-        // no exchange after the first sum: spread the state thin (down to 4
-        // amplitudes per thread, several CTAs per SM) so the iterations' short
-        // dependent update chains interleave across many warps -- as far as
-        // every CTA stays co-resident (the first sum is a grid-wide exchange)
-        while (N / (blocks * 2 * kRegsThreads) >= 4) {
-            int ps = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, pick(N / (blocks * 2 * kRegsThreads)), kRegsThreads, 0);
-            if ((uint64_t)ps * h->num_sms < blocks * 2) break;
-            blocks *= 2;
+    // amplitudes per thread: the instantiated A >= per
+    static const int kA[] = {1, 2, 4, 8, 12, 16, 20, 24, 28, 32};
+    auto inst = [&](int A) -> void * {
+        switch (A) {
+        case 1: return reduce ? (void *)k_grover_regs<1, false> : (void *)k_grover_regs<1, true>;
+        case 2: return reduce ? (void *)k_grover_regs<2, false> : (void *)k_grover_regs<2, true>;
+        case 4: return reduce ? (void *)k_grover_regs<4, false> : (void *)k_grover_regs<4, true>;
+        case 8: return reduce ? (void *)k_grover_regs<8, false> : (void *)k_grover_regs<8, true>;
+        case 12: return reduce ? (void *)k_grover_regs<12, false> : (void *)k_grover_regs<12, true>;
+        case 16: return reduce ? (void *)k_grover_regs<16, false> : (void *)k_grover_regs<16, true>;
+        case 20: return reduce ? (void *)k_grover_regs<20, false> : (void *)k_grover_regs<20, true>;
+        case 24: return reduce ? (void *)k_grover_regs<24, false> : (void *)k_grover_regs<24, true>;
+        case 28: return reduce ? (void *)k_grover_regs<28, false> : (void *)k_grover_regs<28, true>;
+        default: return reduce ? (void *)k_grover_regs<32, false> : (void *)k_grover_regs<32, true>;
         }
-    }
-    const uint64_t per = N / (blocks * kRegsThreads);
-    if (per < 1 || per > 32 || N % (blocks * kRegsThreads)) return false;
+    };
+    // one CTA per SM (every CTA co-resident: the first sum is a grid-wide
+    // exchange), the state spread over all of them: the smallest instantiated
+    // A with A x 256 x SMs >= N, the last CTA ragged (n = 20: A = 28 over 147
+    // CTAs instead of 32 over 128 -- the FP64 update time per iteration is
+    // set by the busiest SM)
+    const uint64_t per_min = (N + (uint64_t)h->num_sms * kRegsThreads - 1) / ((uint64_t)h->num_sms * kRegsThreads);
+    int A = 0;
+    for (int a : kA)
+        if ((uint64_t)a >= per_min) { A = a; break; }
+    if (!A) return false;
+    const uint64_t blocks = (N + (uint64_t)A * kRegsThreads - 1) / ((uint64_t)A * kRegsThreads);
     int per_sm = 0;
-    void *fn = pick(per);
+    void *fn = inst(A);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kRegsThreads, 0);
     if (per_sm < 1 || blocks > (uint64_t)per_sm * h->num_sms) return false;
     // slots: 2 x blocks double4 (parity double buffer); tags[0]: the arrival counter
