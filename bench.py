@@ -296,7 +296,7 @@ def main():
     ap.add_argument("--ref-n", type=int, default=N_QUBITS)
     ap.add_argument("--cpu-n", type=int, default=N_QUBITS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=12)
+    ap.add_argument("--e2e-steps", type=int, default=24)
     ap.add_argument("--profile-only", action="store_true", help="warm-up + steps only (for ncu)")
     ap.add_argument("--config", type=int, default=2, choices=[2, 4],
                     help="2: the headline QFT (default); 4: the noisy brickwork, FP64 roofline (one GPU)")
