@@ -632,9 +632,97 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
     const int s0 = h0->n - lo - m;         // lowest position of the range (canonical)
     std::vector<int> wp(m);                // current position of wire w (same on every rank)
     for (int w = 0; w < m; ++w) wp[w] = h0->pos[lo + w];
+    // H on one GPU ("H passes"): the transform leaves every wire where it is, so the
+    // in-place passes had 128-byte rows on both sides for the top block and
+    // the lowest block stayed on the 12-bit kernel.  Instead every pass but
+    // the last writes its tile out of place to the lowest 13 positions (one
+    // contiguous run per tile) and parks the next block's wires on the top
+    // positions; the last pass puts every bit back.  The plan is simulated
+    // first; any pass it cannot give conflict-free landing reads and coalesced
+    // stores keeps the old in-place plan.
+    const int Gn = (int)gsize.size();
+    static const bool no_hflex = getenv("QSIM_NO_HFLEX") != nullptr;   // measurement knob
+    bool hflex = !qft && !gc && !dry && use13 && R.size() == 1 && h0->world == 1 && !no_hflex && Gn >= 2;
+    for (int a : gsize) hflex &= a >= 5 && a <= 10;
+    for (int w = 0; w < m && hflex; ++w) hflex &= wp[w] < nl;
+    std::vector<std::vector<int>> hf_tpos(Gn), hf_perm(Gn);
+    std::vector<int> hat(nl);              // hat[p]: the start position of the bit now at p
+    for (int p = 0; p < nl; ++p) hat[p] = p;
+    if (hflex) {
+        std::vector<int> blk_of(nl, -1);   // start position -> block of its wire
+        for (int g = 0, b0 = 0; g < Gn; b0 += gsize[g], ++g)
+            for (int u = 0; u < gsize[g]; ++u) blk_of[wp[b0 + u]] = g;
+        std::vector<int> swp(wp), shat(hat);
+        for (int g = 0, b0 = 0; g < Gn && hflex; b0 += gsize[g], ++g) {
+            const int a = gsize[g];
+            const bool last = g + 1 == Gn;
+            std::vector<char> is_act(nl, 0);
+            std::vector<int> act;
+            for (int u = 0; u < a; ++u) { act.push_back(swp[b0 + u]); is_act[swp[b0 + u]] = 1; }
+            std::vector<int> pas;
+            for (int p = 0; p < nl && (int)pas.size() < kTile13Bits - a; ++p)
+                if (!is_act[p]) pas.push_back(p);
+            std::vector<int> sorted(act);
+            sorted.insert(sorted.end(), pas.begin(), pas.end());
+            std::sort(sorted.begin(), sorted.end());
+            auto rank = [&](int p) { return (int)(std::lower_bound(sorted.begin(), sorted.end(), p) - sorted.begin()); };
+            // window 0 (tile bits 0..4): the 5 highest-ranked actives (a
+            // non-final pass), the 5 with the lowest final positions (the last
+            // pass: its stores then run over the lowest outputs from the lanes)
+            std::vector<int> ord(act);
+            if (last) std::sort(ord.begin(), ord.end(), [&](int x, int y) { return shat[x] < shat[y]; });
+            else std::sort(ord.begin(), ord.end(), [&](int x, int y) { return x > y; });
+            for (int i = 0; i < 5; ++i) hflex &= rank(ord[i]) >= 5;   // landing reads stay conflict-free
+            std::vector<int> tpos(ord);
+            tpos.insert(tpos.end(), pas.begin(), pas.end());
+            std::vector<int> perm(nl, -1);
+            if (last) {
+                for (int p = 0; p < nl; ++p) perm[p] = shat[p];
+            } else {
+                // outputs 0..12: [tile bits that stay thread bits in map 1, by
+                // final position] [window-1 bits] [later blocks' wires]; then the
+                // fixed bits, the next block last (lowest final position on top)
+                std::vector<char> in_t(nl, 0), in_w1(nl, 0);
+                for (int p : tpos) in_t[p] = 1;
+                for (int b = a - 5; b < a; ++b) in_w1[tpos[b]] = 1;
+                std::vector<int> s0, s1, s2, f0, f1;
+                for (int p : tpos) {
+                    if (blk_of[shat[p]] > g) s2.push_back(p);
+                    else if (in_w1[p]) s1.push_back(p);
+                    else s0.push_back(p);
+                }
+                for (int p = 0; p < nl; ++p)
+                    if (!in_t[p]) (blk_of[shat[p]] == g + 1 ? f1 : f0).push_back(p);
+                auto up = [&](int x, int y) { return shat[x] < shat[y]; };
+                auto down = [&](int x, int y) { return shat[x] > shat[y]; };
+                std::sort(s0.begin(), s0.end(), up);
+                std::sort(s1.begin(), s1.end(), up);
+                std::sort(s2.begin(), s2.end(), down);
+                // the final block's wires with the lowest final positions on
+                // top (they are that pass's window 0); an intermediate block
+                // keeps its order (tiles running at the same time then write
+                // neighbouring regions, as the QFT's block moves do)
+                if (g + 2 == Gn) std::sort(f1.begin(), f1.end(), down);
+                int q = 0;
+                for (int p : s0) perm[p] = q++;
+                hflex &= q >= 5;   // the lanes' output positions are not window bits
+                for (auto *v : {&s1, &s2, &f0, &f1})
+                    for (int p : *v) perm[p] = q++;
+            }
+            hf_tpos[g] = tpos;
+            hf_perm[g] = perm;
+            for (int w = 0; w < m; ++w) swp[w] = perm[swp[w]];
+            std::vector<int> nh(nl);
+            for (int p = 0; p < nl; ++p) nh[perm[p]] = shat[p];
+            shat = nh;
+        }
+        if (hflex && ensure_scratch(h0) != QSIM_OK) hflex = false;
+    }
+    bool hflex_off = false;                // a planned pass fell back: in place from there on
     int a0 = 0;
     for (int g = 0; g < (int)gsize.size(); ++g) {
         const int a = gsize[g];
+        const bool hf = hflex && !hflex_off;
         std::vector<int> act;
         for (int u = 0; u < a; ++u) act.push_back(lo + a0 + u);
         if (h0->world > 1) {
@@ -669,7 +757,7 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
         // them in the last register window: 512-byte runs per thread, one
         // 16-byte store per lane per run -- that pass stays on the 12-bit kernel
         bool low_block = false;
-        for (int u = 0; u < a; ++u) low_block |= !block_moves && wp[a0 + u] < kTile13Bits - a + 5;
+        for (int u = 0; u < a; ++u) low_block |= !block_moves && !hf && wp[a0 + u] < kTile13Bits - a + 5;
         if (use13 && a >= 5 && a <= 10 && !dry && !low_block) {
             // the 13-bit pass: active wires + the lowest 13 - a other positions
             std::vector<int> tpos;
@@ -677,6 +765,10 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
             for (int u = 0; u < a; ++u) { tpos.push_back(wp[a0 + u]); in13[wp[a0 + u]] = 1; }
             for (int p = 0; p < nl && (int)tpos.size() < kTile13Bits; ++p)
                 if (!in13[p]) { tpos.push_back(p); in13[p] = 1; }
+            if (hf) {   // the planned H pass (same tile, windows and output order chosen above)
+                tpos = hf_tpos[g];
+                perm13 = hf_perm[g];
+            }
             bool moved13 = false;
             for (int p = 0; p < nl; ++p) moved13 |= !in13[p] && perm13[p] != p;
             bool ok13 = true;
@@ -729,10 +821,16 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
             if (ok13) {
                 for (int w = 0; w < m; ++w)
                     if (wp[w] < nl) wp[w] = perm13[wp[w]];
+                if (hf) {
+                    std::vector<int> nh(nl);
+                    for (int p = 0; p < nl; ++p) nh[perm13[p]] = hat[p];
+                    hat = nh;
+                }
                 a0 += a;
                 continue;
             }
         }
+        if (hf) hflex_off = true;   // from here on in place on the current layout
         // tile: active wires (tile bits 0..a-1) + passive low positions
         std::vector<int> tile_pos;
         std::vector<char> in_tile(nl, 0);
@@ -814,6 +912,13 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
         for (int w = 0; w < m; ++w)
             if (wp[w] < nl) wp[w] = perm[wp[w]];
         a0 += a;
+    }
+    if (hflex) {
+        // a plan that fell back part-way: one permutation pass puts every bit back
+        std::vector<int> back(nl);
+        bool ident = true;
+        for (int p = 0; p < nl; ++p) { back[p] = hat[p]; ident &= hat[p] == p; }
+        if (!ident) permute_local(h0, back);
     }
     if (qft && !block_moves && !dry) {
         // closing swaps as a relabelling of the logical -> physical map (not in a

@@ -194,3 +194,39 @@ def test_rank_group_pass_off_matches_on():
         assert r.returncode == 0, r.stderr
         res.append(np.load(path))
     assert np.max(np.abs(res[0] - res[1])) < 1e-13
+
+
+@pytest.mark.parametrize("n,lo,m", [(26, 0, 26), (28, 0, 28), (24, 2, 20), (25, 0, 21), (27, 3, 24)])
+def test_hadamard_free_layouts(n, lo, m):
+    """H_m with free intermediate layouts (R42: every pass but the last writes
+    its tile contiguously, the last puts every bit back) against the oracle;
+    at n = 28 every pass is a 13-bit pass."""
+    got, ref, norm, prof = run(n, "had", lo, m, force=False)
+    assert np.max(np.abs(got - ref)) < TOL
+    assert abs(norm - 1) < 1e-12
+    if (n, lo, m) == (28, 0, 28):
+        assert set(prof) - {"_launches"} == {"k_qft13"}, prof.keys()
+
+
+def test_hadamard_free_layouts_off_matches_on_and_relabelled_start():
+    """QSIM_NO_HFLEX (in-place passes) and the free-layout plan agree, also
+    when the register starts in a relabelled layout (a QFT whose closing
+    swaps were a relabel: QSIM_NO_BLOCK_MOVES)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = (
+        "import sys, numpy as np; sys.path.insert(0, sys.argv[1]);"
+        "from paper_quant_ph_0201042_b200 import qsim as Q;"
+        "h = Q.qsim_create(26); Q.qsim_init_gaussian(h, 5); Q.qsim_qft(h, 0, 26, False);"
+        "Q.qsim_hadamard(h, 0, 26); Q.qsim_hadamard(h, 1, 22);"
+        "np.save(sys.argv[2], Q.qsim_get_state(h, 0, 1 << 26))")
+    outs = []
+    for env in ({}, {"QSIM_NO_HFLEX": "1"}, {"QSIM_NO_BLOCK_MOVES": "1"}):
+        path = f"/tmp/hflex_{len(outs)}.npy"
+        r = subprocess.run([sys.executable, "-c", script, root, path], env=dict(os.environ, **env),
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        outs.append(np.load(path))
+    assert np.max(np.abs(outs[0] - outs[1])) < 1e-13
+    assert np.max(np.abs(outs[0] - outs[2])) < 1e-13
