@@ -670,8 +670,18 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
             // non-final pass), the 5 with the lowest final positions (the last
             // pass: its stores then run over the lowest outputs from the lanes)
             std::vector<int> ord(act);
-            if (last) std::sort(ord.begin(), ord.end(), [&](int x, int y) { return shat[x] < shat[y]; });
-            else std::sort(ord.begin(), ord.end(), [&](int x, int y) { return x > y; });
+            if (last) {
+                std::sort(ord.begin(), ord.end(), [&](int x, int y) { return shat[x] < shat[y]; });
+                // the wire that ends on position 0 goes to window 1 (tile bit
+                // 5): the stores then move neighbouring pairs, 32 bytes each
+                if (a >= 6 && shat[ord[0]] == 0) {
+                    const int z = ord[0];
+                    ord.erase(ord.begin());
+                    ord.insert(ord.begin() + 5, z);
+                }
+            } else {
+                std::sort(ord.begin(), ord.end(), [&](int x, int y) { return x > y; });
+            }
             for (int i = 0; i < 5; ++i) hflex &= rank(ord[i]) >= 5;   // landing reads stay conflict-free
             std::vector<int> tpos(ord);
             tpos.insert(tpos.end(), pas.begin(), pas.end());
@@ -703,9 +713,12 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
                 // keeps its order (tiles running at the same time then write
                 // neighbouring regions, as the QFT's block moves do)
                 if (g + 2 == Gn) std::sort(f1.begin(), f1.end(), down);
+                // one window-1 bit on position 0 (neighbouring pairs per thread:
+                // 32-byte stores), the lanes on the next five positions
                 int q = 0;
+                if (!s1.empty()) { perm[s1[0]] = q++; s1.erase(s1.begin()); }
                 for (int p : s0) perm[p] = q++;
-                hflex &= q >= 5;   // the lanes' output positions are not window bits
+                hflex &= q >= 6;   // the lanes' output positions are not window bits
                 for (auto *v : {&s1, &s2, &f0, &f1})
                     for (int p : *v) perm[p] = q++;
             }

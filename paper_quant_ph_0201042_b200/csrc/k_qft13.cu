@@ -63,6 +63,7 @@ struct Q13 {
     int n_ef;                                 // early wires on tile-id bits (as erun)
     uint64_t y_const;
     int qe0, qe1;                             // ext-id bits of the quarter index (landing ranks 11, 12; -1: global)
+    int pb;                                   // window-1 bit whose output position is 0 (-1: none): 32-byte stores
     int in_first[5], in_len[5];               // tensor-map dim -> ext-id bit run
     // rank-group pass (the exchange fused into the pass, peer memory): ng
     // tile bits sit on rank bits -- the highest-ranked tile bits, i.e. the
@@ -91,6 +92,30 @@ __device__ __forceinline__ uint64_t ins_bit(uint64_t x, int e, uint64_t v)
 {
     const uint64_t lo = x & ((1ull << e) - 1);
     return ((x >> e) << (e + 1)) | (v << e) | lo;
+}
+
+// two adjacent amplitudes in one 256-bit streaming store (STG.E.ENL2.256)
+__device__ __forceinline__ void st_pair_cs(double2 *p, double2 a, double2 b)
+{
+    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y)
+                 : "memory");
+}
+
+// window-1 register slots k and k | 2^PB hold neighbouring output amplitudes
+// (window bit PB sits on output position 0): 16 stores of 32 bytes per thread
+template <int PB>
+__device__ __forceinline__ void store_pairs(double2 *__restrict__ out, uint64_t ib, const uint64_t (&pout)[5],
+                                            const double2 (&v)[32])
+{
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+        if (k & (1 << PB)) continue;
+        uint64_t o = ib;
+#pragma unroll
+        for (int b = 0; b < 5; ++b)
+            if (k & (1 << b)) o |= pout[b];
+        st_pair_cs(out + o, v[k], v[k | (1 << PB)]);
+    }
 }
 
 // 13-bit XOR swizzle (16-byte granules; linear over GF(2))
@@ -359,7 +384,15 @@ __global__ void __launch_bounds__(kThr, 1)
         uint64_t ib = tout;
         for (int e = 0; e < P.n_orun; ++e)
             ib |= ((T >> P.orun_src[e]) & ((1ull << P.orun_len[e]) - 1)) << P.orun_dst[e];
-        if (P.ng == 0) {
+        if (P.ng == 0 && P.pb >= 0) {
+            switch (P.pb) {
+            case 0: store_pairs<0>(out, ib, pout, v); break;
+            case 1: store_pairs<1>(out, ib, pout, v); break;
+            case 2: store_pairs<2>(out, ib, pout, v); break;
+            case 3: store_pairs<3>(out, ib, pout, v); break;
+            default: store_pairs<4>(out, ib, pout, v); break;
+            }
+        } else if (P.ng == 0) {
 #pragma unroll
             for (int k = 0; k < kNS; ++k) {
                 uint64_t o = ib;
@@ -487,6 +520,12 @@ bool launch_qft13(Handle *h, const Qft13Desc &d, const double2 *in, double2 *out
         runs(d.nfix, fidx.data(), d.fout_pos, P.n_orun, P.orun_src, P.orun_len, P.orun_dst);
     }
     P.y_const = d.y_const;
+    // a window-1 bit on output position 0: each thread holds neighbouring
+    // pairs, stored 32 bytes at a time (QSIM_NO_ST256: 16-byte stores)
+    static const bool no_st256 = getenv("QSIM_NO_ST256") != nullptr;   // measurement knob
+    P.pb = -1;
+    for (int b = 0; b < kWB && !no_st256 && d.ng == 0; ++b)
+        if (d.out_pos[d.a - kWB + b] == 0) P.pb = b;
     P.nfix = d.nfix;
     // quarter boxes: the 11 lowest-ranked tile bits form the box; the two
     // highest-ranked tile bits join the fixed positions as "ext-id" bits
