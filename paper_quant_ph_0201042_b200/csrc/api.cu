@@ -632,22 +632,28 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
     const int s0 = h0->n - lo - m;         // lowest position of the range (canonical)
     std::vector<int> wp(m);                // current position of wire w (same on every rank)
     for (int w = 0; w < m; ++w) wp[w] = h0->pos[lo + w];
-    // H on one GPU ("H passes"): the transform leaves every wire where it is, so the
-    // in-place passes had 128-byte rows on both sides for the top block and
-    // the lowest block stayed on the 12-bit kernel.  Instead every pass but
-    // the last writes its tile out of place to the lowest 13 positions (one
-    // contiguous run per tile) and parks the next block's wires on the top
-    // positions; the last pass puts every bit back.  The plan is simulated
-    // first; any pass it cannot give conflict-free landing reads and coalesced
-    // stores keeps the old in-place plan.
+    // Free intermediate layouts on one GPU ("H passes"): every
+    // pass but the last writes its tile out of place to the lowest 13
+    // positions (one contiguous run per tile) and parks the next block's wires
+    // on the top positions; the last pass puts every bit where it ends.  H
+    // (every wire ends where it started: the in-place passes had 128-byte rows
+    // on both sides for the top block, and the lowest block stayed on the
+    // 12-bit kernel) and the QFT of a sub-register above position 0 (its block
+    // moves wrote 128-byte rows, the passives being the other qubits).  The
+    // plan is simulated first; a plan whose passes cannot all have
+    // conflict-free landing reads and coalesced stores keeps the old one.
     const int Gn = (int)gsize.size();
     static const bool no_hflex = getenv("QSIM_NO_HFLEX") != nullptr;   // measurement knob
-    bool hflex = !qft && !gc && !dry && use13 && R.size() == 1 && h0->world == 1 && !no_hflex && Gn >= 2;
+    static const bool no_qflex = getenv("QSIM_NO_QFLEX") != nullptr;   // measurement knob
+    bool hflex = (qft ? block_moves && s0 > 0 && !no_qflex : !no_hflex) && !gc && !dry && use13 && R.size() == 1 &&
+                 h0->world == 1 && Gn >= 2;
     for (int a : gsize) hflex &= a >= 5 && a <= 10;
     for (int w = 0; w < m && hflex; ++w) hflex &= wp[w] < nl;
     std::vector<std::vector<int>> hf_tpos(Gn), hf_perm(Gn);
-    std::vector<int> hat(nl);              // hat[p]: the start position of the bit now at p
-    for (int p = 0; p < nl; ++p) hat[p] = p;
+    std::vector<int> hat(nl), fin_of(nl);  // hat[p]: start position of the bit now at p; fin_of: its end
+    for (int p = 0; p < nl; ++p) hat[p] = fin_of[p] = p;
+    if (hflex && qft)
+        for (int w = 0; w < m; ++w) fin_of[wp[w]] = s0 + w;   // the closing swaps, as the block moves
     if (hflex) {
         std::vector<int> blk_of(nl, -1);   // start position -> block of its wire
         for (int g = 0, b0 = 0; g < Gn; b0 += gsize[g], ++g)
@@ -656,6 +662,7 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
         for (int g = 0, b0 = 0; g < Gn && hflex; b0 += gsize[g], ++g) {
             const int a = gsize[g];
             const bool last = g + 1 == Gn;
+            auto fin = [&](int p) { return fin_of[shat[p]]; };
             std::vector<char> is_act(nl, 0);
             std::vector<int> act;
             for (int u = 0; u < a; ++u) { act.push_back(swp[b0 + u]); is_act[swp[b0 + u]] = 1; }
@@ -666,20 +673,21 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
             sorted.insert(sorted.end(), pas.begin(), pas.end());
             std::sort(sorted.begin(), sorted.end());
             auto rank = [&](int p) { return (int)(std::lower_bound(sorted.begin(), sorted.end(), p) - sorted.begin()); };
-            // window 0 (tile bits 0..4): the 5 highest-ranked actives (a
-            // non-final pass), the 5 with the lowest final positions (the last
-            // pass: its stores then run over the lowest outputs from the lanes)
+            // window 0 (tile bits 0..4).  The QFT: the block's first five wires
+            // (its phases fix the order).  H (any order): the 5 highest-ranked
+            // actives in a non-final pass, the 5 with the lowest final positions
+            // in the last one (its stores then run over the lowest outputs from
+            // the lanes), the wire that ends on position 0 in window 1
+            // (neighbouring pairs per thread: 32-byte stores)
             std::vector<int> ord(act);
-            if (last) {
-                std::sort(ord.begin(), ord.end(), [&](int x, int y) { return shat[x] < shat[y]; });
-                // the wire that ends on position 0 goes to window 1 (tile bit
-                // 5): the stores then move neighbouring pairs, 32 bytes each
-                if (a >= 6 && shat[ord[0]] == 0) {
+            if (!qft && last) {
+                std::sort(ord.begin(), ord.end(), [&](int x, int y) { return fin(x) < fin(y); });
+                if (a >= 6 && fin(ord[0]) == 0) {
                     const int z = ord[0];
                     ord.erase(ord.begin());
                     ord.insert(ord.begin() + 5, z);
                 }
-            } else {
+            } else if (!qft) {
                 std::sort(ord.begin(), ord.end(), [&](int x, int y) { return x > y; });
             }
             for (int i = 0; i < 5; ++i) hflex &= rank(ord[i]) >= 5;   // landing reads stay conflict-free
@@ -687,7 +695,13 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
             tpos.insert(tpos.end(), pas.begin(), pas.end());
             std::vector<int> perm(nl, -1);
             if (last) {
-                for (int p = 0; p < nl; ++p) perm[p] = shat[p];
+                for (int p = 0; p < nl; ++p) perm[p] = fin(p);
+                // the QFT: the last window's wires off the tile's five lowest
+                // output positions (those are the lanes' for coalesced stores)
+                std::vector<std::pair<int, int>> outs;   // (output position, window-1 bit?)
+                for (int b = 0; b < kTile13Bits; ++b) outs.push_back({perm[tpos[b]], b >= a - 5 && b < a});
+                std::sort(outs.begin(), outs.end());
+                for (int i = 0; i < 5 && qft; ++i) hflex &= !outs[i].second;
             } else {
                 // outputs 0..12: [tile bits that stay thread bits in map 1, by
                 // final position] [window-1 bits] [later blocks' wires]; then the
@@ -695,30 +709,28 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
                 std::vector<char> in_t(nl, 0), in_w1(nl, 0);
                 for (int p : tpos) in_t[p] = 1;
                 for (int b = a - 5; b < a; ++b) in_w1[tpos[b]] = 1;
-                std::vector<int> s0, s1, s2, f0, f1;
+                std::vector<int> s0v, s1, s2, f0, f1;
                 for (int p : tpos) {
                     if (blk_of[shat[p]] > g) s2.push_back(p);
                     else if (in_w1[p]) s1.push_back(p);
-                    else s0.push_back(p);
+                    else s0v.push_back(p);
                 }
                 for (int p = 0; p < nl; ++p)
                     if (!in_t[p]) (blk_of[shat[p]] == g + 1 ? f1 : f0).push_back(p);
-                auto up = [&](int x, int y) { return shat[x] < shat[y]; };
-                auto down = [&](int x, int y) { return shat[x] > shat[y]; };
-                std::sort(s0.begin(), s0.end(), up);
+                auto up = [&](int x, int y) { return fin(x) < fin(y); };
+                auto down = [&](int x, int y) { return fin(x) > fin(y); };
+                std::sort(s0v.begin(), s0v.end(), up);
                 std::sort(s1.begin(), s1.end(), up);
                 std::sort(s2.begin(), s2.end(), down);
-                // the final block's wires with the lowest final positions on
-                // top (they are that pass's window 0); an intermediate block
-                // keeps its order (tiles running at the same time then write
+                // H: the final block's wires with the lowest final positions on
+                // top (they are that pass's window 0); otherwise a block keeps
+                // its order (tiles running at the same time then write
                 // neighbouring regions, as the QFT's block moves do)
-                if (g + 2 == Gn) std::sort(f1.begin(), f1.end(), down);
-                // one window-1 bit on position 0 (neighbouring pairs per thread:
-                // 32-byte stores), the lanes on the next five positions
+                if (!qft && g + 2 == Gn) std::sort(f1.begin(), f1.end(), down);
                 int q = 0;
-                if (!s1.empty()) { perm[s1[0]] = q++; s1.erase(s1.begin()); }
-                for (int p : s0) perm[p] = q++;
-                hflex &= q >= 6;   // the lanes' output positions are not window bits
+                if (!qft && !s1.empty()) { perm[s1[0]] = q++; s1.erase(s1.begin()); }   // H: pair stores
+                for (int p : s0v) perm[p] = q++;
+                hflex &= q >= 5;   // the lanes' output positions are not window bits
                 for (auto *v : {&s1, &s2, &f0, &f1})
                     for (int p : *v) perm[p] = q++;
             }
@@ -762,7 +774,7 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
         // output permutation of the local positions (block moves)
         std::vector<int> perm13(nl);
         for (int p = 0; p < nl; ++p) perm13[p] = p;
-        if (block_moves) {
+        if (block_moves && !hflex) {
             for (int w = a0 + a; w < m; ++w) perm13[wp[w]] = wp[w] + a;
             for (int u = 0; u < a; ++u) perm13[wp[a0 + u]] = s0 + a0 + u;
         }
@@ -857,7 +869,7 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
         // output permutation of the local positions
         std::vector<int> perm(nl);
         for (int p = 0; p < nl; ++p) perm[p] = p;
-        if (block_moves) {
+        if (block_moves && !hflex) {
             for (int w = a0 + a; w < m; ++w) perm[wp[w]] = wp[w] + a;   // rest block moves up
             for (int u = 0; u < a; ++u) perm[wp[a0 + u]] = s0 + a0 + u;  // block to final spots
         }
@@ -930,7 +942,7 @@ int fused_range(const Ranks &R, int lo, int m, int qft, int inverse, const GenCi
         // a plan that fell back part-way: one permutation pass puts every bit back
         std::vector<int> back(nl);
         bool ident = true;
-        for (int p = 0; p < nl; ++p) { back[p] = hat[p]; ident &= hat[p] == p; }
+        for (int p = 0; p < nl; ++p) { back[p] = fin_of[hat[p]]; ident &= back[p] == p; }
         if (!ident) permute_local(h0, back);
     }
     if (qft && !block_moves && !dry) {

@@ -230,3 +230,29 @@ def test_hadamard_free_layouts_off_matches_on_and_relabelled_start():
         outs.append(np.load(path))
     assert np.max(np.abs(outs[0] - outs[1])) < 1e-13
     assert np.max(np.abs(outs[0] - outs[2])) < 1e-13
+
+
+@pytest.mark.parametrize("n,lo,m,inverse", [(24, 0, 20, True), (26, 2, 20, False), (25, 1, 17, True), (23, 0, 18, False)])
+def test_qft_sub_register_free_layouts(n, lo, m, inverse):
+    """The QFT of a sub-register above position 0 (configs[3]'s inverse QFT on
+    the exponent register) with free intermediate layouts against the oracle's
+    circuit, and against the block-move plan (QSIM_NO_QFLEX) in a subprocess."""
+    got, ref, norm, prof = run(n, "qft", lo, m, inverse, force=False)
+    assert np.max(np.abs(got - ref)) < TOL
+    assert abs(norm - 1) < 1e-12
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = (
+        "import sys, numpy as np; sys.path.insert(0, sys.argv[1]);"
+        "from paper_quant_ph_0201042_b200 import qsim as Q;"
+        f"h = Q.qsim_create({n}); Q.qsim_init_gaussian(h, 9); Q.qsim_qft(h, {lo}, {m}, {inverse});"
+        f"np.save(sys.argv[2], Q.qsim_get_state(h, 0, 1 << {n}))")
+    outs = []
+    for env in ({}, {"QSIM_NO_QFLEX": "1"}):
+        path = f"/tmp/qflex_{len(outs)}.npy"
+        r = subprocess.run([sys.executable, "-c", script, root, path], env=dict(os.environ, **env),
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        outs.append(np.load(path))
+    assert np.max(np.abs(outs[0] - outs[1])) < 1e-13
