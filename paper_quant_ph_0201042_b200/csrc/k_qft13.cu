@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -446,6 +447,11 @@ bool launch_qft13(Handle *h, const Qft13Desc &d, const double2 *in, double2 *out
 {
     cudaSetDevice(h->device);   // members of a rank group may live on different devices
     if (d.a < kWB || d.a > 10 || h->nl < kTB + 2 || getenv("QSIM_NO_TMA")) return false;
+    // test hook: decline the k-th 13-bit pass of the process (exercises the
+    // callers' fall-back paths, e.g. a free-layout plan that fails part-way)
+    static const int fail_at = getenv("QSIM_TEST_Q13_DECLINE") ? atoi(getenv("QSIM_TEST_Q13_DECLINE")) : -1;
+    static int calls = 0;
+    if (fail_at >= 0 && calls++ == fail_at) return false;
     Q13 P;
     std::memset(&P, 0, sizeof P);
     P.a = d.a;

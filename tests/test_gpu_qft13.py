@@ -256,3 +256,42 @@ def test_qft_sub_register_free_layouts(n, lo, m, inverse):
         assert r.returncode == 0, r.stderr
         outs.append(np.load(path))
     assert np.max(np.abs(outs[0] - outs[1])) < 1e-13
+
+
+@pytest.mark.parametrize("op,n,lo,m,decline", [("had", 26, 0, 26, 1), ("had", 26, 0, 26, 2), ("qft", 25, 0, 20, 1)])
+def test_free_layout_plan_falls_back_part_way(op, n, lo, m, decline):
+    """A free-layout plan whose k-th 13-bit pass is declined (test hook
+    QSIM_TEST_Q13_DECLINE) finishes in place on the current layout and puts
+    every bit back with one permutation pass: the result still equals the
+    oracle."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    call = f"Q.qsim_hadamard(h, {lo}, {m})" if op == "had" else f"Q.qsim_qft(h, {lo}, {m}, True)"
+    script = (
+        "import sys, numpy as np; sys.path.insert(0, sys.argv[1]);"
+        "from paper_quant_ph_0201042_b200 import qsim as Q;"
+        f"h = Q.qsim_create({n}); Q.qsim_init_gaussian(h, 4); Q.qsim_profile(h, True); {call};"
+        "print(sorted(k for k in Q.qsim_profile_json(h) if not k.startswith('_')));"
+        f"np.save(sys.argv[2], Q.qsim_get_state(h, 0, 1 << {n}))")
+    path = "/tmp/decline.npy"
+    r = subprocess.run([sys.executable, "-c", script, root, path],
+                       env=dict(os.environ, QSIM_TEST_Q13_DECLINE=str(decline)),
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    got = np.load(path)
+    import ast
+    kernels = ast.literal_eval(r.stdout.strip().splitlines()[-1])
+    assert "k_qft13" in kernels and len(kernels) > 1, kernels   # the fall-back pass / restore ran
+    h = Q.qsim_create(n)
+    try:
+        Q.qsim_init_gaussian(h, 4)
+        psi = Q.qsim_get_state(h, 0, 1 << n)
+    finally:
+        Q.qsim_destroy(h)
+    ref = psi.copy()
+    if op == "had":
+        O.hadamard_range(ref, lo, m)
+    else:
+        O.qft(ref, lo, m, True)
+    assert np.max(np.abs(got - ref)) < TOL, r.stdout
